@@ -1,0 +1,400 @@
+#!/usr/bin/env python
+"""Benchmark of the compressed view-factor hot path on B200.
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+the spherical-cap crater (d/D = 0.2) inset in a square plain of side 4D,
+~19,200 facets, F-hat built at tol 1e-5 (FP64, or FP32 with --dtype f32),
+64 sun directions at 5 deg elevation as one batched right-hand side.
+One STEP = one vf_solve_thermal call on the 64-column batch: every §8(a)
+row of the hot path (permute-in, low-rank phase 1, row-owner accumulate
+with the fused Jacobi epilogue, convergence, radiosity -> IR chaining and
+the temperature epilogue), i.e. (iters1 + iters2) F-hat applies.
+
+metric value = RHS-column applies per second = sum over ranks of
+64 * (iters1 + iters2) per step / step time (max over ranks).
+Multi-GPU (torchrun): every rank solves its own batch of 64 suns (azimuths
+offset per rank), no data-path collective: weak scaling.
+
+--impl reference runs the FP64 CPU oracle (oracle/, the reference arm for
+this tier) on a bounded sample of the same workload on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "compressed F·X apply: RHS-columns/sec and HBM GB/s (% of roofline) at 1/2/4/8 GPUs"
+UNIT = "RHS-column applies/s"
+NRHS = 64
+TOL_BUILD = 1e-5
+TOL_SOLVE = {"f64": 1e-10, "f32": 1e-6}
+ALBEDO, EMISS = 0.12, 0.95
+S_SUN = 1365.0
+ELEV = 5.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def fp64_peak_tflops(sm_mhz):
+    # B200: 148 SMs x 64 FP64 FMA/clk/SM x 2 flop
+    return 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
+
+
+def fp32_peak_tflops(sm_mhz):
+    return 148 * 128 * 2 * sm_mhz * 1e6 / 1e12
+
+
+class Clocks:
+    """Samples nvidia-smi during the timed region (the recipe's clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.p = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                       "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.p = None
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        try:
+            self.p.wait(2)
+        except Exception:
+            self.p.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def workload(rank, world):
+    import scenegen as sg
+    V, F = sg.cfg2_mesh()
+    phase = 2 * math.pi / NRHS * rank / max(world, 1)
+    suns = sg.sun_dirs(ELEV, NRHS, phase)
+    return V, F, suns
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ----------------------------------------------------------- oracle (CPU) arm
+
+def oracle_sample(V, F, suns, ncols, budget_s):
+    """The oracle as it stands: exact CSR F (eq. FF-def) + FP64 thermal Jacobi
+    solve on `ncols` of the sun columns; repeated until ~budget_s of work."""
+    import oracle
+    S = oracle.Scene(V, F)
+    csr = S.F_csr_rows()
+    Q = S.insolation(suns[:ncols], S_SUN)
+    alb, emi = np.full(S.N, ALBEDO), np.full(S.N, EMISS)
+    applies, t = 0, 0.0
+    reps = 0
+    while t < budget_s and reps < 50:
+        t0 = time.perf_counter()
+        out = oracle.thermal(lambda X: oracle.apply_csr(csr, X), Q, alb, emi, TOL_SOLVE["f64"], 100)
+        t += time.perf_counter() - t0
+        applies += ncols * (out["it1"] + out["it2"])
+        reps += 1
+    return applies / t, t, reps, out
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    V, F, suns = workload(0, 1)
+    import oracle
+    oracle.build()
+    ncols = 8
+    S = None
+    times, applies = [], 0
+    import oracle as O
+    S = O.Scene(V, F)
+    csr = S.F_csr_rows()
+    Q = S.insolation(suns[:ncols], S_SUN)
+    alb, emi = np.full(S.N, ALBEDO), np.full(S.N, EMISS)
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        out = O.thermal(lambda X: O.apply_csr(csr, X), Q, alb, emi, TOL_SOLVE["f64"], 100)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+            applies += ncols * (out["it1"] + out["it2"])
+    tot = sum(times)
+    v = applies / tot
+    sample = f"oracle thermal solve (exact CSR F, FP64, OpenMP) on {ncols} of the 64 sun columns per step"
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_block(S.N, "f64"),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+                             "sample": sample, "cpu": cpu_model()},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_block(N, dtype, extra=None):
+    c = {"workload": "BASELINE configs[1]: cap crater (R=1, d/D=0.2) in a 4D square plain, "
+                     f"{N} facets, 64 suns at {ELEV} deg elevation (batched RHS), F-hat tol {TOL_BUILD:g}, "
+                     f"{dtype.upper()} thermal equilibrium solve (radiosity + IR Jacobi, tol {TOL_SOLVE[dtype]:g})",
+         "N": N, "nrhs": NRHS, "tol_build": TOL_BUILD, "tol_solve": TOL_SOLVE[dtype],
+         "l2": "flushed between timed steps (256 MiB write, outside the step events)"}
+    if extra:
+        c.update(extra)
+    return c
+
+
+# ----------------------------------------------------------- GPU arm
+
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import paper_2209_07632_b200 as vf
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dt = args.dtype
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    V, F, suns = workload(rank, world)
+    M = vf.ViewFactorMatrix.build(V, F, TOL_BUILD, dtype=vf.VF_F64 if dt == "f64" else vf.VF_F32, device=local_rank)
+    info = M.refresh()
+    N = info["N"]
+    stream = torch.cuda.current_stream(dev)
+    M.set_stream(stream.cuda_stream)
+    Qdir_h = M.insolation(suns, S_SUN).astype(np.float64 if dt == "f64" else np.float32, order="F")
+    alb_h = np.full(N, ALBEDO, dtype=Qdir_h.dtype)
+    emi_h = np.full(N, EMISS, dtype=Qdir_h.dtype)
+
+    def colmajor(a):
+        return torch.from_numpy(np.ascontiguousarray(a.T)).to(dev).T
+
+    Qdir, alb, emi = colmajor(Qdir_h), torch.from_numpy(alb_h).to(dev), torch.from_numpy(emi_h).to(dev)
+    T = torch.empty((NRHS, N), dtype=tdt, device=dev).T
+    Qv = torch.empty((NRHS, N), dtype=tdt, device=dev).T
+    Qi = torch.empty((NRHS, N), dtype=tdt, device=dev).T
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    tol = TOL_SOLVE[dt]
+
+    def step():
+        M.solve_thermal(Qdir, alb, emi, T, Qv, Qi, iters=200, tol=tol)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    vf.vf_enable_kernel_timing(M.h, True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = Clocks(local_rank)
+    ms2 = 0.0
+    l2 = 0
+    ms1 = 0.0
+    l1 = 0
+    launches = 0
+    applies = 0
+    its = []
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)                      # L2 flush outside the step events
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+        st = M.stats()
+        kt = vf.vf_kernel_timing(M.h)
+        ms2 += kt["ms_phase2"]; l2 += kt["launches_phase2"]
+        ms1 += kt["ms_phase1"]; l1 += kt["launches_phase1"]
+        launches += kt["launches_total"]
+        applies += NRHS * (st["iters1"] + st["iters2"])
+        its.append((st["iters1"], st["iters2"]))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    vf.vf_enable_kernel_timing(M.h, False)
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    # max over ranks of time, sum of work
+    tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    wk = torch.tensor([float(applies)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.all_reduce(wk, op=dist.ReduceOp.SUM)
+    t_max = tt.item()
+    value = wk.item() / (t_max / 1e3)
+
+    # e2e: the same call with HOST buffers (pinned), H2D/D2H inside the timed region
+    Qdir_p = torch.from_numpy(np.ascontiguousarray(Qdir_h.T)).pin_memory().T
+    alb_p = torch.from_numpy(alb_h).pin_memory()
+    emi_p = torch.from_numpy(emi_h).pin_memory()
+    T_p = torch.empty((NRHS, N), dtype=tdt).pin_memory().T
+    Qv_p = torch.empty((NRHS, N), dtype=tdt).pin_memory().T
+    Qi_p = torch.empty((NRHS, N), dtype=tdt).pin_memory().T
+    ke = max(5, min(args.steps, 30))
+    M.solve_thermal(Qdir_p, alb_p, emi_p, T_p, Qv_p, Qi_p, iters=200, tol=tol)
+    e_ms, e_app = 0.0, 0
+    if dist:
+        dist.barrier()
+    for i in range(ke):
+        flush.fill_(i & 0xFF)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        M.solve_thermal(Qdir_p, alb_p, emi_p, T_p, Qv_p, Qi_p, iters=200, tol=tol)
+        e1.record(stream)
+        e1.synchronize()
+        e_ms += e0.elapsed_time(e1)
+        st = M.stats()
+        e_app += NRHS * (st["iters1"] + st["iters2"])
+    et = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+    ew = torch.tensor([float(e_app)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        dist.all_reduce(ew, op=dist.ReduceOp.SUM)
+    e2e_value = ew.item() / (et.item() / 1e3)
+    w = 8 if dt == "f64" else 4
+    h2d = N * NRHS * w + 2 * N * w
+    d2h = 3 * N * NRHS * w
+
+    if rank == 0:
+        pk, pk_kind = peaks()
+        # dominant kernel: phase 2 (row-owner accumulate + fused epilogue)
+        avg2 = ms2 / max(l2, 1)
+        avg1 = ms1 / max(l1, 1)
+        kp = NRHS
+        bytes2 = info["p2_bytes"] + info["p2_src_rows"] * kp * w + info["active_rows"] * kp * w * 4
+        flops2 = info["p2_flops_per_col"] * kp
+        smax = pk.get("sm_max_mhz", 1965.0)
+        peak_tf = fp64_peak_tflops(smax) if dt == "f64" else fp32_peak_tflops(smax)
+        ach_tf = flops2 / (avg2 * 1e-3) / 1e12 if avg2 > 0 else 0.0
+        ach_gbs = bytes2 / (avg2 * 1e-3) / 1e9 if avg2 > 0 else 0.0
+        share2 = ms2 / t_ms if t_ms > 0 else 0.0
+        roof = {"bound": "alu", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": ach_tf / peak_tf if peak_tf else None, "traffic": None,
+                "kernel": f"segrow_kernel<{'double' if dt == 'f64' else 'float'},16,4,M_SOLVE> (phase 2: "
+                          "row-owner accumulate + fused Jacobi epilogue)",
+                "peak_basis": f"derived: 148 SM x {64 if dt == 'f64' else 128} {dt.upper()} FMA/clk x 2 x "
+                              f"{smax:.0f} MHz (sm_max, {pk_kind} MEASURED_PEAKS.json)",
+                "avg_launch_ms": avg2, "launches": l2, "flops_per_launch": flops2,
+                "alg_bytes_per_launch": bytes2, "achieved_hbm_gbs": ach_gbs,
+                "hbm_peak_gbs": pk.get("hbm_gbs"), "hbm_frac": ach_gbs / pk.get("hbm_gbs", 6556.8),
+                "share_of_step": share2,
+                "phase1": {"avg_launch_ms": avg1, "launches": l1,
+                           "flops_per_launch": info["p1_flops_per_col"] * kp}}
+        # CPU baseline: the oracle as it stands on a bounded sample
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            try:
+                import oracle
+                oracle.build()
+                v_cpu, t_cpu, reps, _ = oracle_sample(V, F, suns, 8, args.cpu_budget)
+                cpu = {"value": v_cpu, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+                       "sample": f"oracle thermal solve (exact CSR F from eq. FF-def, FP64, OpenMP) on 8 of the "
+                                 f"64 sun columns, {reps} repetitions, {t_cpu:.1f} s", "cpu": cpu_model()}
+            except Exception as e:  # noqa
+                cpu = {"value": None, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+                       "sample": f"failed: {e}"}
+        it_arr = np.array(its)
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
+                "config": config_block(N, dt, {
+                    "iters_radiosity": int(np.median(it_arr[:, 0])), "iters_ir": int(np.median(it_arr[:, 1])),
+                    "solve_columns_per_s": NRHS * world * args.steps / (t_max / 1e3),
+                    "fhat_alg_bytes": info["alg_bytes"], "fhat_device_bytes": info["device_bytes"],
+                    "blocks": {"dense": info["n_dense"], "csr": info["n_csr"], "svd": info["n_svd"]},
+                    "active_rows": info["active_rows"], "sum_rank": info["sum_rank"],
+                    "build_seconds": info["build_seconds"], "parallelism": f"cols{world}"}),
+                "roofline": roof, "cpu_baseline": cpu,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "gpu_launches": launches, "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local_rank = int(os.environ.get("LOCAL_RANK", 0))
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    run_gpu(args, rank, world, local_rank)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,222 @@
+/*
+ * vf.h -- C ABI of libvf, the B200 (sm_100a) compressed view-factor library.
+ *
+ * The operation (PAPER.md = "P:<line>", arXiv 2209.07632):
+ *   F is the N x N view-factor matrix of a triangle mesh,
+ *     F_ij = [n_i.(x_j - x_i)][n_j.(x_i - x_j)] V_ij A_j / (pi |x_i - x_j|^4),
+ *   F_ii = 0                                   (eq. FF-def)
+ *   with V_ij the culled, ray-cast visibility   (§3.2).
+ *   F-hat is its hierarchical compression: a quadtree permutation (Alg. 2,
+ *   P:198-213) and a dynamic-programming choice per block pair of
+ *   Zero / CSR / dense / truncated-SVD U S V^T / subdivided (Alg. 3-4,
+ *   P:219-256).  The hot path applies F-hat to many right-hand sides
+ *   (Alg. 5) and iterates the Jacobi solves built on it
+ *   (eq. radiosity-system).
+ *
+ * Conventions (all calls):
+ *   - Every call returns an int status (vf_status); no exceptions cross the
+ *     ABI.  vf_last_error() returns a thread-local message for the last
+ *     failure on this thread.
+ *   - Vectors are COLUMN-MAJOR N x nrhs with leading dimension N, in the
+ *     caller's facet order (facet f = face f of the mesh).  Per-facet
+ *     parameters (rho, albedo, emissivity) are length-N vectors shared by all
+ *     columns.  Element type = the handle's dtype (VF_F64 -> double,
+ *     VF_F32 -> float) unless stated otherwise.
+ *   - Vector arguments may be DEVICE pointers (on the handle's device) or
+ *     HOST pointers (pageable or pinned); the library detects which with
+ *     cudaPointerGetAttributes and, for host pointers, stages through
+ *     handle-owned device buffers inside the call.  The caller owns every
+ *     vector; the library keeps no reference after the call returns.
+ *   - Stream ordering: work is enqueued on the handle's stream
+ *     (vf_set_stream; default: the legacy default stream).  vf_matvec with
+ *     device pointers is asynchronous; solves synchronise the stream to test
+ *     convergence and return when finished.
+ *   - X must not alias Y.  B / T / Qvis / Qir are outputs only.
+ *   - Scratch: the handle owns all device scratch, grown to the largest
+ *     nrhs seen.  A handle is not thread-safe: one call at a time.
+ *   - No CPU fallback: every apply/solve runs in the CUDA kernels of this
+ *     library; without a usable sm_100 device those calls fail with
+ *     VF_ENODEV.
+ */
+#ifndef VF_H_
+#define VF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct vf_handle_s* vf_handle;
+
+typedef enum {
+    VF_OK = 0,
+    VF_EINVAL = -1,        /* bad argument (null pointer, size, dtype, ...)          */
+    VF_ENOMEM = -2,        /* host or device allocation failed                        */
+    VF_ECUDA = -3,         /* a CUDA runtime call or kernel failed                    */
+    VF_ENOCONV = -4,       /* solve hit `iters` before `tol`; outputs hold last iterate */
+    VF_EIO = -5,           /* file open/read/write failed or bad HVFM container       */
+    VF_ENCCL = -6,         /* reserved for the multi-GPU row-sharded mode             */
+    VF_EUNSUPPORTED = -7,  /* valid request this build does not implement             */
+    VF_ENODEV = -8         /* no usable CUDA device / handle has no device copy       */
+} vf_status;
+
+enum { VF_F64 = 1, VF_F32 = 2 };                 /* storage + arithmetic dtype     */
+enum { VF_VIS_RAYCAST = 0, VF_VIS_CULL_ONLY = 1 };  /* V_ij: culling + ray cast, or
+                                                      culling only (tests)  */
+
+/* Triangle mesh, HOST arrays borrowed for the duration of the call.
+ * V: nv x 3 row-major vertex coordinates (metres); F: nf x 3 row-major
+ * 0-based vertex indices.  Facet data follows P:129: x_i = centroid,
+ * A_i = area, n_i = unit normal (right-hand rule, flipped to n_z > 0 when
+ * opts.orient_up, the height-field convention).  Zero-area faces -> VF_EINVAL. */
+typedef struct {
+    int64_t nv, nf;
+    const double* V;
+    const int32_t* F;
+} vf_mesh;
+
+typedef struct {
+    int dtype;           /* VF_F64 (default) or VF_F32: factor/value + vector type  */
+    int max_depth;       /* quadtree depth cap (Alg. 2 reading A3), default 16       */
+    int min_leaf;        /* quadtree leaf size (A3), default 16                       */
+    int64_t min_block;   /* |I||J| below which a block is CSR or dense (Alg. 4 step 2,
+                            reading A4), default 16384                               */
+    int k0;              /* initial rank guess of Alg. 3, default 8           */
+    int visibility;      /* VF_VIS_RAYCAST (default) or VF_VIS_CULL_ONLY               */
+    int orient_up;       /* 1 (default): n_z > 0; 0: keep right-hand-rule normals     */
+    int device;          /* CUDA device to upload to; -1 = host-only handle (build,
+                            save, info work; apply/solve return VF_ENODEV)            */
+    int threads;         /* host threads for the build (0 = all cores)               */
+    uint64_t seed;       /* seed of the randomized truncated SVD (default 0x5eed)      */
+} vf_build_opts;
+
+/* Fill *opts with the defaults above. */
+void vf_default_opts(vf_build_opts* opts);
+
+/* Assemble F-hat for a mesh with compression tolerance tol (eps of Alg. 3,
+ * relative to each block's sigma_1).  Host-side, untimed: facet data,
+ * BVH visibility (Alg. 1), quadtree (Alg. 2), rank estimation (Alg. 3) and
+ * DP assembly (Alg. 4), then flattening and upload to opts->device.
+ * opts may be NULL (defaults).  On success *out owns everything. */
+int vf_build(const vf_mesh* mesh, double tol, const vf_build_opts* opts, vf_handle* out);
+
+/* Same from explicit facet data (HOST, borrowed): x, n: N x 3 row-major
+ * centroids and unit normals, A: N areas.  Visibility is culling only when
+ * occluders == NULL or opts->visibility == VF_VIS_CULL_ONLY; otherwise the
+ * occluder triangles are ray-cast (facet f is NOT excluded from its own ray
+ * unless occluders->nf == N and face f is facet f).  Test hook for
+ * sphere-exact facet data (pins P1/P4). */
+int vf_build_facets(int64_t N, const double* x, const double* n, const double* A,
+                    const vf_mesh* occluders, double tol, const vf_build_opts* opts,
+                    vf_handle* out);
+
+/* Load an HVFM container (format below) and upload it to `device` (-1: host
+ * only).  Values are applied exactly as stored. */
+int vf_load(const char* path, int device, vf_handle* out);
+
+/* Write the handle's F-hat as an HVFM container. */
+int vf_save(vf_handle h, const char* path);
+
+/* Upload a host-only handle (device == -1 at build/load) to `device`. */
+int vf_upload(vf_handle h, int device);
+
+/* Release the handle, its host metadata and device memory.  NULL is OK. */
+int vf_free(vf_handle h);
+
+/* Order all subsequent work on `stream` (a cudaStream_t, e.g.
+ * torch.cuda.current_stream().cuda_stream).  NULL = legacy default stream. */
+int vf_set_stream(vf_handle h, void* stream);
+
+/* Y = F-hat X (Alg. 5), overwrite, no clamping (reading A12).  X, Y: N x nrhs. */
+int vf_matvec(vf_handle h, const void* X, void* Y, int nrhs);
+
+/* Jacobi solve of B = E + diag(rho) F-hat B (eq. radiosity-system):
+ * B_0 = E; Q_k = F-hat B_k, clamped to >= 0 when clamp != 0;
+ * B_{k+1} = E + rho * Q_k; per-column r_k = ||B_{k+1}-B_k||_2 / ||E||_2
+ * (||E|| = 0 -> 0).  Stops when all columns have r_k <= tol, or after `iters`
+ * iterations (-> VF_ENOCONV, B = last iterate).  E, B: N x nrhs; rho: N. */
+int vf_solve_radiosity(vf_handle h, const void* E, const void* rho, void* B,
+                       int nrhs, int iters, double tol, int clamp);
+
+/* Equilibrium temperature (eq. 3d-equilbr):
+ *   stage 1: the radiosity solve with rho = albedo, E = albedo * Qdir;
+ *            Qrefl = the last clamped Q;  Qvis = Qdir + Qrefl;
+ *   stage 2: rho = 1, E = (1 - albedo) * Qvis; Qir = the last clamped Q
+ *            (eq. time-indep-system-2 with H = 0);
+ *   T = (((1 - albedo) Qvis + emiss Qir) / (emiss sigma))^(1/4).
+ * Qdir, T, Qvis, Qir: N x nrhs (Qvis/Qir may be NULL); albedo, emiss: N. */
+int vf_solve_thermal(vf_handle h, const void* Qdir, const void* albedo, const void* emiss,
+                     void* T, void* Qvis, void* Qir, int nrhs, int iters, double tol);
+
+/* Iteration counts and max-over-columns final residuals of the last solve
+ * (stage 2 values are 0 after a radiosity solve).  Any pointer may be NULL. */
+int vf_last_solve_stats(vf_handle h, int* iters1, double* resid1, int* iters2, double* resid2);
+
+/* Direct insolation (P:76-80 eq. insolation) with R_sun = 1 AU:
+ * Q_if = S max(0, n_i.s_f) V_sun(x_i, s_f).  suns: k x 3 unit vectors (HOST);
+ * Qdir: N x k column-major HOST double output.  Needs a mesh-built handle. */
+int vf_insolation(vf_handle h, const double* suns, int k, double S, double* Qdir);
+
+typedef struct {
+    int64_t N;             /* facets                                               */
+    int dtype;             /* VF_F64 / VF_F32                                      */
+    double tol;
+    int64_t n_dense, n_csr, n_svd;        /* leaf counts by kind                    */
+    int64_t bytes_dense, bytes_csr, bytes_svd;  /* A7/A8 accounting per kind          */
+    int64_t nnz_csr;       /* stored CSR nonzeros                                  */
+    int64_t sum_rank;      /* sum of q over SVD blocks                              */
+    int64_t max_rank;
+    int64_t active_rows;   /* rows of F-hat with any stored entry                    */
+    int64_t device_bytes;  /* bytes of the device layout of F-hat (values, indices,
+                              segment descriptors, permutation)                      */
+    int64_t alg_bytes;     /* algorithmic bytes per apply, excluding X/Y traffic:
+                              values + CSR column indices + SVD row indices          */
+    int64_t alg_flops_per_col; /* 2 (sum q(mu+nv) + nnz + sum mn) + sum q            */
+    int64_t visible_pairs; /* nonzeros of the exact F seen during the build (0 if loaded) */
+    double build_seconds;
+    int device;            /* -1 = host only                                       */
+    /* device-layout accounting of the two apply phases (0 for host-only handles) */
+    int64_t t_rows;        /* rank-1 terms = rows of T (sum of q)                   */
+    int64_t p1_bytes;      /* phase 1 payload: V values + V row indices + S          */
+    int64_t p2_bytes;      /* phase 2 payload: dense/U/CSR values + CSR indices      */
+    int64_t p1_src_rows;   /* distinct X rows phase 1 reads                          */
+    int64_t p2_src_rows;   /* distinct X/T rows phase 2 reads                        */
+    int64_t p1_flops_per_col, p2_flops_per_col;
+} vf_info_t;
+
+int vf_info(vf_handle h, vf_info_t* out);
+
+/* Per-launch timing of the dominant kernel of the last apply/solve, measured
+ * with CUDA events on the handle's stream when enabled (0/1).  *ms is the
+ * summed duration of the row-owner accumulate kernel (phase 2) over the last
+ * call, *launches its launch count. */
+int vf_enable_kernel_timing(vf_handle h, int on);
+int vf_kernel_timing(vf_handle h, double* ms_phase2, int* launches_phase2,
+                     double* ms_phase1, int* launches_phase1, int* launches_total);
+
+const char* vf_last_error(void);
+
+/*
+ * HVFM v1 container (little-endian), written by vf_save and oracle/hmatrix.py:
+ *   char  magic[4] = "HVFM"; u32 version = 1; u32 dtype (1 f64, 2 f32); u32 0;
+ *   i64   N; f64 tol; i64 nleaves;
+ *   i32   perm[N]              tree position r holds caller facet perm[r]
+ *   then nleaves leaves in Alg. 5 order, each:
+ *     i32 kind (1 dense, 2 csr, 3 svd); i32 level; i64 row0, m, col0, n
+ *         (tree-order row range [row0, row0+m), column range [col0, col0+n))
+ *     dense: val[m*n] row-major
+ *     csr:   i64 nnz; i64 rowptr[m+1]; i32 col[nnz] (local to col0); val[nnz]
+ *     svd:   i64 q, mu, nv; i32 urow[mu]; i32 vrow[nv] (local indices of the
+ *            nonzero rows of U / V, reading A8); val S[q]; val U[mu*q] and
+ *            val V[nv*q], both row-major (row r holds its q entries)
+ *   val = double (dtype 1) or float (dtype 2).  The block contributes
+ *   Y[row0+urow] += U diag(S) V^T X[col0+vrow] (svd) and the obvious
+ *   products for dense / csr.  Zero blocks are not stored.
+ */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VF_H_ */

@@ -1,0 +1,101 @@
+// vf_internal.h -- host-side data structures of libvf (not part of the ABI).
+// PAPER.md = "P:<line>".  See include/vf.h for the operation and DESIGN.md for
+// the device layout.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/vf.h"
+
+namespace vf {
+
+enum LeafKind : int { K_ZERO = 0, K_DENSE = 1, K_CSR = 2, K_SVD = 3, K_SUB = 4 };
+
+// One leaf block of F-hat (Alg. 4 output), tree-order ranges.  Values are
+// kept in double on the host; for VF_F32 handles they are already rounded to
+// float (so save/load and upload see exactly the stored values).
+struct Leaf {
+    int kind = K_ZERO;
+    int level = 0;
+    int64_t row0 = 0, m = 0, col0 = 0, n = 0;
+    // dense: a = m*n row-major
+    // csr:   rowptr (m+1), idx_a = local cols, a = values
+    // svd:   q; idx_a = urows (mu), idx_b = vrows (nv); s = S (q);
+    //        a = U (mu*q row-major), b = V (nv*q row-major)
+    int64_t q = 0;
+    std::vector<int64_t> rowptr;
+    std::vector<int32_t> idx_a, idx_b;
+    std::vector<double> a, b, s;
+    int64_t nbytes = 0;
+};
+
+// Device copy of the flattened F-hat (see vf_device.cu).
+struct DeviceHMat;
+
+struct Handle {
+    int64_t N = 0;
+    int dtype = VF_F64;
+    double tol = 0;
+    std::vector<int32_t> perm;       // perm[r] = caller facet at tree position r
+    std::vector<Leaf> leaves;        // Alg. 5 order
+    // geometry kept for vf_insolation (empty for loaded handles)
+    std::vector<double> x, nrm, A;
+    std::vector<double> occ_V;
+    std::vector<int32_t> occ_F;
+    std::vector<int64_t> tri_of;     // facet -> occluder triangle (-1 none)
+    bool has_mesh = false;
+    int64_t visible_pairs = 0;
+    double build_seconds = 0;
+    int device = -1;
+    void* stream = nullptr;
+    DeviceHMat* dev = nullptr;
+    // last-solve stats
+    int iters1 = 0, iters2 = 0;
+    double resid1 = 0, resid2 = 0;
+    // kernel timing
+    bool timing = false;
+    double ms_p2 = 0, ms_p1 = 0;
+    int launches_p2 = 0, launches_p1 = 0, launches_total = 0;
+};
+
+// error reporting (thread-local message)
+int set_error(int code, const std::string& msg);
+
+// host build (vf_build.cpp)
+int build_handle(Handle* h, int64_t N, const double* x, const double* n, const double* A,
+                 const double* occV, int64_t nv, const int32_t* occF, int64_t nt,
+                 const int64_t* tri_of, double tol, const vf_build_opts& o);
+int insolation(const Handle* h, const double* suns, int k, double S, double* Q);
+int64_t leaf_nbytes(const Leaf& L, int w);
+
+// HVFM io (vf_io.cpp)
+int save_hvfm(const Handle* h, const char* path);
+int load_hvfm(Handle* h, const char* path);
+
+// device (vf_device.cu)
+int device_upload(Handle* h, int device);
+void device_free(Handle* h);
+int device_matvec(Handle* h, const void* X, void* Y, int nrhs);
+int device_solve_radiosity(Handle* h, const void* E, const void* rho, void* B, int nrhs,
+                           int iters, double tol, int clamp);
+int device_solve_thermal(Handle* h, const void* Qdir, const void* alb, const void* emi, void* T,
+                         void* Qvis, void* Qir, int nrhs, int iters, double tol);
+int64_t device_bytes(const Handle* h);
+
+// truncated SVD (vf_svd.cpp)
+struct SvdResult {
+    int64_t q = 0;              // accepted rank (0 = failure)
+    std::vector<double> U;      // mu x q row-major
+    std::vector<double> S;      // q
+    std::vector<double> V;      // nv x q row-major
+};
+// Rank estimation of Alg. 3 on the compact (nonzero rows/cols) block given as
+// a dense row-major mu x nv matrix or a CSR (rowptr/cols/vals with local
+// compact columns).  target_bytes = nbytes(F_IJ) of eq. nbytes-comparison.
+SvdResult estimate_rank(int64_t mu, int64_t nv, const double* dense, const int64_t* rowptr,
+                        const int32_t* cols, const double* vals, double eps, int w, int k0,
+                        int64_t target_bytes, int64_t m_full, int64_t n_full, uint64_t seed);
+
+}  // namespace vf

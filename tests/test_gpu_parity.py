@@ -1,0 +1,283 @@
+"""GPU parity: the CUDA path through the C ABI vs the FP64 oracle.
+
+  * same blocks:  GPU apply/solves of an oracle-built F-hat (written by
+    oracle/hmatrix.py as HVFM, loaded with vf_load) vs the oracle's Alg. 5
+    apply and Jacobi/thermal solves of the same blocks:  rel. L2 <= 1e-12
+    (f64), <= 1e-5 (f32), identical iteration counts (BASELINE north_star
+    tolerances);
+  * whole pipeline: the product's own vf_build F-hat on the GPU vs the
+    oracle's exact F:  <= 10 tol, Sherman-Morrison closed form;
+  * full size (BASELINE configs[1], the bench workload): sampled rows of the
+    exact F and the thermal solve of the bench's launch configuration.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import oracle.hmatrix as hm
+import paper_2209_07632_b200 as vf
+import scenegen as sg
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def dev(a, dtype=np.float64):
+    a = np.asarray(a, dtype=dtype)
+    if a.ndim == 1:
+        return torch.from_numpy(a.copy()).cuda()
+    return torch.from_numpy(np.ascontiguousarray(a.T)).cuda().T        # (N, k), strides (1, N)
+
+
+def empty(N, k, dtype=torch.float64):
+    return torch.empty((k, N), dtype=dtype, device="cuda").T
+
+
+def host(t):
+    return t.cpu().numpy().astype(np.float64)
+
+
+def rel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+# ----------------------------------------------------------------- fixtures
+
+@pytest.fixture(scope="module")
+def cap():
+    V, F = sg.cfg1_mesh()
+    S = oracle.Scene(V, F)
+    return V, F, S, S.F_dense()
+
+
+@pytest.fixture(scope="module")
+def rough():
+    V, F = sg.rough_small_mesh(24)          # 1152 facets, occluded: CSR leaves
+    S = oracle.Scene(V, F)
+    return V, F, S, S.F_dense()
+
+
+def oracle_handle(S, Fd, tmp_path_factory, eps, dtype="f64", min_size=16384, tag=""):
+    H = hm.compress(S.x, Fd, eps, dtype=dtype, min_size=min_size)
+    p = str(tmp_path_factory.mktemp("hv") / f"o{tag}{dtype}.hvfm")
+    hm.write_hvfm(H, p)
+    return H, vf.ViewFactorMatrix.load(p, device=0)
+
+
+CASES = [("cap", 1e-5, 16384), ("cap", 1e-7, 2048), ("rough", 1e-5, 2048), ("rough", 1e-14, 16384)]
+
+
+@pytest.mark.parametrize("which,eps,min_size", CASES)
+@pytest.mark.parametrize("k", [1, 2, 3, 8, 17, 64, 130, 300])
+def test_matvec_same_blocks_f64(cap, rough, tmp_path_factory, which, eps, min_size, k):
+    V, F, S, Fd = cap if which == "cap" else rough
+    H, M = oracle_handle(S, Fd, tmp_path_factory, eps, "f64", min_size, f"{which}{eps}{min_size}")
+    kinds = {b.kind for b in H.leaves()}
+    assert kinds
+    X = sg.random_rhs(S.N, k, seed=3 + k)
+    Y = empty(S.N, k)
+    M.matvec(dev(X), Y)
+    assert rel(host(Y), hm.hmatvec(H, X)) <= 1e-12
+
+
+def test_block_kinds_covered(cap, rough, tmp_path_factory):
+    seen = set()
+    for which, eps, ms in CASES:
+        V, F, S, Fd = cap if which == "cap" else rough
+        H = hm.compress(S.x, Fd, eps, min_size=ms)
+        seen |= {b.kind for b in H.leaves()}
+    assert seen == {hm.DENSE, hm.CSR, hm.SVD}
+
+
+@pytest.mark.parametrize("k", [1, 4, 64])
+def test_matvec_same_blocks_f32(cap, rough, tmp_path_factory, k):
+    for which in ("cap", "rough"):
+        V, F, S, Fd = cap if which == "cap" else rough
+        H, M = oracle_handle(S, Fd, tmp_path_factory, 1e-5, "f32", 2048, which)
+        X = sg.random_rhs(S.N, k).astype(np.float32).astype(np.float64)
+        Y = empty(S.N, k, torch.float32)
+        M.matvec(dev(X, np.float32), Y)
+        assert rel(host(Y), hm.hmatvec(H, X)) <= 1e-5
+
+
+def test_host_pointers_equal_device_and_deterministic(cap, tmp_path_factory):
+    V, F, S, Fd = cap
+    H, M = oracle_handle(S, Fd, tmp_path_factory, 1e-5, "f64", 4096, "hp")
+    X = sg.random_rhs(S.N, 5)
+    Yh = np.empty((S.N, 5), order="F")
+    M.matvec(np.asfortranarray(X), Yh)
+    Yd = empty(S.N, 5)
+    M.matvec(dev(X), Yd)
+    Yd2 = empty(S.N, 5)
+    M.matvec(dev(X), Yd2)
+    assert np.array_equal(Yh, host(Yd)) and torch.equal(Yd, Yd2)
+
+
+@pytest.mark.parametrize("k", [1, 3, 64])
+def test_radiosity_same_blocks(cap, rough, tmp_path_factory, k):
+    for which in ("cap", "rough"):
+        V, F, S, Fd = cap if which == "cap" else rough
+        H, M = oracle_handle(S, Fd, tmp_path_factory, 1e-6, "f64", 2048, "rad" + which)
+        rng = np.random.default_rng(11)
+        E = np.asfortranarray(1000 * rng.random((S.N, k)))
+        rho = 0.05 + 0.9 * rng.random(S.N)
+        B0, Q0, it0, r0 = oracle.jacobi(lambda X: hm.hmatvec(H, X), E, rho, 1e-13, 200)
+        B = empty(S.N, k)
+        M.solve_radiosity(dev(E), dev(rho), B, iters=200, tol=1e-13)
+        st = M.stats()
+        assert st["iters1"] == it0
+        assert rel(host(B), B0) <= 1e-12
+
+
+@pytest.mark.parametrize("k", [1, 64])
+def test_thermal_same_blocks(cap, tmp_path_factory, k):
+    V, F, S, Fd = cap
+    H, M = oracle_handle(S, Fd, tmp_path_factory, 1e-5, "f64", 16384, "th")
+    Q = S.insolation(sg.sun_dirs(10.0, k, 0.1))
+    alb, emi = np.full(S.N, 0.12), np.full(S.N, 0.95)
+    ref = oracle.thermal(lambda X: hm.hmatvec(H, X), Q, alb, emi, 1e-12, 100)
+    T, Qv, Qi = empty(S.N, k), empty(S.N, k), empty(S.N, k)
+    M.solve_thermal(dev(Q), dev(alb), dev(emi), T, Qv, Qi, iters=100, tol=1e-12)
+    st = M.stats()
+    assert (st["iters1"], st["iters2"]) == (ref["it1"], ref["it2"])
+    assert rel(host(Qv), ref["Qvis"]) <= 1e-12
+    assert rel(host(Qi), ref["Qir"]) <= 1e-12
+    assert rel(host(T), ref["T"]) <= 1e-12
+
+
+def test_noconv_keeps_last_iterate(cap, tmp_path_factory):
+    V, F, S, Fd = cap
+    H, M = oracle_handle(S, Fd, tmp_path_factory, 1e-5, "f64", 16384, "nc")
+    E = np.asfortranarray(np.random.default_rng(1).random((S.N, 2)))
+    rho = np.full(S.N, 0.9)
+    B0, *_ = oracle.jacobi(lambda X: hm.hmatvec(H, X), E, rho, 1e-300, 2)
+    B = empty(S.N, 2)
+    with pytest.raises(vf.VFError) as e:
+        M.solve_radiosity(dev(E), dev(rho), B, iters=2, tol=1e-300)
+    assert e.value.code == vf.VF_ENOCONV
+    assert rel(host(B), B0) <= 1e-12
+
+
+# ----------------------------------------------------------- whole pipeline
+
+@pytest.mark.parametrize("tol", [1e-3, 1e-5])
+def test_product_build_matvec_vs_exact_F(cap, tol):
+    V, F, S, Fd = cap
+    M = vf.ViewFactorMatrix.build(V, F, tol)
+    X = sg.random_rhs(S.N, 20)
+    Y = empty(S.N, 20)
+    M.matvec(dev(X), Y)
+    assert rel(host(Y), oracle.apply_dense(Fd, X)) <= 10 * tol
+
+
+def test_product_build_f32(cap):
+    V, F, S, Fd = cap
+    M = vf.ViewFactorMatrix.build(V, F, 1e-5, dtype=vf.VF_F32)
+    X = sg.random_rhs(S.N, 8)
+    Y = empty(S.N, 8, torch.float32)
+    M.matvec(dev(X, np.float32), Y)
+    assert rel(host(Y), oracle.apply_dense(Fd, X)) <= 1e-4
+
+
+def test_sherman_morrison_pipeline():
+    R = 1.0
+    x, n, A = sg.sphere_exact_facets(1200, R, cap_cos=0.2)
+    M = vf.ViewFactorMatrix.build_facets(x, n, A, 1e-10, min_block=4096)
+    c = 1 / (4 * math.pi * R * R)
+    rng = np.random.default_rng(5)
+    rho = 0.05 + 0.9 * rng.random(1200)
+    E = np.asfortranarray(rng.random((1200, 4)))
+    Dg = 1.0 + c * rho * A
+    y = E / Dg[:, None]
+    u = rho / Dg
+    exact = y + u[:, None] * (c * (A @ y)) / (1.0 - c * (A @ u))
+    B = empty(1200, 4)
+    M.solve_radiosity(dev(E), dev(rho), B, iters=100, tol=1e-15, clamp=True)
+    assert rel(host(B), exact) <= 1e-12
+
+
+def test_product_thermal_vs_exact_F_cfg1(cap):
+    V, F, S, Fd = cap
+    M = vf.ViewFactorMatrix.build(V, F, 1e-5)
+    Q = S.insolation(sg.sun_dirs(10.0, 1))
+    alb, emi = np.full(S.N, 0.12), np.full(S.N, 0.95)
+    ref = oracle.thermal(lambda X: oracle.apply_dense(Fd, X), Q, alb, emi, 1e-10, 100)
+    T = empty(S.N, 1)
+    M.solve_thermal(dev(Q), dev(alb), dev(emi), T, iters=100, tol=1e-10)
+    assert rel(host(T), ref["T"]) <= 10 * 1e-5
+
+
+# ------------------------------------------------------------- edge cases
+
+def test_empty_operator_flat_plane():
+    V, F = sg.flat_plane_mesh(16)
+    M = vf.ViewFactorMatrix.build(V, F, 1e-5)
+    N = F.shape[0]
+    X = sg.random_rhs(N, 3)
+    Y = empty(N, 3)
+    M.matvec(dev(X), Y)
+    assert torch.count_nonzero(Y) == 0
+    B = empty(N, 3)
+    M.solve_radiosity(dev(X), dev(np.full(N, 0.3)), B, iters=10, tol=1e-12)
+    assert np.array_equal(host(B), X) and M.stats()["iters1"] == 1
+
+
+def test_zero_inputs_and_rho_zero(cap, tmp_path_factory):
+    V, F, S, Fd = cap
+    H, M = oracle_handle(S, Fd, tmp_path_factory, 1e-5, "f64", 16384, "z")
+    Y = empty(S.N, 2)
+    M.matvec(dev(np.zeros((S.N, 2))), Y)
+    assert torch.count_nonzero(Y) == 0
+    E = np.asfortranarray(np.random.default_rng(2).random((S.N, 2)))
+    B = empty(S.N, 2)
+    M.solve_radiosity(dev(E), dev(np.zeros(S.N)), B, iters=10, tol=1e-14)
+    assert np.array_equal(host(B), E)
+    T = empty(S.N, 2)
+    M.solve_thermal(dev(np.zeros((S.N, 2))), dev(np.full(S.N, .1)), dev(np.full(S.N, .9)), T, iters=10, tol=1e-12)
+    assert torch.count_nonzero(T) == 0
+
+
+# ---------------------------------------------- full size: BASELINE configs[1]
+
+@pytest.fixture(scope="module")
+def cfg2():
+    V, F = sg.cfg2_mesh()
+    S = oracle.Scene(V, F)
+    M = vf.ViewFactorMatrix.build(V, F, 1e-5)
+    return V, F, S, M
+
+
+def test_cfg2_sampled_rows_vs_exact_F(cfg2):
+    V, F, S, M = cfg2
+    k = 64
+    X = sg.random_rhs(S.N, k)
+    Y = empty(S.N, k)
+    M.matvec(dev(X), Y)
+    Yh = host(Y)
+    crater = np.flatnonzero(S.x[:, 2] < -1e-9)
+    rng = np.random.default_rng(7)
+    rows = np.concatenate([rng.choice(crater, 300, replace=False), rng.choice(S.N, 300, replace=False)])
+    csr = S.F_csr_rows(rows)
+    Yex = oracle.apply_csr(csr, X)
+    assert rel(Yh[rows], Yex) <= 10 * 1e-5
+
+
+def test_cfg2_bench_configuration_thermal(cfg2):
+    """The bench's launch configuration: 64 suns at 5 deg elevation, f64."""
+    V, F, S, M = cfg2
+    suns = sg.sun_dirs(5.0, 64)
+    Q = M.insolation(suns, 1365.0)
+    Q0 = S.insolation(suns, 1365.0)
+    assert np.array_equal(Q > 0, Q0 > 0) and np.max(np.abs(Q - Q0)) <= 1e-12 * 1365
+    csr = S.F_csr_rows()
+    alb, emi = np.full(S.N, 0.12), np.full(S.N, 0.95)
+    ref = oracle.thermal(lambda X: oracle.apply_csr(csr, X), Q0, alb, emi, 1e-10, 100)
+    T = empty(S.N, 64)
+    M.solve_thermal(dev(Q), dev(alb), dev(emi), T, iters=100, tol=1e-10)
+    assert rel(host(T), ref["T"]) <= 10 * 1e-5
+    sh = (Q0 == 0) & (S.x[:, 2:3] < -1e-9)
+    assert rel(host(T)[sh], ref["T"][sh]) <= 10 * 1e-5
