@@ -184,6 +184,7 @@ typedef struct {
     int64_t p1_src_rows;   /* distinct X rows phase 1 reads                          */
     int64_t p2_src_rows;   /* distinct X/T rows phase 2 reads                        */
     int64_t p1_flops_per_col, p2_flops_per_col;
+    int64_t groups1, groups2;  /* row groups of the batched layout (phase 1 / 2)      */
 } vf_info_t;
 
 int vf_info(vf_handle h, vf_info_t* out);

@@ -1,8 +1,8 @@
 // vf_device.cu -- device layout of F-hat and the sm_100a hot path.
 // PAPER.md = "P:<line>".  DESIGN.md §"Device layout" / §"Kernels".
 //
-// Alg. 5 is flattened into two launches of ONE segmented-row
-// kernel over a single source buffer XT = [Xp ; T] (tree-order rows, k
+// Alg. 5 is flattened into two phases of ONE segmented-row
+// computation over a single source buffer XT = [Xp ; T] (tree-order rows, k
 // contiguous per row):
 //   phase 1  (a2)  T_t = S_b[l] * sum_j V_b[j,l] Xp[col0_b + vrow_j]     for
 //                  every rank-1 term t = (b, l) of every SVD block, blocks
@@ -13,13 +13,22 @@
 //                  (contiguous T rows), merged CSR row (gathered X rows);
 //                  followed by the fused Jacobi epilogue (clamp P:237,
 //                  B' = E + rho Q, residual partials, B'/Q stores).
+// A whole Jacobi solve (a1..a5) is ONE persistent cooperative launch: the
+// grid loops over iterations, phases separated by a grid barrier; every CTA
+// reduces the per-CTA residual partials in the same fixed order and takes
+// the same convergence decision, so no host round trip per iteration.
 // Every output row is owned by one warp; segments are summed in a fixed
-// order and per-CTA residual partials are reduced in a fixed order, so
-// results are bitwise reproducible (no float atomics).
+// order; no float atomics: results are bitwise reproducible.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
+#include <map>
+#include <queue>
+#include <cstddef>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <vector>
@@ -31,8 +40,10 @@ namespace vf {
 namespace {
 
 constexpr int kWarps = 8;               // warps per CTA (256 threads)
-constexpr int kCtasPerSm = 6;
-constexpr int kNumSms = 148;            // B200
+constexpr int kThreads = kWarps * 32;
+constexpr int kMaxCtasPerSm = 2;
+constexpr int kMaxKp = 2048;
+constexpr int kMaxGrid = 512;           // CTAs of a persistent launch (<= 2 x SMs)            // columns per launch (sred: kWarps*kp doubles)
 constexpr double kSigmaSB = 5.670374419e-8;
 
 struct Seg {                            // one run of a row's terms
@@ -42,13 +53,15 @@ struct Seg {                            // one run of a row's terms
     int32_t kind;                       // 0 contiguous, 1 gather
 };
 
-struct Ctl {                            // device-side loop control
+struct Ctl {                            // device-side loop state
     int iter;                           // completed iterations
     int done;
-    int pad[2];
+    int bad[2];                         // some column not converged (by iteration parity)
+    unsigned bar_arrive;                // grid barrier
+    unsigned bar_gen;
 };
 
-enum Mode { M_PHASE1 = 0, M_MATVEC = 1, M_SOLVE = 2 };
+enum Mode { M_MATVEC = 0, M_SOLVE = 1 };
 
 #define CK(call)                                                                         \
     do {                                                                                 \
@@ -57,24 +70,24 @@ enum Mode { M_PHASE1 = 0, M_MATVEC = 1, M_SOLVE = 2 };
             return set_error(VF_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
-template <typename T, int VEC>
-struct VecIO;
-template <>
-struct VecIO<double, 1> {
-    static __device__ __forceinline__ void ld(const double* p, double* v) { v[0] = __ldg(p); }
+// ---- vector loads: F-hat data through the read-only path, XT (written
+// inside the persistent kernel by other CTAs) through L2 (ld.global.cg).
+template <typename T, int VEC> struct Vec;
+template <> struct Vec<double, 1> {
+    static __device__ __forceinline__ void cg(const double* p, double* v) { v[0] = __ldcg(p); }
     static __device__ __forceinline__ void st(double* p, const double* v) { p[0] = v[0]; }
 };
-template <>
-struct VecIO<double, 2> {
-    static __device__ __forceinline__ void ld(const double* p, double* v) {
-        double2 a = __ldg(reinterpret_cast<const double2*>(p)); v[0] = a.x; v[1] = a.y;
+template <> struct Vec<double, 2> {
+    static __device__ __forceinline__ void cg(const double* p, double* v) {
+        double2 a = __ldcg(reinterpret_cast<const double2*>(p)); v[0] = a.x; v[1] = a.y;
     }
-    static __device__ __forceinline__ void st(double* p, const double* v) { *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]); }
+    static __device__ __forceinline__ void st(double* p, const double* v) {
+        *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+    }
 };
-template <>
-struct VecIO<double, 4> {
-    static __device__ __forceinline__ void ld(const double* p, double* v) {
-        double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+template <> struct Vec<double, 4> {
+    static __device__ __forceinline__ void cg(const double* p, double* v) {
+        double2 a = __ldcg(reinterpret_cast<const double2*>(p)), b = __ldcg(reinterpret_cast<const double2*>(p) + 1);
         v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
     }
     static __device__ __forceinline__ void st(double* p, const double* v) {
@@ -82,226 +95,531 @@ struct VecIO<double, 4> {
         reinterpret_cast<double2*>(p)[1] = make_double2(v[2], v[3]);
     }
 };
-template <>
-struct VecIO<float, 1> {
-    static __device__ __forceinline__ void ld(const float* p, float* v) { v[0] = __ldg(p); }
+template <> struct Vec<float, 1> {
+    static __device__ __forceinline__ void cg(const float* p, float* v) { v[0] = __ldcg(p); }
     static __device__ __forceinline__ void st(float* p, const float* v) { p[0] = v[0]; }
 };
-template <>
-struct VecIO<float, 2> {
-    static __device__ __forceinline__ void ld(const float* p, float* v) {
-        float2 a = __ldg(reinterpret_cast<const float2*>(p)); v[0] = a.x; v[1] = a.y;
+template <> struct Vec<float, 2> {
+    static __device__ __forceinline__ void cg(const float* p, float* v) {
+        float2 a = __ldcg(reinterpret_cast<const float2*>(p)); v[0] = a.x; v[1] = a.y;
     }
-    static __device__ __forceinline__ void st(float* p, const float* v) { *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]); }
-};
-template <>
-struct VecIO<float, 4> {
-    static __device__ __forceinline__ void ld(const float* p, float* v) {
-        float4 a = __ldg(reinterpret_cast<const float4*>(p)); v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    static __device__ __forceinline__ void st(float* p, const float* v) {
+        *reinterpret_cast<float2*>(p) = make_float2(v[0], v[1]);
     }
-    static __device__ __forceinline__ void st(float* p, const float* v) { *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]); }
+};
+template <> struct Vec<float, 4> {
+    static __device__ __forceinline__ void cg(const float* p, float* v) {
+        float4 a = __ldcg(reinterpret_cast<const float4*>(p)); v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    }
+    static __device__ __forceinline__ void st(float* p, const float* v) {
+        *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+    }
 };
 
-struct RowArgs {
-    const int64_t* segptr;    // [nrows + 1]
-    const Seg* segs;
-    const int32_t* rows;      // output row id per row (phase 2: tree row; phase 1: t)
-    int64_t nrows;
-    const void* vals;
-    const int32_t* idx;
-    const void* scale;        // phase 1: S per T row
-    const void* xt;           // source rows (XT[cur])
-    void* out;                // phase 1: XT[cur] (T region written at row N+t); matvec: Yp; solve: XT[next]
-    const void* E;            // solve
-    const void* rho;          // solve (nullptr => rho = 1)
-    void* Q;                  // solve: last Q
-    double* partial;          // solve: [gridDim.x][kp] residual partial sums
-    const Ctl* ctl;
-    int64_t N;                // rows of Xp (T region starts at N)
-    int kp;
-    int clamp;
+template <> struct Vec<double, 8> {
+    static __device__ __forceinline__ void cg(const double* p, double* v) {
+        Vec<double, 4>::cg(p, v);
+        Vec<double, 4>::cg(p + 4, v + 4);
+    }
+    static __device__ __forceinline__ void st(double* p, const double* v) {
+        Vec<double, 4>::st(p, v);
+        Vec<double, 4>::st(p + 4, v + 4);
+    }
+};
+template <> struct Vec<float, 8> {
+    static __device__ __forceinline__ void cg(const float* p, float* v) {
+        Vec<float, 4>::cg(p, v);
+        Vec<float, 4>::cg(p + 4, v + 4);
+    }
+    static __device__ __forceinline__ void st(float* p, const float* v) {
+        Vec<float, 4>::st(p, v);
+        Vec<float, 4>::st(p + 4, v + 4);
+    }
 };
 
-// Segmented-row kernel.  One warp per output row; lane = (group g, sub-lane c):
-// KC sub-lanes cover KC*VEC consecutive columns, the 32/KC groups split the
-// row's terms; groups are combined by a fixed xor-shuffle tree.
-template <typename T, int KC, int VEC, int MODE>
-__global__ void __launch_bounds__(kWarps * 32)
-segrow_kernel(RowArgs a) {
-    constexpr int G = 32 / KC;
-    constexpr int CW = KC * VEC;
-    if (a.ctl && a.ctl->done) return;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int g = lane / KC, c = lane % KC;
-    const int col = blockIdx.y * CW + c * VEC;
-    const bool col_ok = col < a.kp;
-    const int64_t kp = a.kp;
-    const T* __restrict__ vals = static_cast<const T*>(a.vals);
-    const T* __restrict__ xt = static_cast<const T*>(a.xt);
-    int cur = a.ctl ? (a.ctl->iter & 1) : 0;
-    (void)cur;
-    double part[VEC];
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) part[v] = 0.0;
+// ---- row groups (batched right-hand sides).  Up to kGroup output rows that
+// share the SOURCE of their dense / U (phase 2) or V (phase 1) segments are
+// one work item: a warp computes a kGroup-row x (2 VEC)-column tile, lane =
+// (row r = lane/2, half h = lane%2), so every XT source row is loaded once per
+// tile (a broadcast to the 16 lanes of a half) instead of once per row.
+constexpr int kGroup = 16;
+struct GSeg {                           // shared source run of a group
+    int64_t src;                        // kind 0: first XT row; kind 1: offset into idx[]
+    int32_t len;
+    int32_t kind;
+};
+struct Group {
+    int32_t nrows;                      // <= kGroup
+    int32_t nseg;
+    int64_t seg_off;                    // first GSeg; values of row r of seg s at gvo[(seg_off+s)*kGroup + r]
+};
 
-    const int64_t wstride = (int64_t)gridDim.x * kWarps;
-    for (int64_t r = (int64_t)blockIdx.x * kWarps + warp; r < a.nrows; r += wstride) {
-        T acc[VEC];
+template <typename T, int VEC>
+__device__ __forceinline__ void group_accumulate(const Group& G, int64_t gi, const GSeg* __restrict__ gseg,
+                                                 const int64_t* __restrict__ gvo, const int64_t* __restrict__ gcsr,
+                                                 const Seg* __restrict__ segs, const T* __restrict__ vals,
+                                                 const int32_t* __restrict__ idx, const T* xt, int64_t kp, int col,
+                                                 bool col_ok, int r, T* acc, int part, int nparts) {
+    constexpr int U = 4;
+    T acc2[VEC];
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) acc[v] = T(0);
-        const int64_t s0 = a.segptr[r], s1 = a.segptr[r + 1];
-        for (int64_t s = s0; s < s1; ++s) {
-            const Seg sg = a.segs[s];
-            const T* __restrict__ vp = vals + sg.val_off;
-            if (sg.kind == 0) {
-                const T* __restrict__ xp = xt + sg.src * kp + col;
-#pragma unroll 4
-                for (int e = g; e < sg.len; e += G) {
-                    const T w = __ldg(vp + e);
-                    if (col_ok) {
-                        T x[VEC];
-                        VecIO<T, VEC>::ld(xp + (int64_t)e * kp, x);
+    for (int v = 0; v < VEC; ++v) { acc[v] = T(0); acc2[v] = T(0); }
+    const bool rv = r < G.nrows;
+    for (int s = 0; s < G.nseg; ++s) {
+        const GSeg sg = gseg[G.seg_off + s];
+        const T* __restrict__ vp = vals + (rv ? gvo[(G.seg_off + s) * kGroup + r] : 0);
+        const int32_t* __restrict__ ip = idx + (sg.kind ? sg.src : 0);
+        const int len = sg.len;
+        for (int j0 = part * U; j0 < len; j0 += nparts * U) {
+            T w[U];
+            int64_t xr[U];
 #pragma unroll
-                        for (int v = 0; v < VEC; ++v) acc[v] = fma(w, x[v], acc[v]);
+            for (int u = 0; u < U; ++u) {
+                const int j = j0 + u;
+                const bool ok = j < len;
+                w[u] = (ok && rv) ? __ldg(vp + j) : T(0);
+                xr[u] = sg.kind ? (ok ? (int64_t)__ldg(ip + j) : 0) : sg.src + (ok ? j : 0);
+            }
+            if (col_ok) {
+                T x[U][VEC];
+#pragma unroll
+                for (int u = 0; u < U; ++u) Vec<T, VEC>::cg(xt + xr[u] * kp + col, x[u]);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) {
+                        if (u & 1) acc2[v] = fma(w[u], x[u][v], acc2[v]);
+                        else acc[v] = fma(w[u], x[u][v], acc[v]);
                     }
-                }
-            } else {
-                const int32_t* __restrict__ ip = a.idx + sg.src;
-#pragma unroll 4
-                for (int e = g; e < sg.len; e += G) {
-                    const T w = __ldg(vp + e);
-                    const int64_t xr = __ldg(ip + e);
-                    if (col_ok) {
-                        T x[VEC];
-                        VecIO<T, VEC>::ld(xt + xr * kp + col, x);
-#pragma unroll
-                        for (int v = 0; v < VEC; ++v) acc[v] = fma(w, x[v], acc[v]);
-                    }
-                }
             }
         }
+    }
+    // the row's own CSR gather segment (phase 2), summed last
+    const int64_t cs = rv ? gcsr[gi * kGroup + r] : -1;
+    if (cs >= 0 && col_ok) {
+        const Seg sg = segs[cs];
+        const T* __restrict__ vp = vals + sg.val_off;
+        const int32_t* __restrict__ ip = idx + sg.src;
+        for (int e0 = part * U; e0 < sg.len; e0 += nparts * U) {
+            T w[U];
+            int64_t xr[U];
 #pragma unroll
-        for (int off = KC; off < 32; off <<= 1)
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
-        if (g != 0 || !col_ok) continue;
-        const int64_t orow = a.rows[r];
-        if (MODE == M_PHASE1) {
-            const T s = static_cast<const T*>(a.scale)[orow];
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) acc[v] *= s;
-            VecIO<T, VEC>::st(static_cast<T*>(a.out) + (a.N + orow) * kp + col, acc);
-        } else if (MODE == M_MATVEC) {
-            VecIO<T, VEC>::st(static_cast<T*>(a.out) + orow * kp + col, acc);
-        } else {
-            const int64_t o = orow * kp + col;
-            T e[VEC], bo[VEC], bn[VEC];
-            VecIO<T, VEC>::ld(static_cast<const T*>(a.E) + o, e);
-            VecIO<T, VEC>::ld(xt + o, bo);
-            const T rh = a.rho ? static_cast<const T*>(a.rho)[orow] : T(1);
-#pragma unroll
-            for (int v = 0; v < VEC; ++v) {
-                if (a.clamp) acc[v] = acc[v] > T(0) ? acc[v] : T(0);
-                bn[v] = e[v] + rh * acc[v];                               // eq. (1)
-                const double d = (double)bn[v] - (double)bo[v];
-                if (col + v < a.kp) part[v] += d * d;
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u;
+                const bool ok = e < sg.len;
+                w[u] = ok ? __ldg(vp + e) : T(0);
+                xr[u] = ok ? (int64_t)__ldg(ip + e) : 0;
             }
-            VecIO<T, VEC>::st(static_cast<T*>(a.out) + o, bn);
-            VecIO<T, VEC>::st(static_cast<T*>(a.Q) + o, acc);
-        }
-    }
-    if (MODE == M_SOLVE) {
-        // CTA-level fixed-order reduction of residual partials: [warp][CW]
-        __shared__ double red[kWarps][32 * 4];
-        if (g == 0) {
+            T x[U][VEC];
 #pragma unroll
-            for (int v = 0; v < VEC; ++v) red[warp][c * VEC + v] = part[v];
-        }
-        __syncthreads();
-        for (int cc = threadIdx.x; cc < CW; cc += blockDim.x) {
-            double s = 0.0;
-            for (int w = 0; w < kWarps; ++w) s += red[w][cc];
-            const int gc = blockIdx.y * CW + cc;
-            if (gc < a.kp) a.partial[(int64_t)blockIdx.x * kp + gc] = s;
+            for (int u = 0; u < U; ++u) Vec<T, VEC>::cg(xt + xr[u] * kp + col, x[u]);
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) {
+                    if (u & 1) acc2[v] = fma(w[u], x[u][v], acc2[v]);
+                    else acc[v] = fma(w[u], x[u][v], acc[v]);
+                }
         }
     }
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[v] += acc2[v];
 }
 
-// Per-column sums of partial[nblk][kp] in block order -> r_c, loop control.
-__global__ void reduce_kernel(const double* partial, int nblk, int kp, int k, const double* enorm2,
-                              double* resid, Ctl* ctl, int iters, double tol) {
-    if (ctl->done) return;
-    __shared__ int ok;
-    if (threadIdx.x == 0) ok = 1;
-    __syncthreads();
-    for (int c = threadIdx.x; c < k; c += blockDim.x) {
-        double s = 0.0;
-        for (int b = 0; b < nblk; ++b) s += partial[(int64_t)b * kp + c];
-        const double en = enorm2[c];
-        const double r = en > 0.0 ? sqrt(s) / sqrt(en) : 0.0;
-        resid[c] = r;
-        if (!(r <= tol)) atomicAnd(&ok, 0);
+// Sum over a row's segments of value * XT[source row, col .. col+VEC).
+// Lane (g, c): group g takes terms g, g+G, ...; U terms are loaded before
+// they are used (memory-level parallelism), two accumulator sets break the
+// FMA chain.  The caller combines the G groups.
+template <typename T, int KC, int VEC>
+__device__ __forceinline__ void row_accumulate(const Seg* __restrict__ segs, int64_t s0, int64_t s1,
+                                               const T* __restrict__ vals, const int32_t* __restrict__ idx,
+                                               const T* xt, int64_t kp, int col, bool col_ok, int g, T* acc) {
+    constexpr int G = 32 / KC;
+    constexpr int U = 4;
+    T acc2[VEC];
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) { acc[v] = T(0); acc2[v] = T(0); }
+    for (int64_t s = s0; s < s1; ++s) {
+        const Seg sg = segs[s];
+        const T* __restrict__ vp = vals + sg.val_off;
+        const int32_t* __restrict__ ip = idx + (sg.kind ? sg.src : 0);
+        const int len = sg.len;
+        for (int e0 = g; e0 < len; e0 += G * U) {
+            T w[U];
+            int64_t xr[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int e = e0 + u * G;
+                const bool ok = e < len;
+                w[u] = ok ? __ldg(vp + e) : T(0);
+                xr[u] = sg.kind ? (ok ? (int64_t)__ldg(ip + e) : 0) : sg.src + (ok ? e : 0);
+            }
+            if (col_ok) {
+                T x[U][VEC];
+#pragma unroll
+                for (int u = 0; u < U; ++u) Vec<T, VEC>::cg(xt + xr[u] * kp + col, x[u]);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+#pragma unroll
+                    for (int v = 0; v < VEC; ++v) {
+                        if (u & 1) acc2[v] = fma(w[u], x[u][v], acc2[v]);
+                        else acc[v] = fma(w[u], x[u][v], acc[v]);
+                    }
+            }
+        }
     }
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) acc[v] += acc2[v];
+#pragma unroll
+    for (int off = KC; off < 32; off <<= 1)
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
+}
+
+// Software grid barrier for a cooperative (co-resident) launch.  Traps
+// instead of hanging if a CTA never arrives.
+__device__ __forceinline__ void grid_sync(Ctl* ctl, unsigned nblk) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const int it = ctl->iter + 1;
-        ctl->iter = it;
-        if (ok || it >= iters) ctl->done = 1;
-    }
-}
-
-// Column sums of squares of V (tree order, N x kp): per-CTA partials.
-template <typename T>
-__global__ void colnorm_partial_kernel(const T* V, int64_t N, int kp, double* partial) {
-    extern __shared__ double sh[];
-    for (int c = threadIdx.x; c < kp; c += blockDim.x) sh[c] = 0.0;
-    __syncthreads();
-    // each CTA owns a contiguous row range; thread t handles column t % kp
-    const int64_t rows_per = (N + gridDim.x - 1) / gridDim.x;
-    const int64_t r0 = (int64_t)blockIdx.x * rows_per, r1 = min(N, r0 + rows_per);
-    const int lanes_per_col = max(1, (int)blockDim.x / kp);
-    const int c = threadIdx.x % kp, j = threadIdx.x / kp;
-    double s = 0.0;
-    if (j < lanes_per_col && threadIdx.x < lanes_per_col * kp)
-        for (int64_t r = r0 + j; r < r1; r += lanes_per_col) {
-            const double v = (double)V[r * kp + c];
-            s += v * v;
+        volatile unsigned* gen = &ctl->bar_gen;
+        const unsigned g0 = *gen;
+        __threadfence();
+        const unsigned prev = atomicAdd(&ctl->bar_arrive, 1u);
+        if (prev == nblk - 1) {
+            atomicExch(&ctl->bar_arrive, 0u);
+            __threadfence();
+            atomicAdd(&ctl->bar_gen, 1u);
+        } else {
+            unsigned long long spins = 0;
+            while (*gen == g0) {
+                __nanosleep(32);
+                if (++spins > (1ull << 27)) __trap();
+            }
         }
-    // fixed-order combine: sh[c] += s for j = 0..lanes_per_col-1 in order
-    for (int jj = 0; jj < lanes_per_col; ++jj) {
-        __syncthreads();
-        if (j == jj && threadIdx.x < lanes_per_col * kp) sh[c] += s;
+        __threadfence();
     }
     __syncthreads();
-    for (int cc = threadIdx.x; cc < kp; cc += blockDim.x) partial[(int64_t)blockIdx.x * kp + cc] = sh[cc];
 }
 
-__global__ void colnorm_final_kernel(const double* partial, int nblk, int kp, int k, double* out) {
-    for (int c = threadIdx.x; c < k; c += blockDim.x) {
-        double s = 0.0;
-        for (int b = 0; b < nblk; ++b) s += partial[(int64_t)b * kp + c];
-        out[c] = s;
+struct HotArgs {
+    // per-row layout (nrhs <= 2): phase 1 / phase 2 rows and their segments
+    const int64_t* p1_segptr;
+    const int32_t* p1_rows;
+    int64_t n_p1;
+    const void* p1_scale;
+    const int64_t* p2_segptr;
+    const int32_t* p2_rows;
+    int64_t n_p2;
+    // row-group layout (nrhs >= 4)
+    const Group* g1;
+    int64_t n_g1;
+    const Group* g2;
+    int64_t n_g2;
+    const GSeg* gseg;
+    const int64_t* gvo;
+    const int32_t* grow1;     // [group][kGroup] output T row t (phase 1)
+    const int64_t* gcsr1;     // [group][kGroup] all -1 (phase 1 has no CSR)
+    const int32_t* grow2;     // [group][kGroup] output tree row (phase 2)
+    const int64_t* gcsr2;     // [group][kGroup] CSR Seg index or -1
+    // F-hat payload
+    const Seg* segs;
+    const void* vals;
+    const int32_t* idx;
+    // state
+    void* xt0;                // XT buffers (rows 0..N: B or X; rows N..: T)
+    void* xt1;
+    void* Y;                  // matvec output (tree order)
+    const void* E;            // solve
+    const void* rho;          // solve; nullptr => rho = 1
+    void* Q;                  // solve: last clamped Q
+    double* partial;          // [2][gridDim.x][kp]
+    const double* enorm2;     // [k]
+    double* resid;            // [k]
+    Ctl* ctl;
+    int64_t N;
+    int kp, k, iters, clamp;
+    double tol;
+    // static LPT schedules: worker w (a warp in the row layout, a CTA in the
+    // row-group layout) processes items sN_items[sN_ptr[w] .. sN_ptr[w+1])
+    const int32_t* s1_ptr;
+    const int32_t* s1_items;
+    const int32_t* s2_ptr;
+    const int32_t* s2_items;
+    unsigned long long* trace;    // optional: [iter][event][cta] globaltimer (VF_TRACE_FILE)
+    int trace_iters;
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// events per iteration: 0 start, 1 phase-1 done, 2 after barrier 1, 3 phase-2 done, 4 after barrier 2
+__device__ __forceinline__ void trace_ev(const HotArgs& a, int it, int ev) {
+    if (a.trace && threadIdx.x == 0 && it < a.trace_iters)
+        a.trace[((int64_t)it * 5 + ev) * gridDim.x + blockIdx.x] = gtimer();
+}
+
+// Fused Jacobi epilogue for one output row x VEC columns (a4): clamp,
+// B' = E + rho Q (eq. (1)), store B' and Q, return (B' - B)^2 per column.
+template <typename T, int VEC>
+__device__ __forceinline__ void solve_epilogue(const HotArgs& a, const T* xc, T* xn, int64_t orow, int col, T* acc,
+                                               double* d2) {
+    const int64_t o = orow * (int64_t)a.kp + col;
+    T e[VEC], bo[VEC], bn[VEC];
+    Vec<T, VEC>::cg(static_cast<const T*>(a.E) + o, e);
+    Vec<T, VEC>::cg(xc + o, bo);
+    const T rh = a.rho ? static_cast<const T*>(a.rho)[orow] : T(1);
+#pragma unroll
+    for (int v = 0; v < VEC; ++v) {
+        if (a.clamp) acc[v] = acc[v] > T(0) ? acc[v] : T(0);
+        bn[v] = e[v] + rh * acc[v];
+        const double d = (double)bn[v] - (double)bo[v];
+        d2[v] = (col + v < a.k) ? d * d : 0.0;
     }
+    Vec<T, VEC>::st(xn + o, bn);
+    Vec<T, VEC>::st(static_cast<T*>(a.Q) + o, acc);
+}
+
+// Phase 1 (a2), per-row layout.
+template <typename T, int KC, int VEC>
+__device__ __forceinline__ void phase1_rows(const HotArgs& a, T* xc, int64_t gwarp, int64_t nwarp, int lane) {
+    constexpr int CW = KC * VEC;
+    const int g = lane / KC, c = lane % KC;
+    const int nchunk = (a.kp + CW - 1) / CW;
+    const T* vals = static_cast<const T*>(a.vals);
+    for (int32_t q = a.s1_ptr[gwarp]; q < a.s1_ptr[gwarp + 1]; ++q) {
+        const int64_t item = a.s1_items[q];
+        const int64_t r = item / nchunk;
+        const int col = (int)(item - r * nchunk) * CW + c * VEC;
+        const bool col_ok = col < a.kp;
+        T acc[VEC];
+        row_accumulate<T, KC, VEC>(a.segs, a.p1_segptr[r], a.p1_segptr[r + 1], vals, a.idx, xc, a.kp, col, col_ok,
+                                   g, acc);
+        if (g == 0 && col_ok) {
+            const int64_t t = a.p1_rows[r];
+            const T sc = static_cast<const T*>(a.p1_scale)[t];
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[v] *= sc;
+            Vec<T, VEC>::st(xc + (a.N + t) * a.kp + col, acc);
+        }
+    }
+}
+
+// Phase 2 (a3 + a4), per-row layout.  Adds residual partials into sw[kp].
+template <typename T, int KC, int VEC, int MODE>
+__device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn, int64_t gwarp, int64_t nwarp,
+                                            int lane, double* sw) {
+    constexpr int CW = KC * VEC;
+    const int g = lane / KC, c = lane % KC;
+    const int nchunk = (a.kp + CW - 1) / CW;
+    const T* vals = static_cast<const T*>(a.vals);
+    for (int32_t q = a.s2_ptr[gwarp]; q < a.s2_ptr[gwarp + 1]; ++q) {
+        const int64_t item = a.s2_items[q];
+        const int64_t r = item / nchunk;
+        const int col = (int)(item - r * nchunk) * CW + c * VEC;
+        const bool col_ok = col < a.kp;
+        T acc[VEC];
+        row_accumulate<T, KC, VEC>(a.segs, a.p2_segptr[r], a.p2_segptr[r + 1], vals, a.idx, xc, a.kp, col, col_ok,
+                                   g, acc);
+        if (g != 0 || !col_ok) continue;
+        const int64_t orow = a.p2_rows[r];
+        if (MODE == M_MATVEC) {
+            Vec<T, VEC>::st(static_cast<T*>(a.Y) + orow * a.kp + col, acc);
+        } else {
+            double d2[VEC];
+            solve_epilogue<T, VEC>(a, xc, xn, orow, col, acc, d2);
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) sw[col + v] += d2[v];
+        }
+    }
+}
+
+// Row-group phases (a2, a3 + a4).  One CTA per (group, 2 VEC-column chunk):
+// its 8 warps split the shared term range (warp w takes every 8th run of U
+// terms), each computing a kGroup x (2 VEC) partial tile; the tiles are
+// summed in warp order through shared memory and the epilogue runs with one
+// thread per tile element.  PHASE 1 writes S_t * tile into the T rows of XT.
+// sw: per-CTA residual partials [kp] (phase 2, solve mode).
+template <typename T, int VEC, int PHASE, int MODE>
+__device__ __forceinline__ void groups_phase(const HotArgs& a, T* xc, T* xn, double* stile, double* sw) {
+    constexpr int CW = 2 * VEC;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int r = lane >> 1, col0 = (lane & 1) * VEC;
+    const int nchunk = (a.kp + CW - 1) / CW;
+    const Group* groups = PHASE == 1 ? a.g1 : a.g2;
+    const int32_t* grow = PHASE == 1 ? a.grow1 : a.grow2;
+    const int64_t* gcsr = PHASE == 1 ? a.gcsr1 : a.gcsr2;
+    const int32_t* sp = PHASE == 1 ? a.s1_ptr : a.s2_ptr;
+    const int32_t* si = PHASE == 1 ? a.s1_items : a.s2_items;
+    const T* vals = static_cast<const T*>(a.vals);
+    const int t = threadIdx.x, tr = t / CW, tc = t % CW;      // epilogue element of this thread
+    for (int32_t q = sp[blockIdx.x]; q < sp[blockIdx.x + 1]; ++q) {
+        const int64_t item = si[q];
+        const int64_t gi = item / nchunk;
+        const int cbase = (int)(item - gi * nchunk) * CW;
+        const Group G = groups[gi];
+        T acc[VEC];
+        group_accumulate<T, VEC>(G, gi, a.gseg, a.gvo, gcsr, a.segs, vals, a.idx, xc, a.kp, cbase + col0,
+                                 cbase + col0 < a.kp, r, acc, warp, kWarps);
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) stile[(warp * kGroup + r) * CW + col0 + v] = (double)acc[v];
+        __syncthreads();
+        const int col = cbase + tc;
+        const bool mine = t < kGroup * CW && tr < G.nrows && col < a.kp;
+        double d2 = 0.0;
+        if (mine) {
+            T q = T(0);
+            for (int w = 0; w < kWarps; ++w) q += (T)stile[(w * kGroup + tr) * CW + tc];
+            const int64_t orow = grow[gi * kGroup + tr];
+            if (PHASE == 1) {
+                xc[(a.N + orow) * a.kp + col] = static_cast<const T*>(a.p1_scale)[orow] * q;
+            } else if (MODE == M_MATVEC) {
+                static_cast<T*>(a.Y)[orow * a.kp + col] = q;
+            } else {
+                const int64_t o = orow * a.kp + col;
+                if (a.clamp) q = q > T(0) ? q : T(0);
+                const T rh = a.rho ? static_cast<const T*>(a.rho)[orow] : T(1);
+                const T bn = __ldcg(static_cast<const T*>(a.E) + o) + rh * q;           // eq. (1)
+                const double d = (double)bn - (double)__ldcg(xc + o);
+                d2 = col < a.k ? d * d : 0.0;
+                xn[o] = bn;
+                static_cast<T*>(a.Q)[o] = q;
+            }
+        }
+        if (PHASE == 2 && MODE == M_SOLVE) {
+            __syncthreads();
+            if (t < kGroup * CW) stile[t] = d2;                  // [row][col]
+            __syncthreads();
+            if (t < CW && cbase + t < a.kp) {
+                double sum = 0.0;
+                for (int rr = 0; rr < kGroup; ++rr) sum += stile[rr * CW + t];
+                sw[cbase + t] += sum;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// The persistent hot-path kernel (a2-a5).  MODE = M_MATVEC: phase 1, grid
+// barrier, phase 2 -> Y.  MODE = M_SOLVE: Jacobi iterations until every
+// column has r <= tol or `iters` is reached.  GROUPED selects the row-group
+// layout (VEC columns per lane) or the per-row layout (KC lanes x VEC).
+template <typename T, int KC, int VEC, int MODE, bool GROUPED>
+__global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a) {
+    extern __shared__ double sred[];        // residual partials
+    __shared__ double stile[GROUPED ? kWarps * kGroup * 2 * VEC : 1];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t kp = a.kp;
+    const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp, nwarp = (int64_t)gridDim.x * kWarps;
+    const unsigned nblk = gridDim.x;
+    const bool have_p1 = GROUPED ? a.n_g1 > 0 : a.n_p1 > 0;
+    int cur = 0;
+    for (int it = 0;; ++it) {
+        T* xc = static_cast<T*>(cur ? a.xt1 : a.xt0);
+        T* xn = static_cast<T*>(cur ? a.xt0 : a.xt1);
+        trace_ev(a, it, 0);
+        if (have_p1) {                                           // ---- phase 1: T rows
+            if (GROUPED) groups_phase<T, VEC, 1, MODE>(a, xc, xn, stile, nullptr);
+            else phase1_rows<T, KC, VEC>(a, xc, gwarp, nwarp, lane);
+        }
+        trace_ev(a, it, 1);
+        if (MODE == M_MATVEC) {
+            if (have_p1) grid_sync(a.ctl, nblk);
+            if (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sred);
+            else phase2_rows<T, KC, VEC, MODE>(a, xc, xn, gwarp, nwarp, lane, sred);
+            return;
+        }
+        grid_sync(a.ctl, nblk);                                  // B1
+        trace_ev(a, it, 2);
+        // a5 decision of iteration it-1 (column reductions finished before B1);
+        // phase 1 above ran speculatively and only touched T rows (scratch).
+        if (it > 0) {
+            const int bad = *(volatile int*)&a.ctl->bad[(it - 1) & 1];
+            if (!bad || it >= a.iters) {
+                if (blockIdx.x == 0 && threadIdx.x == 0) { a.ctl->iter = it; a.ctl->done = 1; }
+                return;
+            }
+        }
+        // ---- phase 2.  Residual partials: per warp [kWarps][kp] (row layout)
+        // or per CTA [kp] (row groups).
+        const int nsw = GROUPED ? 1 : kWarps;
+        double* sw = sred + (GROUPED ? 0 : warp * kp);
+        for (int cc = threadIdx.x; cc < nsw * a.kp; cc += kThreads) sred[cc] = 0.0;
+        __syncthreads();
+        if (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sw);
+        else phase2_rows<T, KC, VEC, MODE>(a, xc, xn, gwarp, nwarp, lane, sw);
+        __syncthreads();
+        double* part = a.partial + (int64_t)(it & 1) * nblk * kp;   // column-major [kp][nblk]
+        for (int cc = threadIdx.x; cc < a.kp; cc += kThreads) {
+            double sum = 0.0;
+            for (int w = 0; w < nsw; ++w) sum += sred[w * kp + cc];
+            part[(int64_t)cc * nblk + blockIdx.x] = sum;
+        }
+        trace_ev(a, it, 3);
+        grid_sync(a.ctl, nblk);                                  // B2
+        trace_ev(a, it, 4);
+        // column c's residual is reduced by warp (c / nblk) of CTA (c % nblk):
+        // lanes over CTAs, all loads in flight, fixed xor tree.
+        for (int c = blockIdx.x + (int)nblk * warp; c < a.k; c += (int)nblk * kWarps) {
+            const double* pc = part + (int64_t)c * nblk;
+            double v[kMaxGrid / 32];
+#pragma unroll
+            for (int i = 0; i < kMaxGrid / 32; ++i) {
+                const unsigned b = lane + 32u * i;
+                v[i] = b < nblk ? __ldcg(pc + b) : 0.0;
+            }
+            double sum = 0.0;
+#pragma unroll
+            for (int i = 0; i < kMaxGrid / 32; ++i) sum += v[i];
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+            if (lane == 0) {
+                const double en = a.enorm2[c];
+                const double rr = en > 0.0 ? sqrt(sum) / sqrt(en) : 0.0;
+                a.resid[c] = rr;
+                if (!(rr <= a.tol)) atomicOr(&a.ctl->bad[it & 1], 1);
+            }
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->bad[(it + 1) & 1] = 0;
+        cur ^= 1;
+    }
+}
+
+// Column sums of squares of V (tree order, N x kp): one CTA per column block
+// of 1 column, fixed-order tree reduction -> out[c].
+template <typename T>
+__global__ void colnorm_kernel(const T* V, int64_t N, int kp, int k, double* out) {
+    const int c = blockIdx.x;
+    if (c >= k) return;
+    __shared__ double sh[kThreads];
+    double s = 0.0;
+    for (int64_t r = threadIdx.x; r < N; r += kThreads) {
+        const double v = (double)V[r * kp + c];
+        s += v * v;
+    }
+    sh[threadIdx.x] = s;
+    __syncthreads();
+    for (int off = kThreads / 2; off > 0; off >>= 1) {
+        if (threadIdx.x < off) sh[threadIdx.x] += sh[threadIdx.x + off];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[c] = sh[0];
 }
 
 // Caller order (column-major N x k, ld N) -> tree order (N x kp, row-major):
 // dst[r, c] = src[perm[r] + c N] * (mul ? mul[perm[r]] : 1); padding columns 0.
-// Writes up to three destinations (for E/B initialisation).
 template <typename T>
 __global__ void permute_in_kernel(const T* src, const int32_t* perm, int64_t N, int k, int kp,
                                   const T* mul, T* d0, T* d1, T* d2, T* raw) {
     __shared__ T tile[32][33];
     const int64_t r0 = (int64_t)blockIdx.x * 32;
     const int c0 = blockIdx.y * 32;
-    // load: threads over rows (gather through perm), loop over 32 columns
     for (int cc = threadIdx.y; cc < 32; cc += blockDim.y) {
         const int64_t r = r0 + threadIdx.x;
         const int c = c0 + cc;
         T v = T(0);
-        if (r < N && c < k) {
-            const int64_t p = perm[r];
-            v = src[p + (int64_t)c * N];
-        }
+        if (r < N && c < k) v = src[(int64_t)perm[r] + (int64_t)c * N];
         tile[threadIdx.x][cc] = v;
     }
     __syncthreads();
@@ -341,7 +659,6 @@ __global__ void permute_out_kernel(const T* src, const int32_t* perm, const uint
     }
 }
 
-// length-N parameter vector, caller order -> tree order
 template <typename T>
 __global__ void gather_vec_kernel(const T* src, const int32_t* perm, int64_t N, T* dst) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x)
@@ -403,6 +720,16 @@ struct DeviceHMat {
     int64_t* p2_segptr = nullptr;
     int32_t* p2_rows = nullptr;
     int64_t n_p2 = 0;
+    // row-group layout (batched right-hand sides)
+    Group* g1 = nullptr;
+    Group* g2 = nullptr;
+    int64_t n_g1 = 0, n_g2 = 0;
+    GSeg* gseg = nullptr;
+    int64_t* gvo = nullptr;
+    int32_t* grow1 = nullptr;
+    int32_t* grow2 = nullptr;
+    int64_t* gcsr1 = nullptr;
+    int64_t* gcsr2 = nullptr;
     int32_t* perm = nullptr;
     uint8_t* active = nullptr;
     int64_t bytes = 0;
@@ -431,18 +758,18 @@ struct DeviceHMat {
     Ctl* ctl_host = nullptr;  // pinned
     double* resid_host = nullptr;
     int resid_host_cap = 0;
+    int device = 0;
+    int last_grid = 0;
+    // work-item costs (terms per unit) for the static LPT schedules
+    std::vector<int64_t> cost_p1, cost_p2, cost_g1, cost_g2;
+    struct Sched { int32_t* ptr = nullptr; int32_t* items = nullptr; };
+    std::map<std::array<int64_t, 4>, Sched> sched;
     // staging for host pointers
     void* stage[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     size_t stage_cap[6] = {0, 0, 0, 0, 0, 0};
 };
 
 namespace {
-
-int grid_rows(int64_t nrows) {
-    int64_t g = (nrows + kWarps - 1) / kWarps;
-    g = std::min<int64_t>(g, (int64_t)kNumSms * kCtasPerSm);
-    return (int)std::max<int64_t>(g, 1);
-}
 
 template <typename T>
 int upload_impl(Handle* h, DeviceHMat* D) {
@@ -595,6 +922,95 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         D->p2_src = std::count(used.begin(), used.end(), 1);
     }
 
+
+    // ---- row-group layout: consecutive rows whose shared segments have the
+    // same sources (phase 1: the q terms of one SVD block; phase 2: rows of one
+    // quadtree leaf range), at most kGroup rows per group.
+    std::vector<Group> g1v, g2v;
+    std::vector<GSeg> gsegv;
+    std::vector<int64_t> gvov, gcsr1v, gcsr2v;
+    std::vector<int32_t> grow1v, grow2v;
+    auto same_src = [](const Seg& x, const Seg& y) { return x.kind == y.kind && x.src == y.src && x.len == y.len; };
+    for (int64_t r = 0; r < (int64_t)p1_rows.size();) {
+        const Seg& s0 = segs[p1_segptr[r]];
+        int64_t e = r + 1;
+        while (e < (int64_t)p1_rows.size() && e - r < kGroup && same_src(segs[p1_segptr[e]], s0)) ++e;
+        Group G{(int32_t)(e - r), 1, (int64_t)gsegv.size()};
+        gsegv.push_back(GSeg{s0.src, s0.len, s0.kind});
+        for (int q = 0; q < kGroup; ++q) {
+            const bool v = r + q < e;
+            gvov.push_back(v ? segs[p1_segptr[r + q]].val_off : 0);
+            grow1v.push_back(v ? p1_rows[r + q] : 0);
+            gcsr1v.push_back(-1);
+        }
+        g1v.push_back(G);
+        r = e;
+    }
+    auto shared_of = [&](int64_t r, std::vector<Seg>& out, int64_t& csr) {
+        out.clear();
+        csr = -1;
+        for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1]; ++q) {
+            if (segs[q].kind == 0) out.push_back(segs[q]);
+            else csr = q;
+        }
+    };
+    std::vector<Seg> sh0, sh1;
+    for (int64_t r = 0; r < (int64_t)p2_rows.size();) {
+        int64_t c0;
+        shared_of(r, sh0, c0);
+        int64_t e = r + 1;
+        while (e < (int64_t)p2_rows.size() && e - r < kGroup) {
+            int64_t c1;
+            shared_of(e, sh1, c1);
+            bool same = sh1.size() == sh0.size();
+            for (size_t q = 0; same && q < sh0.size(); ++q) same = same_src(sh0[q], sh1[q]);
+            if (!same) break;
+            ++e;
+        }
+        Group G{(int32_t)(e - r), (int32_t)sh0.size(), (int64_t)gsegv.size()};
+        for (auto& x : sh0) gsegv.push_back(GSeg{x.src, x.len, x.kind});
+        for (size_t q = 0; q < sh0.size(); ++q)
+            for (int i = 0; i < kGroup; ++i) {
+                int64_t vo = 0;
+                if (r + i < e) {
+                    shared_of(r + i, sh1, c0);
+                    vo = sh1[q].val_off;
+                }
+                gvov.push_back(vo);
+            }
+        for (int i = 0; i < kGroup; ++i) {
+            int64_t c1 = -1;
+            if (r + i < e) shared_of(r + i, sh1, c1);
+            grow2v.push_back(r + i < e ? p2_rows[r + i] : 0);
+            gcsr2v.push_back(c1);
+        }
+        g2v.push_back(G);
+        r = e;
+    }
+    D->n_g1 = (int64_t)g1v.size();
+    D->n_g2 = (int64_t)g2v.size();
+    // static-schedule costs: number of terms a work item sums (+ fixed overhead)
+    auto row_cost = [&](const std::vector<int64_t>& ptr, int64_t r) {
+        int64_t c = 8;
+        for (int64_t q = ptr[r]; q < ptr[r + 1]; ++q) c += segs[q].len;
+        return c;
+    };
+    for (int64_t r = 0; r < (int64_t)p1_rows.size(); ++r) D->cost_p1.push_back(row_cost(p1_segptr, r));
+    for (int64_t r = 0; r < (int64_t)p2_rows.size(); ++r) D->cost_p2.push_back(row_cost(p2_segptr, r));
+    auto group_cost = [&](const Group& G, const std::vector<int64_t>& gcsr, int64_t gi) {
+        int64_t c = 16, mx = 0;
+        for (int q = 0; q < G.nseg; ++q) c += gsegv[G.seg_off + q].len;
+        for (int r = 0; r < G.nrows; ++r) {
+            int64_t cs = gcsr[gi * kGroup + r];
+            if (cs >= 0) mx = std::max<int64_t>(mx, segs[cs].len);
+        }
+        return c + mx;
+    };
+    for (int64_t g = 0; g < D->n_g1; ++g) D->cost_g1.push_back(group_cost(g1v[g], gcsr1v, g));
+    for (int64_t g = 0; g < D->n_g2; ++g) D->cost_g2.push_back(group_cost(g2v[g], gcsr2v, g));
+    if (gsegv.empty()) gsegv.push_back(GSeg{0, 0, 0});
+    if (gvov.empty()) gvov.push_back(0);
+
     auto up = [&](void** dst, const void* src, size_t bytes) -> int {
         if (bytes == 0) bytes = 16;
         CK(cudaMalloc(dst, bytes));
@@ -612,6 +1028,14 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     if ((rc = up((void**)&D->p2_segptr, p2_segptr.data(), p2_segptr.size() * 8))) return rc;
     if ((rc = up((void**)&D->p2_rows, p2_rows.data(), p2_rows.size() * 4))) return rc;
     if ((rc = up((void**)&D->perm, h->perm.data(), h->perm.size() * 4))) return rc;
+    if ((rc = up((void**)&D->g1, g1v.data(), g1v.size() * sizeof(Group)))) return rc;
+    if ((rc = up((void**)&D->g2, g2v.data(), g2v.size() * sizeof(Group)))) return rc;
+    if ((rc = up((void**)&D->gseg, gsegv.data(), gsegv.size() * sizeof(GSeg)))) return rc;
+    if ((rc = up((void**)&D->gvo, gvov.data(), gvov.size() * 8))) return rc;
+    if ((rc = up((void**)&D->grow1, grow1v.data(), grow1v.size() * 4))) return rc;
+    if ((rc = up((void**)&D->grow2, grow2v.data(), grow2v.size() * 4))) return rc;
+    if ((rc = up((void**)&D->gcsr1, gcsr1v.data(), gcsr1v.size() * 8))) return rc;
+    if ((rc = up((void**)&D->gcsr2, gcsr2v.data(), gcsr2v.size() * 8))) return rc;
     if ((rc = up((void**)&D->active, active.data(), active.size()))) return rc;
     CK(cudaMalloc((void**)&D->ctl, sizeof(Ctl)));
     CK(cudaMallocHost((void**)&D->ctl_host, sizeof(Ctl)));
@@ -621,62 +1045,22 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     return VF_OK;
 }
 
-int ensure_scratch(DeviceHMat* D, int kp) {
-    if (kp <= D->kp_cap) return VF_OK;
-    void** bufs[] = {&D->xt[0], &D->xt[1], &D->Ep, &D->Qp, &D->Qdp, &D->Qvp, &D->Yp, &D->Qip};
-    for (void** b : bufs) if (*b) { cudaFree(*b); *b = nullptr; }
-    for (void*& b : D->pv) if (b) { cudaFree(b); b = nullptr; }
-    const size_t rows_x = (size_t)(D->N + D->NT), rows = (size_t)D->N;
-    for (int i = 0; i < 2; ++i) {
-        CK(cudaMalloc(&D->xt[i], std::max<size_t>(16, rows_x * kp * D->w)));
-        CK(cudaMemset(D->xt[i], 0, std::max<size_t>(16, rows_x * kp * D->w)));
-    }
-    void** vbufs[] = {&D->Ep, &D->Qp, &D->Qdp, &D->Qvp, &D->Yp, &D->Qip};
-    for (void** b : vbufs) {
-        CK(cudaMalloc(b, std::max<size_t>(16, rows * kp * D->w)));
-        CK(cudaMemset(*b, 0, std::max<size_t>(16, rows * kp * D->w)));
-    }
-    for (void*& b : D->pv) CK(cudaMalloc(&b, std::max<size_t>(16, rows * D->w)));
-    const int64_t nblk = (int64_t)kNumSms * kCtasPerSm;
-    if (D->partial) cudaFree(D->partial);
-    CK(cudaMalloc((void**)&D->partial, (size_t)nblk * kp * 8));
-    CK(cudaMemset(D->partial, 0, (size_t)nblk * kp * 8));
-    if (D->enorm2) cudaFree(D->enorm2);
-    if (D->resid) cudaFree(D->resid);
-    CK(cudaMalloc((void**)&D->enorm2, (size_t)kp * 8));
-    CK(cudaMalloc((void**)&D->resid, (size_t)kp * 8));
-    if (D->resid_host) cudaFreeHost(D->resid_host);
-    CK(cudaMallocHost((void**)&D->resid_host, (size_t)kp * 8));
-    D->kp_cap = kp;
-    return VF_OK;
-}
+}  // namespace
 
+namespace {
+
+// nrhs <= 2: per-row layout, kp = k.  Otherwise the row-group layout: kp a
+// multiple of its column tile (2 VEC).
 int pad_k(int k) {
     if (k <= 2) return k;
-    return (k + 3) & ~3;
+    if (k <= 4) return 4;
+    if (k <= 8) return 8;
+    return (k + 15) & ~15;
 }
 
-// ---------------------------------------------------------- launching
-template <typename T, int MODE>
-void launch_segrow(const RowArgs& a, int kp, cudaStream_t st, int* nblk_out) {
-    const int grid = grid_rows(a.nrows);
-    if (nblk_out) *nblk_out = grid;
-    auto go = [&](auto kern, int cw) {
-        dim3 g(grid, (kp + cw - 1) / cw);
-        kern<<<g, kWarps * 32, 0, st>>>(a);
-    };
-    if (kp == 1) go(segrow_kernel<T, 1, 1, MODE>, 1);
-    else if (kp == 2) go(segrow_kernel<T, 1, 2, MODE>, 2);
-    else if (kp <= 4) go(segrow_kernel<T, 1, 4, MODE>, 4);
-    else if (kp <= 8) go(segrow_kernel<T, 2, 4, MODE>, 8);
-    else if (kp <= 16) go(segrow_kernel<T, 4, 4, MODE>, 16);
-    else if (kp <= 32) go(segrow_kernel<T, 8, 4, MODE>, 32);
-    else if (kp <= 64) go(segrow_kernel<T, 16, 4, MODE>, 64);
-    else go(segrow_kernel<T, 32, 4, MODE>, 128);
-}
-
-// Records a CUDA event pair around one phase launch on the launching stream
-// (no synchronisation); collect_timing() reads them after the call's final sync.
+// Records a CUDA event pair around one hot-kernel launch on the launching
+// stream (no synchronisation); collect_timing() reads them after the call's
+// final synchronisation.
 struct Timer {
     Handle* h;
     cudaStream_t st;
@@ -711,32 +1095,36 @@ void reset_counters(Handle* h) {
     h->dev->evused = 0;
 }
 
-// One F-hat apply of XT[src] (phases 1 and 2).
-template <typename T, int MODE>
-int apply_once(Handle* h, int src, int kp, cudaStream_t st, void* out, const void* E, const void* rho, int clamp,
-               int* nblk2) {
-    DeviceHMat* D = h->dev;
-    if (D->n_p1 > 0) {
-        RowArgs a{};
-        a.segptr = D->p1_segptr; a.segs = D->segs; a.rows = D->p1_rows; a.nrows = D->n_p1;
-        a.vals = D->vals; a.idx = D->idx; a.scale = D->p1_scale;
-        a.xt = D->xt[src]; a.out = D->xt[src];
-        a.ctl = D->ctl; a.N = D->N; a.kp = kp;
-        Timer tm(h, st, 1);
-        launch_segrow<T, M_PHASE1>(a, kp, st, nullptr);
-        h->launches_total++;
+int ensure_scratch(DeviceHMat* D, int kp) {
+    if (kp <= D->kp_cap) return VF_OK;
+    void** bufs[] = {&D->xt[0], &D->xt[1], &D->Ep, &D->Qp, &D->Qdp, &D->Qvp, &D->Yp, &D->Qip};
+    for (void** b : bufs) if (*b) { cudaFree(*b); *b = nullptr; }
+    for (void*& b : D->pv) if (b) { cudaFree(b); b = nullptr; }
+    const size_t rows_x = (size_t)(D->N + D->NT), rows = (size_t)D->N;
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaMalloc(&D->xt[i], std::max<size_t>(16, rows_x * kp * D->w)));
+        CK(cudaMemset(D->xt[i], 0, std::max<size_t>(16, rows_x * kp * D->w)));
     }
-    RowArgs a{};
-    a.segptr = D->p2_segptr; a.segs = D->segs; a.rows = D->p2_rows; a.nrows = D->n_p2;
-    a.vals = D->vals; a.idx = D->idx;
-    a.xt = D->xt[src]; a.out = out;
-    a.E = E; a.rho = rho; a.Q = D->Qp; a.partial = D->partial;
-    a.ctl = D->ctl; a.N = D->N; a.kp = kp; a.clamp = clamp;
-    {
-        Timer tm(h, st, 2);
-        launch_segrow<T, MODE>(a, kp, st, nblk2);
+    void** vbufs[] = {&D->Ep, &D->Qp, &D->Qdp, &D->Qvp, &D->Yp, &D->Qip};
+    for (void** b : vbufs) {
+        CK(cudaMalloc(b, std::max<size_t>(16, rows * kp * D->w)));
+        CK(cudaMemset(*b, 0, std::max<size_t>(16, rows * kp * D->w)));
     }
-    h->launches_total++;
+    for (void*& b : D->pv) CK(cudaMalloc(&b, std::max<size_t>(16, rows * D->w)));
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, D->device);
+    const int64_t nblk = (int64_t)nsm * kMaxCtasPerSm;
+    if (D->partial) cudaFree(D->partial);
+    CK(cudaMalloc((void**)&D->partial, (size_t)2 * nblk * kp * 8));
+    CK(cudaMemset(D->partial, 0, (size_t)2 * nblk * kp * 8));
+    if (D->enorm2) cudaFree(D->enorm2);
+    if (D->resid) cudaFree(D->resid);
+    CK(cudaMalloc((void**)&D->enorm2, (size_t)kp * 8));
+    CK(cudaMalloc((void**)&D->resid, (size_t)kp * 8));
+    CK(cudaMemset(D->resid, 0, (size_t)kp * 8));
+    if (D->resid_host) cudaFreeHost(D->resid_host);
+    CK(cudaMallocHost((void**)&D->resid_host, (size_t)kp * 8));
+    D->kp_cap = kp;
     return VF_OK;
 }
 
@@ -753,7 +1141,6 @@ bool is_device_ptr(const void* p) {
     return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
-// Stage a host pointer into a handle buffer (slot) when needed.
 int stage_in(Handle* h, int slot, const void* p, size_t bytes, cudaStream_t st, const void** out) {
     if (!p || is_device_ptr(p)) { *out = p; return VF_OK; }
     DeviceHMat* D = h->dev;
@@ -807,43 +1194,152 @@ void launch_permute_out(Handle* h, const void* src, int k, int kp, bool use_acti
 template <typename T>
 void launch_colnorm(Handle* h, const void* V, int k, int kp, cudaStream_t st) {
     DeviceHMat* D = h->dev;
-    const int nblk = 148;
-    colnorm_partial_kernel<T><<<nblk, 256, kp * sizeof(double), st>>>((const T*)V, D->N, kp, D->partial);
-    colnorm_final_kernel<<<1, 256, 0, st>>>(D->partial, nblk, kp, k, D->enorm2);
-    h->launches_total += 2;
+    colnorm_kernel<T><<<k, kThreads, 0, st>>>((const T*)V, D->N, kp, k, D->enorm2);
+    h->launches_total++;
 }
 
-// Jacobi iterations on the current XT/E/rho state until ctl->done.
+// Longest-processing-time-first static schedule of nunits x nchunk items
+// onto nworkers workers (deterministic: ties broken by index).  Cached per
+// (phase, layout, nchunk, nworkers).
+int get_sched(DeviceHMat* D, int phase, bool grouped, int nchunk, int nworkers, DeviceHMat::Sched* out) {
+    std::array<int64_t, 4> key{phase, grouped ? 1 : 0, nchunk, nworkers};
+    auto it = D->sched.find(key);
+    if (it != D->sched.end()) { *out = it->second; return VF_OK; }
+    const std::vector<int64_t>& cu = grouped ? (phase == 1 ? D->cost_g1 : D->cost_g2) : (phase == 1 ? D->cost_p1 : D->cost_p2);
+    const int64_t nitems = (int64_t)cu.size() * nchunk;
+    if (nitems >= INT32_MAX) return set_error(VF_EUNSUPPORTED, "too many work items");
+    std::vector<int32_t> order(nitems);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return cu[x / nchunk] > cu[y / nchunk]; });
+    using E = std::pair<int64_t, int32_t>;           // (load, worker)
+    std::priority_queue<E, std::vector<E>, std::greater<E>> pq;
+    for (int32_t w = 0; w < nworkers; ++w) pq.push({0, w});
+    std::vector<std::vector<int32_t>> lists(nworkers);
+    for (int32_t itm : order) {
+        E e = pq.top();
+        pq.pop();
+        lists[e.second].push_back(itm);
+        pq.push({e.first + cu[itm / nchunk], e.second});
+    }
+    std::vector<int32_t> ptr(nworkers + 1, 0), items;
+    items.reserve(nitems);
+    for (int32_t w = 0; w < nworkers; ++w) {
+        std::sort(lists[w].begin(), lists[w].end());
+        items.insert(items.end(), lists[w].begin(), lists[w].end());
+        ptr[w + 1] = (int32_t)items.size();
+    }
+    if (items.empty()) items.push_back(0);
+    DeviceHMat::Sched sc;
+    CK(cudaMalloc((void**)&sc.ptr, ptr.size() * 4));
+    CK(cudaMalloc((void**)&sc.items, items.size() * 4));
+    CK(cudaMemcpy(sc.ptr, ptr.data(), ptr.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(sc.items, items.data(), items.size() * 4, cudaMemcpyHostToDevice));
+    D->sched[key] = sc;
+    *out = sc;
+    return VF_OK;
+}
+
+// Cooperative launch of the persistent hot kernel; grid = SMs x resident CTAs.
+template <typename T, int KC, int VEC, int MODE, bool GROUPED>
+int launch_hot_t(Handle* h, HotArgs& a, cudaStream_t st) {
+    DeviceHMat* D = h->dev;
+    auto fn = hot_kernel<T, KC, VEC, MODE, GROUPED>;
+    const size_t smem = MODE == M_SOLVE ? (size_t)(GROUPED ? 1 : kWarps) * a.kp * sizeof(double) : 0;
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
+    if (per_sm < 1) return set_error(VF_ECUDA, "hot kernel cannot be resident");
+    int nsm = 148;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
+    const int grid = std::min(kMaxGrid, nsm * std::min(per_sm, kMaxCtasPerSm));
+    const int cw = GROUPED ? 2 * VEC : KC * VEC;
+    const int nchunk = (a.kp + cw - 1) / cw;
+    const int nworkers = GROUPED ? grid : grid * kWarps;
+    DeviceHMat::Sched s1, s2;
+    int rc;
+    if ((rc = get_sched(D, 1, GROUPED, nchunk, nworkers, &s1)) || (rc = get_sched(D, 2, GROUPED, nchunk, nworkers, &s2)))
+        return rc;
+    a.s1_ptr = s1.ptr; a.s1_items = s1.items; a.s2_ptr = s2.ptr; a.s2_items = s2.items;
+    static const char* trace_file = getenv("VF_TRACE_FILE");
+    unsigned long long* tbuf = nullptr;
+    const int tit = 64;
+    if (trace_file && MODE == M_SOLVE) {
+        CK(cudaMalloc(&tbuf, (size_t)tit * 5 * grid * 8));
+        CK(cudaMemsetAsync(tbuf, 0, (size_t)tit * 5 * grid * 8, st));
+        a.trace = tbuf;
+        a.trace_iters = tit;
+    }
+    void* args[] = {&a};
+    CK(cudaMemsetAsync(a.ctl, 0, offsetof(Ctl, bar_gen), st));       // iter, done, bad, bar_arrive
+    {
+        Timer tm(h, st, 2);
+        CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kThreads), args, smem, st));
+    }
+    h->launches_total++;
+    D->last_grid = grid;
+    if (tbuf) {
+        std::vector<unsigned long long> hb((size_t)tit * 5 * grid);
+        CK(cudaMemcpyAsync(hb.data(), tbuf, hb.size() * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        cudaFree(tbuf);
+        a.trace = nullptr;
+        if (FILE* f = fopen(trace_file, "ab")) {
+            int32_t hdr[4] = {grid, tit, (int32_t)a.kp, GROUPED ? 1 : 0};
+            fwrite(hdr, 4, 4, f);
+            fwrite(hb.data(), 8, hb.size(), f);
+            fclose(f);
+        }
+    }
+    return VF_OK;
+}
+
+template <typename T, int MODE>
+int launch_hot(Handle* h, HotArgs& a, cudaStream_t st) {
+    const int kp = a.kp;
+    if (kp == 1) return launch_hot_t<T, 1, 1, MODE, false>(h, a, st);
+    if (kp == 2) return launch_hot_t<T, 1, 2, MODE, false>(h, a, st);
+    if (kp == 4) return launch_hot_t<T, 1, 2, MODE, true>(h, a, st);
+    if (kp == 8) return launch_hot_t<T, 1, 4, MODE, true>(h, a, st);
+    return launch_hot_t<T, 1, 8, MODE, true>(h, a, st);
+}
+
+HotArgs hot_args(DeviceHMat* D, int kp, int k) {
+    HotArgs a{};
+    a.p1_segptr = D->p1_segptr; a.p1_rows = D->p1_rows; a.n_p1 = D->n_p1; a.p1_scale = D->p1_scale;
+    a.p2_segptr = D->p2_segptr; a.p2_rows = D->p2_rows; a.n_p2 = D->n_p2;
+    a.g1 = D->g1; a.n_g1 = D->n_g1; a.g2 = D->g2; a.n_g2 = D->n_g2;
+    a.gseg = D->gseg; a.gvo = D->gvo; a.grow1 = D->grow1; a.grow2 = D->grow2; a.gcsr1 = D->gcsr1; a.gcsr2 = D->gcsr2;
+    a.segs = D->segs; a.vals = D->vals; a.idx = D->idx;
+    a.xt0 = D->xt[0]; a.xt1 = D->xt[1];
+    a.partial = D->partial; a.enorm2 = D->enorm2; a.resid = D->resid; a.ctl = D->ctl;
+    a.N = D->N; a.kp = kp; a.k = k;
+    return a;
+}
+
+// One Jacobi solve on the current XT/E state: one persistent launch.
 template <typename T>
 int iterate(Handle* h, int k, int kp, const void* rho, int clamp, int iters, double tol, cudaStream_t st,
             int* iters_done, double* max_resid) {
     DeviceHMat* D = h->dev;
-    CK(cudaMemsetAsync(D->ctl, 0, sizeof(Ctl), st));
     *iters_done = 0;
     *max_resid = 0;
     if (iters <= 0) return VF_OK;
-    int enq = 0, chunk = 2;
-    while (true) {
-        for (int c = 0; c < chunk && enq < iters; ++c, ++enq) {
-            const int src = enq & 1;     // == ctl->iter & 1 while not done
-            int nblk = 1;
-            int rc = apply_once<T, M_SOLVE>(h, src, kp, st, D->xt[src ^ 1], D->Ep, rho, clamp, &nblk);
-            if (rc) return rc;
-            reduce_kernel<<<1, 256, 0, st>>>(D->partial, nblk, kp, k, D->enorm2, D->resid, D->ctl, iters, tol);
-            h->launches_total++;
-        }
-        CK(cudaGetLastError());
-        CK(cudaMemcpyAsync(D->ctl_host, D->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-        CK(cudaStreamSynchronize(st));
-        if (D->ctl_host->done || enq >= iters) break;
-        chunk = std::min(chunk * 2, 16);
-    }
-    *iters_done = D->ctl_host->iter;
+    HotArgs a = hot_args(D, kp, k);
+    a.E = D->Ep; a.rho = rho; a.Q = D->Qp; a.iters = iters; a.clamp = clamp; a.tol = tol;
+    int rc = launch_hot<T, M_SOLVE>(h, a, st);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(D->ctl_host, D->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(D->resid_host, D->resid, (size_t)k * 8, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    *iters_done = D->ctl_host->iter;
     double mr = 0;
     for (int c = 0; c < k; ++c) mr = std::max(mr, D->resid_host[c]);
     *max_resid = mr;
+    return VF_OK;
+}
+
+int check_k(int nrhs) {
+    if (nrhs > kMaxKp) return set_error(VF_EUNSUPPORTED, "nrhs > 2048 per call: split the batch");
     return VF_OK;
 }
 
@@ -852,7 +1348,7 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     DeviceHMat* D = h->dev;
     cudaStream_t st;
     int rc;
-    if ((rc = stream_of(h, &st))) return rc;
+    if ((rc = check_k(nrhs)) || (rc = stream_of(h, &st))) return rc;
     const int kp = pad_k(nrhs);
     if ((rc = ensure_scratch(D, kp))) return rc;
     reset_counters(h);
@@ -861,9 +1357,10 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     void* Yd;
     if ((rc = stage_in(h, 0, X, vb, st, &Xd))) return rc;
     if ((rc = stage_out_buf(h, 1, Y, vb, &Yd))) return rc;
-    CK(cudaMemsetAsync(D->ctl, 0, sizeof(Ctl), st));
     launch_permute_in<T>(h, Xd, nrhs, kp, nullptr, D->xt[0], nullptr, nullptr, nullptr, st);
-    if ((rc = apply_once<T, M_MATVEC>(h, 0, kp, st, D->Yp, nullptr, nullptr, 0, nullptr))) return rc;
+    HotArgs a = hot_args(D, kp, nrhs);
+    a.Y = D->Yp;
+    if ((rc = launch_hot<T, M_MATVEC>(h, a, st))) return rc;
     launch_permute_out<T>(h, D->Yp, nrhs, kp, true, Yd, st);
     CK(cudaGetLastError());
     if ((rc = stage_out_copy(Y, Yd, vb, st))) return rc;
@@ -877,7 +1374,7 @@ int radiosity_impl(Handle* h, const void* E, const void* rho, void* B, int nrhs,
     DeviceHMat* D = h->dev;
     cudaStream_t st;
     int rc;
-    if ((rc = stream_of(h, &st))) return rc;
+    if ((rc = check_k(nrhs)) || (rc = stream_of(h, &st))) return rc;
     const int kp = pad_k(nrhs);
     if ((rc = ensure_scratch(D, kp))) return rc;
     reset_counters(h);
@@ -910,7 +1407,7 @@ int thermal_impl(Handle* h, const void* Qdir, const void* alb, const void* emi, 
     DeviceHMat* D = h->dev;
     cudaStream_t st;
     int rc;
-    if ((rc = stream_of(h, &st))) return rc;
+    if ((rc = check_k(nrhs)) || (rc = stream_of(h, &st))) return rc;
     const int kp = pad_k(nrhs);
     if ((rc = ensure_scratch(D, kp))) return rc;
     reset_counters(h);
@@ -936,15 +1433,14 @@ int thermal_impl(Handle* h, const void* Qdir, const void* alb, const void* emi, 
     if ((rc = iterate<T>(h, nrhs, kp, alpha, 1, iters, tol, st, &it1, &r1))) return rc;
     // stage 2: Qvis = Qdir + Qrefl, E = (1 - alpha) Qvis, rho = 1
     const int64_t tot = D->N * kp;
-    const int gb = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
-    thermal_mid_kernel<T><<<std::max(gb, 1), 256, 0, st>>>((const T*)D->Qdp, (const T*)D->Qp, D->active, alpha, D->N,
-                                                          nrhs, kp, (T*)D->Qvp, (T*)D->Ep, (T*)D->xt[0],
-                                                          (T*)D->xt[1]);
+    const int gb = (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, 148 * 8));
+    thermal_mid_kernel<T><<<gb, 256, 0, st>>>((const T*)D->Qdp, (const T*)D->Qp, D->active, alpha, D->N, nrhs, kp,
+                                              (T*)D->Qvp, (T*)D->Ep, (T*)D->xt[0], (T*)D->xt[1]);
     h->launches_total++;
     launch_colnorm<T>(h, D->Ep, nrhs, kp, st);
     if ((rc = iterate<T>(h, nrhs, kp, nullptr, 1, iters, tol, st, &it2, &r2))) return rc;
-    thermal_T_kernel<T><<<std::max(gb, 1), 256, 0, st>>>((const T*)D->Qvp, (const T*)D->Qp, D->active, alpha, emis,
-                                                        D->N, nrhs, kp, (T*)D->Yp, (T*)D->Qip);
+    thermal_T_kernel<T><<<gb, 256, 0, st>>>((const T*)D->Qvp, (const T*)D->Qp, D->active, alpha, emis, D->N, nrhs,
+                                            kp, (T*)D->Yp, (T*)D->Qip);
     h->launches_total++;
     launch_permute_out<T>(h, D->Yp, nrhs, kp, false, Td, st);
     if (Qvd) launch_permute_out<T>(h, D->Qvp, nrhs, kp, false, Qvd, st);
@@ -973,9 +1469,11 @@ int device_upload(Handle* h, int device) {
     cudaDeviceProp prop;
     CK(cudaGetDeviceProperties(&prop, device));
     if (prop.major != 10) return set_error(VF_ENODEV, "libvf is built for sm_100a (B200); device is not sm_100");
+    if (!prop.cooperativeLaunch) return set_error(VF_ENODEV, "device does not support cooperative launch");
     CK(cudaSetDevice(device));
     if (h->dev) device_free(h);
     h->dev = new DeviceHMat();
+    h->dev->device = device;
     h->device = device;
     int rc = h->dtype == VF_F64 ? upload_impl<double>(h, h->dev) : upload_impl<float>(h, h->dev);
     if (rc) { device_free(h); h->device = -1; }
@@ -987,13 +1485,15 @@ void device_free(Handle* h) {
     if (!D) return;
     cudaSetDevice(h->device);
     void* ptrs[] = {D->vals, D->idx, D->segs, D->p1_segptr, D->p1_rows, D->p1_scale, D->p2_segptr, D->p2_rows,
-                    D->perm, D->active, D->xt[0], D->xt[1], D->Ep, D->Qp, D->Qdp, D->Qvp, D->Yp, D->Qip,
+                    D->perm, D->active, D->g1, D->g2, D->gseg, D->gvo, D->grow1, D->grow2, D->gcsr1, D->gcsr2,
+                    D->xt[0], D->xt[1], D->Ep, D->Qp, D->Qdp, D->Qvp, D->Yp, D->Qip,
                     D->pv[0], D->pv[1], D->pv[2], D->partial, D->enorm2, D->resid, D->ctl,
                     D->stage[0], D->stage[1], D->stage[2], D->stage[3], D->stage[4], D->stage[5]};
     for (void* p : ptrs) if (p) cudaFree(p);
     if (D->ctl_host) cudaFreeHost(D->ctl_host);
     if (D->resid_host) cudaFreeHost(D->resid_host);
     for (auto& e : D->evpool) if (e) cudaEventDestroy(e);
+    for (auto& kv : D->sched) { cudaFree(kv.second.ptr); cudaFree(kv.second.items); }
     delete D;
     h->dev = nullptr;
 }
@@ -1018,11 +1518,11 @@ int64_t device_bytes(const Handle* h) { return h->dev ? h->dev->bytes : 0; }
 int64_t device_alg_bytes(const Handle* h) { return h->dev ? h->dev->alg_bytes : -1; }
 int64_t device_alg_flops(const Handle* h) { return h->dev ? h->dev->alg_flops_per_col : -1; }
 int64_t device_active_rows(const Handle* h) { return h->dev ? h->dev->n_p2 : -1; }
-void device_phase_info(const Handle* h, int64_t* out7) {
+void device_phase_info(const Handle* h, int64_t* out9) {
     const DeviceHMat* D = h->dev;
-    if (!D) { for (int i = 0; i < 7; ++i) out7[i] = 0; return; }
-    out7[0] = D->NT; out7[1] = D->p1_bytes; out7[2] = D->p2_bytes; out7[3] = D->p1_src; out7[4] = D->p2_src;
-    out7[5] = D->p1_flops; out7[6] = D->p2_flops;
+    if (!D) { for (int i = 0; i < 9; ++i) out9[i] = 0; return; }
+    out9[0] = D->NT; out9[1] = D->p1_bytes; out9[2] = D->p2_bytes; out9[3] = D->p1_src; out9[4] = D->p2_src;
+    out9[5] = D->p1_flops; out9[6] = D->p2_flops; out9[7] = D->n_g1; out9[8] = D->n_g2;
 }
 
 }  // namespace vf
