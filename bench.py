@@ -149,7 +149,7 @@ def oracle_sample(V, F, suns, ncols, budget_s):
     alb, emi = np.full(S.N, ALBEDO), np.full(S.N, EMISS)
     applies, t = 0, 0.0
     reps = 0
-    while t < budget_s and reps < 50:
+    while t < budget_s and reps < 5000:
         t0 = time.perf_counter()
         out = oracle.thermal(lambda X: oracle.apply_csr(csr, X), Q, alb, emi, TOL_SOLVE["f64"], 100)
         t += time.perf_counter() - t0
