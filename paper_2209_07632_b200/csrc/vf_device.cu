@@ -435,6 +435,112 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
     }
 }
 
+// ---- cp.async helpers (Ampere+ async global->shared copies; LDGSTS in SASS)
+template <int CP>
+__device__ __forceinline__ void cpa(void* sdst, const void* gsrc, int src_bytes) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(sdst));
+    if (CP == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(gsrc), "r"(src_bytes));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2, %3;\n" ::"r"(d), "l"(gsrc), "n"(CP), "r"(src_bytes));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+constexpr int kJC = 64;      // terms per staged chunk
+constexpr int kStages = 3;   // cp.async ring depth
+constexpr int kMaxSegSmem = 64;  // shared runs per group whose metadata is cached in smem
+
+template <typename T>
+__host__ __device__ constexpr int wstride() { return kJC + 16 / (int)sizeof(T); }   // padded W row (16-B aligned)
+template <typename T, int VEC>
+__host__ __device__ constexpr int stage_elems() { return kGroup * wstride<T>() + kJC * 2 * VEC; }
+// dynamic smem bytes of the row-group kernel besides the residual partials
+template <typename T, int VEC>
+__host__ __device__ constexpr int stage_bytes() {
+    return kStages * stage_elems<T, VEC>() * (int)sizeof(T) + kMaxSegSmem * (kGroup * 8 + 16);
+}
+
+// Shared-segment part of a row group, staged through shared memory: chunks of
+// kJC terms of every shared run; per chunk the kGroup rows' values (Ws[r][j],
+// rows padded by 16 B) and the source rows' 2 VEC columns (Xs[j][c]) are
+// copied with 16-byte cp.async into a kStages-deep ring, then warp w
+// accumulates the chunk's terms j in [w kJC/8, (w+1) kJC/8) for its (row r,
+// half h) lane.  Zero-filled tails contribute exact zeros.  The group's run
+// descriptors and per-row value offsets are cached in smem once per item.
+template <typename T, int VEC>
+__device__ __forceinline__ void group_shared_staged(const Group& G, const GSeg* __restrict__ gseg,
+                                                    const int64_t* __restrict__ gvo, const T* __restrict__ vals,
+                                                    const int32_t* __restrict__ idx, const T* xt, int64_t kp,
+                                                    int cbase, int r, int h, T* acc, T* stage) {
+    constexpr int CW = 2 * VEC;
+    constexpr int EPL = 16 / (int)sizeof(T);
+    constexpr int XU = CW / EPL;                 // 16-B units per staged source row
+    constexpr int WU = kJC / EPL;                // 16-B units per staged value row
+    constexpr int WSTR = wstride<T>();
+    constexpr int WS = kGroup * WSTR, SE = stage_elems<T, VEC>();
+    constexpr int JW = kJC / kWarps;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    // metadata cache (after the stage ring)
+    int64_t* m_vo = reinterpret_cast<int64_t*>(stage + kStages * SE);          // [kMaxSegSmem][kGroup]
+    GSeg* m_seg = reinterpret_cast<GSeg*>(m_vo + kMaxSegSmem * kGroup);       // [kMaxSegSmem]
+    const bool cached = G.nseg <= kMaxSegSmem;
+    if (cached) {
+        for (int e = tid; e < G.nseg * kGroup; e += kThreads) m_vo[e] = gvo[G.seg_off * kGroup + e];
+        for (int e = tid; e < G.nseg; e += kThreads) m_seg[e] = gseg[G.seg_off + e];
+        __syncthreads();
+    }
+    const GSeg* sgp = cached ? m_seg : gseg + G.seg_off;
+    const int64_t* vop = cached ? m_vo : gvo + G.seg_off * kGroup;
+    int nch = 0;
+    for (int s = 0; s < G.nseg; ++s) nch += (sgp[s].len + kJC - 1) / kJC;
+    int is = 0, ij = 0;                          // issue cursor (segment, first term)
+    auto issue = [&](int st) {
+        while (is < G.nseg && ij >= sgp[is].len) { ++is; ij = 0; }
+        const GSeg sg = sgp[is];
+        T* Ws = stage + st * SE;
+        T* Xs = Ws + WS;
+        for (int u = tid; u < kJC * XU; u += kThreads) {
+            const int jj = u / XU, cu = u - jj * XU, j = ij + jj;
+            const bool ok = j < sg.len;
+            const int64_t row = ok ? (sg.kind ? (int64_t)__ldg(idx + sg.src + j) : sg.src + j) : 0;
+            cpa<16>(Xs + jj * CW + cu * EPL, xt + row * kp + cbase + cu * EPL, ok ? 16 : 0);
+        }
+        const int64_t* vo = vop + is * kGroup;
+        for (int u = tid; u < kGroup * WU; u += kThreads) {
+            const int rr = u / WU, ju = u - rr * WU, j = ij + ju * EPL;
+            const int nval = rr < G.nrows ? min(EPL, sg.len - j) : 0;
+            const bool ok = nval > 0;
+            cpa<16>(Ws + rr * WSTR + ju * EPL, ok ? vals + vo[rr] + j : vals, ok ? nval * (int)sizeof(T) : 0);
+        }
+        ij += kJC;
+    };
+#pragma unroll
+    for (int p = 0; p < kStages - 1; ++p) {
+        if (p < nch) issue(p);
+        cpa_commit();
+    }
+    for (int c = 0; c < nch; ++c) {
+        cpa_wait<kStages - 2>();
+        __syncthreads();
+        if (c + kStages - 1 < nch) issue((c + kStages - 1) % kStages);
+        cpa_commit();
+        const T* Ws = stage + (c % kStages) * SE;
+        const T* Xs = Ws + WS;
+#pragma unroll
+        for (int q = 0; q < JW; ++q) {
+            const int jj = warp * JW + q;
+            const T wv = Ws[r * WSTR + jj];
+            const T* xr = Xs + jj * CW + h * VEC;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) acc[v] = fma(wv, xr[v], acc[v]);
+        }
+    }
+    cpa_wait<0>();
+    __syncthreads();
+}
+
 // Row-group phases (a2, a3 + a4).  One CTA per (group, 2 VEC-column chunk):
 // its 8 warps split the shared term range (warp w takes every 8th run of U
 // terms), each computing a kGroup x (2 VEC) partial tile; the tiles are
@@ -442,7 +548,7 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
 // thread per tile element.  PHASE 1 writes S_t * tile into the T rows of XT.
 // sw: per-CTA residual partials [kp] (phase 2, solve mode).
 template <typename T, int VEC, int PHASE, int MODE>
-__device__ __forceinline__ void groups_phase(const HotArgs& a, T* xc, T* xn, double* stile, double* sw) {
+__device__ __forceinline__ void groups_phase(const HotArgs& a, T* xc, T* xn, double* stile, double* sw, T* stage) {
     constexpr int CW = 2 * VEC;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int r = lane >> 1, col0 = (lane & 1) * VEC;
@@ -460,8 +566,11 @@ __device__ __forceinline__ void groups_phase(const HotArgs& a, T* xc, T* xn, dou
         const int cbase = (int)(item - gi * nchunk) * CW;
         const Group G = groups[gi];
         T acc[VEC];
-        group_accumulate<T, VEC>(G, gi, a.gseg, a.gvo, gcsr, a.segs, vals, a.idx, xc, a.kp, cbase + col0,
+        Group Gc = G;
+        Gc.nseg = 0;                                            // the rows' CSR runs (global gathers)
+        group_accumulate<T, VEC>(Gc, gi, a.gseg, a.gvo, gcsr, a.segs, vals, a.idx, xc, a.kp, cbase + col0,
                                  cbase + col0 < a.kp, r, acc, warp, kWarps);
+        group_shared_staged<T, VEC>(G, a.gseg, a.gvo, vals, a.idx, xc, a.kp, cbase, r, lane & 1, acc, stage);
 #pragma unroll
         for (int v = 0; v < VEC; ++v) stile[(warp * kGroup + r) * CW + col0 + v] = (double)acc[v];
         __syncthreads();
@@ -507,8 +616,9 @@ __device__ __forceinline__ void groups_phase(const HotArgs& a, T* xc, T* xn, dou
 // layout (VEC columns per lane) or the per-row layout (KC lanes x VEC).
 template <typename T, int KC, int VEC, int MODE, bool GROUPED>
 __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a) {
-    extern __shared__ double sred[];        // residual partials
+    extern __shared__ double sred[];        // [residual partials | cp.async stage ring (row groups)]
     __shared__ double stile[GROUPED ? kWarps * kGroup * 2 * VEC : 1];
+    T* stage = reinterpret_cast<T*>(sred + ((a.kp + 1) & ~1));
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t kp = a.kp;
     const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp, nwarp = (int64_t)gridDim.x * kWarps;
@@ -520,13 +630,13 @@ __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a)
         T* xn = static_cast<T*>(cur ? a.xt0 : a.xt1);
         trace_ev(a, it, 0);
         if (have_p1) {                                           // ---- phase 1: T rows
-            if (GROUPED) groups_phase<T, VEC, 1, MODE>(a, xc, xn, stile, nullptr);
+            if (GROUPED) groups_phase<T, VEC, 1, MODE>(a, xc, xn, stile, nullptr, stage);
             else phase1_rows<T, KC, VEC>(a, xc, gwarp, nwarp, lane);
         }
         trace_ev(a, it, 1);
         if (MODE == M_MATVEC) {
             if (have_p1) grid_sync(a.ctl, nblk);
-            if (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sred);
+            if (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sred, stage);
             else phase2_rows<T, KC, VEC, MODE>(a, xc, xn, gwarp, nwarp, lane, sred);
             return;
         }
@@ -547,7 +657,7 @@ __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a)
         double* sw = sred + (GROUPED ? 0 : warp * kp);
         for (int cc = threadIdx.x; cc < nsw * a.kp; cc += kThreads) sred[cc] = 0.0;
         __syncthreads();
-        if (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sw);
+        if (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sw, stage);
         else phase2_rows<T, KC, VEC, MODE>(a, xc, xn, gwarp, nwarp, lane, sw);
         __syncthreads();
         double* part = a.partial + (int64_t)(it & 1) * nblk * kp;   // column-major [kp][nblk]
@@ -1244,8 +1354,9 @@ template <typename T, int KC, int VEC, int MODE, bool GROUPED>
 int launch_hot_t(Handle* h, HotArgs& a, cudaStream_t st) {
     DeviceHMat* D = h->dev;
     auto fn = hot_kernel<T, KC, VEC, MODE, GROUPED>;
-    const size_t smem = MODE == M_SOLVE ? (size_t)(GROUPED ? 1 : kWarps) * a.kp * sizeof(double) : 0;
-    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    size_t smem = MODE == M_SOLVE ? (size_t)(GROUPED ? 1 : kWarps) * a.kp * sizeof(double) : 0;
+    if (GROUPED) smem = (size_t)((a.kp + 1) & ~1) * sizeof(double) + (size_t)stage_bytes<T, VEC>();
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
     if (per_sm < 1) return set_error(VF_ECUDA, "hot kernel cannot be resident");
