@@ -57,7 +57,7 @@ typedef enum {
     VF_ECUDA = -3,         /* a CUDA runtime call or kernel failed                    */
     VF_ENOCONV = -4,       /* solve hit `iters` before `tol`; outputs hold last iterate */
     VF_EIO = -5,           /* file open/read/write failed or bad HVFM container       */
-    VF_ENCCL = -6,         /* reserved for the multi-GPU row-sharded mode             */
+    VF_ENCCL = -6,         /* an NCCL call of the row-sharded mode failed             */
     VF_EUNSUPPORTED = -7,  /* valid request this build does not implement             */
     VF_ENODEV = -8         /* no usable CUDA device / handle has no device copy       */
 } vf_status;
@@ -196,6 +196,43 @@ int vf_info(vf_handle h, vf_info_t* out);
 int vf_enable_kernel_timing(vf_handle h, int on);
 int vf_kernel_timing(vf_handle h, double* ms_phase2, int* launches_phase2,
                      double* ms_phase1, int* launches_phase1, int* launches_total);
+
+/*
+ * Block-row sharding (multi-GPU single-RHS solves; SURVEY §8(e) "ROWS",
+ * §8(a) a6).  Alg. 5 sums Y_I = sum_J F_IJ X_J per block row, so
+ * the operator splits by output rows: rank g of `world` owns the contiguous
+ * tree-order rows [bounds[g], bounds[g+1]), cut so every rank streams about
+ * the same F-hat bytes per apply (A7/A8 byte accounting).  A rank keeps the
+ * leaf rows inside its range (SVD blocks: its rows of U; V and S duplicated)
+ * and the full right-hand side; each Jacobi iteration ends with one
+ * ncclAllGather of the ranks' new rows (and their residual partial sums).
+ * One process per GPU; every rank makes the same calls with the same full
+ * (caller-order, N x nrhs) inputs and receives the same full outputs.
+ */
+
+/* Cut points of the row partition for `world` ranks (bounds: world + 1
+ * int64, HOST, caller-owned).  Does not modify the handle.  For a sharded
+ * handle `world` must equal its world and its own cut points are returned. */
+int vf_row_partition(vf_handle h, int world, int64_t* bounds);
+
+/* Restrict the handle to rank `rank`'s rows of the partition above (host
+ * metadata and, if uploaded, the device copy).  Irreversible; a handle can be
+ * sharded once.  Without a communicator, vf_matvec on a sharded handle writes
+ * this rank's rows of Y and zeros elsewhere, and the solves fail with
+ * VF_EINVAL; after vf_comm_init every call returns full results. */
+int vf_shard_rows(vf_handle h, int rank, int world);
+
+/* This rank's tree-order row range [*lo, *hi) ([0, N) if not sharded). */
+int vf_row_range(vf_handle h, int64_t* lo, int64_t* hi);
+
+/* A fresh NCCL unique id (128 bytes written to id128, HOST).  Rank 0 creates
+ * it and the caller broadcasts it (e.g. through a torch process group). */
+int vf_get_nccl_id(void* id128);
+
+/* Create the handle's NCCL communicator (rank, world as in vf_shard_rows; the
+ * handle's device must be this process's GPU).  Collective over all ranks.
+ * Failures -> VF_ENCCL.  Released by vf_free. */
+int vf_comm_init(vf_handle h, int rank, int world, const void* id128);
 
 const char* vf_last_error(void);
 

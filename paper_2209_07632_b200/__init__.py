@@ -25,7 +25,8 @@ __all__ = [
     "VFError", "lib", "ViewFactorMatrix", "vf_build", "vf_build_facets", "vf_load", "vf_save", "vf_free",
     "vf_upload", "vf_set_stream", "vf_matvec", "vf_solve_radiosity", "vf_solve_thermal", "vf_insolation",
     "vf_info", "vf_last_solve_stats", "vf_enable_kernel_timing", "vf_kernel_timing", "VF_F64", "VF_F32",
-    "VF_VIS_RAYCAST", "VF_VIS_CULL_ONLY", "HEADER",
+    "VF_VIS_RAYCAST", "VF_VIS_CULL_ONLY", "HEADER", "vf_row_partition", "vf_shard_rows", "vf_row_range",
+    "vf_get_nccl_id", "vf_comm_init",
 ]
 
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "vf.h")
@@ -101,6 +102,11 @@ def lib():
             "vf_enable_kernel_timing": ([H, i], i),
             "vf_kernel_timing": ([H, ctypes.POINTER(d), ctypes.POINTER(i), ctypes.POINTER(d),
                                   ctypes.POINTER(i), ctypes.POINTER(i)], i),
+            "vf_row_partition": ([H, i, P], i),
+            "vf_shard_rows": ([H, i, i], i),
+            "vf_row_range": ([H, ctypes.POINTER(I), ctypes.POINTER(I)], i),
+            "vf_get_nccl_id": ([P], i),
+            "vf_comm_init": ([H, i, i, P], i),
             "vf_last_error": ([], ctypes.c_char_p),
         }
         for name, (args, res) in sig.items():
@@ -286,6 +292,36 @@ def vf_kernel_timing(h) -> dict:
                 launches_total=lt.value)
 
 
+def vf_row_partition(h, world: int) -> np.ndarray:
+    """Cut points (world + 1,) of the block-row partition (ROWS mode)."""
+    b = np.zeros(world + 1, dtype=np.int64)
+    _check(lib().vf_row_partition(h, int(world), b.ctypes.data))
+    return b
+
+
+def vf_shard_rows(h, rank: int, world: int):
+    _check(lib().vf_shard_rows(h, int(rank), int(world)))
+
+
+def vf_row_range(h) -> tuple[int, int]:
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().vf_row_range(h, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
+
+
+def vf_get_nccl_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().vf_get_nccl_id(buf))
+    return buf.raw
+
+
+def vf_comm_init(h, rank: int, world: int, nccl_id: bytes):
+    if len(nccl_id) != 128:
+        raise ValueError("nccl_id must be 128 bytes")
+    buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
+    _check(lib().vf_comm_init(h, int(rank), int(world), buf))
+
+
 class ViewFactorMatrix:
     """Owning wrapper around a vf_handle (frees it on close / GC)."""
 
@@ -334,6 +370,27 @@ class ViewFactorMatrix:
 
     def stats(self):
         return vf_last_solve_stats(self.h)
+
+    def shard_rows(self, rank, world):
+        """Keep only this rank's block rows (ROWS mode)."""
+        vf_shard_rows(self.h, rank, world)
+        return self.refresh()
+
+    def row_range(self):
+        return vf_row_range(self.h)
+
+    def comm_init(self, rank, world, nccl_id):
+        vf_comm_init(self.h, rank, world, nccl_id)
+
+    def init_rows(self, group=None):
+        """Shard by rows over a torch.distributed process group and create the
+        NCCL communicator (rank 0's unique id is broadcast through the group)."""
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        self.shard_rows(rank, world)
+        obj = [vf_get_nccl_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+        self.comm_init(rank, world, obj[0])
 
     def close(self):
         if self.h:

@@ -151,6 +151,7 @@ int vf_upload(vf_handle hh, int device) {
 int vf_free(vf_handle hh) {
     if (!hh) return VF_OK;
     Handle* h = reinterpret_cast<Handle*>(hh);
+    comm_destroy(h);
     device_free(h);
     delete h;
     return VF_OK;
@@ -275,6 +276,61 @@ int vf_kernel_timing(vf_handle hh, double* ms2, int* l2, double* ms1, int* l1, i
     if (l1) *l1 = h->launches_p1;
     if (lt) *lt = h->launches_total;
     return VF_OK;
+}
+
+int vf_row_partition(vf_handle hh, int world, int64_t* bounds) {
+    GUARD({
+        if (!hh || !bounds || world < 1) return set_error(VF_EINVAL, "vf_row_partition: bad arguments");
+        Handle* h = reinterpret_cast<Handle*>(hh);
+        if (h->sharded) {
+            if (world != h->world) return set_error(VF_EINVAL, "vf_row_partition: handle is sharded for another world");
+            std::copy(h->row_bounds.begin(), h->row_bounds.end(), bounds);
+            return VF_OK;
+        }
+        std::vector<int64_t> b;
+        int rc = row_partition(h, world, b);
+        if (rc) return rc;
+        std::copy(b.begin(), b.end(), bounds);
+        return VF_OK;
+    })
+}
+
+int vf_shard_rows(vf_handle hh, int rank, int world) {
+    GUARD({
+        if (!hh) return set_error(VF_EINVAL, "vf_shard_rows: null handle");
+        Handle* h = reinterpret_cast<Handle*>(hh);
+        int rc = shard_rows(h, rank, world);
+        if (rc) return rc;
+        if (h->dev) return device_upload(h, h->device);    // re-flatten the shard
+        return VF_OK;
+    })
+}
+
+int vf_row_range(vf_handle hh, int64_t* lo, int64_t* hi) {
+    if (!hh || !lo || !hi) return set_error(VF_EINVAL, "vf_row_range: null argument");
+    Handle* h = reinterpret_cast<Handle*>(hh);
+    *lo = h->sharded ? h->row_lo : 0;
+    *hi = h->sharded ? h->row_hi : h->N;
+    return VF_OK;
+}
+
+int vf_get_nccl_id(void* id128) {
+    GUARD({
+        if (!id128) return set_error(VF_EINVAL, "vf_get_nccl_id: null argument");
+        return comm_get_id(id128);
+    })
+}
+
+int vf_comm_init(vf_handle hh, int rank, int world, const void* id128) {
+    GUARD({
+        if (!hh || !id128) return set_error(VF_EINVAL, "vf_comm_init: null argument");
+        Handle* h = reinterpret_cast<Handle*>(hh);
+        if (!h->dev) return set_error(VF_ENODEV, "vf_comm_init: handle has no device copy");
+        if (!h->sharded) return set_error(VF_EINVAL, "vf_comm_init: call vf_shard_rows first");
+        if (rank != h->rank || world != h->world)
+            return set_error(VF_EINVAL, "vf_comm_init: rank/world differ from vf_shard_rows");
+        return comm_init(h, rank, world, id128);
+    })
 }
 
 const char* vf_last_error(void) { return g_err.c_str(); }

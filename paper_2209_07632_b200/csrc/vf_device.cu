@@ -61,7 +61,7 @@ struct Ctl {                            // device-side loop state
     unsigned bar_gen;
 };
 
-enum Mode { M_MATVEC = 0, M_SOLVE = 1 };
+enum Mode { M_MATVEC = 0, M_SOLVE = 1, M_STEP = 2 };   // M_STEP: one Jacobi iteration (ROWS mode)
 
 #define CK(call)                                                                         \
     do {                                                                                 \
@@ -596,7 +596,7 @@ __device__ __forceinline__ void groups_phase(const HotArgs& a, T* xc, T* xn, dou
                 static_cast<T*>(a.Q)[o] = q;
             }
         }
-        if (PHASE == 2 && MODE == M_SOLVE) {
+        if (PHASE == 2 && MODE != M_MATVEC) {
             __syncthreads();
             if (t < kGroup * CW) stile[t] = d2;                  // [row][col]
             __syncthreads();
@@ -624,6 +624,32 @@ __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a)
     const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp, nwarp = (int64_t)gridDim.x * kWarps;
     const unsigned nblk = gridDim.x;
     const bool have_p1 = GROUPED ? a.n_g1 > 0 : a.n_p1 > 0;
+    if (MODE == M_STEP) {
+        // ROWS mode (a6): one iteration on this rank's rows; the iterate
+        // parity and the stop flag live in ctl (rows_decide_kernel).
+        if (*(volatile int*)&a.ctl->done) return;
+        const int it = *(volatile int*)&a.ctl->iter;
+        T* xc = static_cast<T*>((it & 1) ? a.xt1 : a.xt0);
+        T* xn = static_cast<T*>((it & 1) ? a.xt0 : a.xt1);
+        if (have_p1) {
+            if (GROUPED) groups_phase<T, VEC, 1, MODE>(a, xc, xn, stile, nullptr, stage);
+            else phase1_rows<T, KC, VEC>(a, xc, gwarp, nwarp, lane);
+            grid_sync(a.ctl, nblk);
+        }
+        const int nsw = GROUPED ? 1 : kWarps;
+        double* sw = sred + (GROUPED ? 0 : warp * kp);
+        for (int cc = threadIdx.x; cc < nsw * a.kp; cc += kThreads) sred[cc] = 0.0;
+        __syncthreads();
+        if (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sw, stage);
+        else phase2_rows<T, KC, VEC, MODE>(a, xc, xn, gwarp, nwarp, lane, sw);
+        __syncthreads();
+        for (int cc = threadIdx.x; cc < a.kp; cc += kThreads) {
+            double sum = 0.0;
+            for (int w = 0; w < nsw; ++w) sum += sred[w * kp + cc];
+            a.partial[(int64_t)cc * nblk + blockIdx.x] = sum;          // column-major [kp][nblk]
+        }
+        return;
+    }
     int cur = 0;
     for (int it = 0;; ++it) {
         T* xc = static_cast<T*>(cur ? a.xt1 : a.xt0);
@@ -812,6 +838,71 @@ __global__ void thermal_T_kernel(const T* Qvis, const T* Q, const uint8_t* activ
     }
 }
 
+// ---- ROWS mode exchange.  Every rank's slot of the
+// allgather buffer is [own rows x kp values | kp residual partial sums],
+// padded to 16 B; slot size is the same on all ranks (max row count).
+// Pack: own rows of the new iterate (parity from ctl) or of `src`; the
+// per-column residual partials of this rank are summed over CTAs in a fixed
+// order into the slot's tail.
+template <typename T>
+__global__ void rows_pack_kernel(const Ctl* ctl, const T* xt0, const T* xt1, const T* src, int64_t lo, int64_t nrows,
+                                 int kp, const double* partial, int nblk, int64_t tail_off, unsigned char* send) {
+    if (ctl && *(const volatile int*)&ctl->done) return;
+    const T* x = ctl ? ((*(const volatile int*)&ctl->iter & 1) ? xt0 : xt1) : src;   // B_{it+1}
+    const int64_t n = nrows * kp;
+    T* dst = reinterpret_cast<T*>(send);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = x[lo * kp + i];
+    if (ctl && blockIdx.x == 0) {
+        double* tail = reinterpret_cast<double*>(send + tail_off);
+        for (int c = threadIdx.x; c < kp; c += blockDim.x) {
+            double sum = 0.0;
+            for (int b = 0; b < nblk; ++b) sum += partial[(int64_t)c * nblk + b];
+            tail[c] = sum;
+        }
+    }
+}
+
+// Unpack every rank's rows into the new iterate (or `dst`).
+template <typename T>
+__global__ void rows_unpack_kernel(const Ctl* ctl, T* xt0, T* xt1, T* dst, const int64_t* bounds, int world, int kp,
+                                   int64_t slot_bytes, const unsigned char* recv) {
+    if (ctl && *(const volatile int*)&ctl->done) return;
+    T* x = ctl ? ((*(const volatile int*)&ctl->iter & 1) ? xt0 : xt1) : dst;
+    for (int g = 0; g < world; ++g) {
+        const int64_t lo = bounds[g], n = (bounds[g + 1] - lo) * kp;
+        const T* src = reinterpret_cast<const T*>(recv + (int64_t)g * slot_bytes);
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+            x[lo * kp + i] = src[i];
+    }
+}
+
+// a5 for ROWS mode: r_c = sqrt(sum over ranks, in rank order, of their
+// partials) / ||E_c||; iteration count and stop flag (same rule as the
+// persistent solve: stop when every column has r <= tol or iters reached).
+__global__ void rows_decide_kernel(Ctl* ctl, const unsigned char* recv, int64_t slot_bytes, int64_t tail_off, int world,
+                                   int k, const double* enorm2, double* resid, double tol, int iters) {
+    if (*(volatile int*)&ctl->done) return;
+    __shared__ int bad;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        double sum = 0.0;
+        for (int g = 0; g < world; ++g)
+            sum += reinterpret_cast<const double*>(recv + (int64_t)g * slot_bytes + tail_off)[c];
+        const double en = enorm2[c];
+        const double rr = en > 0.0 ? sqrt(sum) / sqrt(en) : 0.0;
+        resid[c] = rr;
+        if (!(rr <= tol)) atomicOr(&bad, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int it = ctl->iter + 1;
+        ctl->iter = it;
+        if (!bad || it >= iters) ctl->done = 1;
+    }
+}
+
 }  // namespace
 
 // --------------------------------------------------------------- layout
@@ -874,6 +965,13 @@ struct DeviceHMat {
     std::vector<int64_t> cost_p1, cost_p2, cost_g1, cost_g2;
     struct Sched { int32_t* ptr = nullptr; int32_t* items = nullptr; };
     std::map<std::array<int64_t, 4>, Sched> sched;
+    // ROWS mode (sharded handle): cut points and the allgather buffers
+    int64_t* bounds = nullptr;
+    int64_t row_lo = 0, row_hi = 0, rows_max = 0;
+    int world = 1;
+    unsigned char* send = nullptr;
+    unsigned char* recv = nullptr;
+    size_t slot_cap = 0;
     // staging for host pointers
     void* stage[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     size_t stage_cap[6] = {0, 0, 0, 0, 0, 0};
@@ -1146,6 +1244,17 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     if ((rc = up((void**)&D->grow2, grow2v.data(), grow2v.size() * 4))) return rc;
     if ((rc = up((void**)&D->gcsr1, gcsr1v.data(), gcsr1v.size() * 8))) return rc;
     if ((rc = up((void**)&D->gcsr2, gcsr2v.data(), gcsr2v.size() * 8))) return rc;
+    if (h->sharded) {
+        // outputs are masked by the UNSHARDED operator's stored rows: after the
+        // allgather every rank holds valid rows of all ranks
+        active.assign(h->active_global.begin(), h->active_global.end());
+        D->world = h->world;
+        D->row_lo = h->row_lo;
+        D->row_hi = h->row_hi;
+        for (int g = 0; g < h->world; ++g)
+            D->rows_max = std::max<int64_t>(D->rows_max, h->row_bounds[g + 1] - h->row_bounds[g]);
+        if ((rc = up((void**)&D->bounds, h->row_bounds.data(), h->row_bounds.size() * 8))) return rc;
+    }
     if ((rc = up((void**)&D->active, active.data(), active.size()))) return rc;
     CK(cudaMalloc((void**)&D->ctl, sizeof(Ctl)));
     CK(cudaMallocHost((void**)&D->ctl_host, sizeof(Ctl)));
@@ -1354,7 +1463,7 @@ template <typename T, int KC, int VEC, int MODE, bool GROUPED>
 int launch_hot_t(Handle* h, HotArgs& a, cudaStream_t st) {
     DeviceHMat* D = h->dev;
     auto fn = hot_kernel<T, KC, VEC, MODE, GROUPED>;
-    size_t smem = MODE == M_SOLVE ? (size_t)(GROUPED ? 1 : kWarps) * a.kp * sizeof(double) : 0;
+    size_t smem = MODE != M_MATVEC ? (size_t)(GROUPED ? 1 : kWarps) * a.kp * sizeof(double) : 0;
     if (GROUPED) smem = (size_t)((a.kp + 1) & ~1) * sizeof(double) + (size_t)stage_bytes<T, VEC>();
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
@@ -1374,14 +1483,14 @@ int launch_hot_t(Handle* h, HotArgs& a, cudaStream_t st) {
     static const char* trace_file = getenv("VF_TRACE_FILE");
     unsigned long long* tbuf = nullptr;
     const int tit = 64;
-    if (trace_file && MODE == M_SOLVE) {
+    if (trace_file && MODE == M_SOLVE) {    // (M_STEP: not traced)
         CK(cudaMalloc(&tbuf, (size_t)tit * 5 * grid * 8));
         CK(cudaMemsetAsync(tbuf, 0, (size_t)tit * 5 * grid * 8, st));
         a.trace = tbuf;
         a.trace_iters = tit;
     }
     void* args[] = {&a};
-    CK(cudaMemsetAsync(a.ctl, 0, offsetof(Ctl, bar_gen), st));       // iter, done, bad, bar_arrive
+    if (MODE != M_STEP) CK(cudaMemsetAsync(a.ctl, 0, offsetof(Ctl, bar_gen), st));   // iter, done, bad, bar_arrive
     {
         Timer tm(h, st, 2);
         CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kThreads), args, smem, st));
@@ -1449,6 +1558,99 @@ int iterate(Handle* h, int k, int kp, const void* rho, int clamp, int iters, dou
     return VF_OK;
 }
 
+// ---- ROWS mode host side -------------------------------------------------
+size_t rows_tail_off(const DeviceHMat* D, int kp) { return ((size_t)D->rows_max * kp * D->w + 15) & ~(size_t)15; }
+size_t rows_slot(const DeviceHMat* D, int kp) { return (rows_tail_off(D, kp) + (size_t)kp * 8 + 15) & ~(size_t)15; }
+
+int ensure_rows_bufs(DeviceHMat* D, int kp) {
+    const size_t slot = rows_slot(D, kp);
+    if (slot <= D->slot_cap) return VF_OK;
+    if (D->send) cudaFree(D->send);
+    if (D->recv) cudaFree(D->recv);
+    D->send = D->recv = nullptr;
+    CK(cudaMalloc((void**)&D->send, slot));
+    CK(cudaMalloc((void**)&D->recv, slot * D->world));
+    CK(cudaMemset(D->send, 0, slot));
+    D->slot_cap = slot;
+    return VF_OK;
+}
+
+int rows_grid(int64_t n) { return (int)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 4)); }
+
+// Allgather of a plain tree-order N x kp buffer (own rows -> every rank).
+template <typename T>
+int rows_allgather_buf(Handle* h, void* buf, int kp, cudaStream_t st) {
+    DeviceHMat* D = h->dev;
+    int rc;
+    if ((rc = ensure_rows_bufs(D, kp))) return rc;
+    const size_t slot = rows_slot(D, kp);
+    const int64_t own = D->row_hi - D->row_lo;
+    rows_pack_kernel<T><<<rows_grid(own * kp), 256, 0, st>>>(nullptr, nullptr, nullptr, (const T*)buf, D->row_lo, own,
+                                                              kp, nullptr, 0, 0, D->send);
+    if ((rc = comm_allgather(h, D->send, D->recv, slot, st))) return rc;
+    rows_unpack_kernel<T><<<rows_grid(D->rows_max * kp), 256, 0, st>>>(nullptr, nullptr, nullptr, (T*)buf, D->bounds,
+                                                                       D->world, kp, (int64_t)slot, D->recv);
+    h->launches_total += 2;
+    return VF_OK;
+}
+
+// ROWS-mode Jacobi solve: per iteration one M_STEP launch of the hot kernel
+// on this rank's rows, pack, ncclAllGather, unpack, decide.  Launches are
+// issued in batches; once the device-side stop flag is set the remaining
+// launches of a batch return immediately (the allgather resends unchanged
+// data), so the host reads the flag only once per batch.
+template <typename T>
+int iterate_rows(Handle* h, int k, int kp, const void* rho, int clamp, int iters, double tol, cudaStream_t st,
+                 int* iters_done, double* max_resid) {
+    DeviceHMat* D = h->dev;
+    *iters_done = 0;
+    *max_resid = 0;
+    if (iters <= 0) return VF_OK;
+    if (!h->comm) return set_error(VF_EINVAL, "solve on a row-sharded handle needs vf_comm_init");
+    int rc;
+    if ((rc = ensure_rows_bufs(D, kp))) return rc;
+    const size_t slot = rows_slot(D, kp), toff = rows_tail_off(D, kp);
+    const int64_t own = D->row_hi - D->row_lo;
+    CK(cudaMemsetAsync(D->ctl, 0, sizeof(Ctl), st));
+    HotArgs a = hot_args(D, kp, k);
+    a.E = D->Ep; a.rho = rho; a.Q = D->Qp; a.iters = iters; a.clamp = clamp; a.tol = tol;
+    const int batch = 4;
+    for (int launched = 0;;) {
+        for (int b = 0; b < batch; ++b) {
+            if ((rc = launch_hot<T, M_STEP>(h, a, st))) return rc;
+            rows_pack_kernel<T><<<rows_grid(own * kp), 256, 0, st>>>(D->ctl, (const T*)D->xt[0], (const T*)D->xt[1],
+                                                                      nullptr, D->row_lo, own, kp, D->partial,
+                                                                      D->last_grid, (int64_t)toff, D->send);
+            if ((rc = comm_allgather(h, D->send, D->recv, slot, st))) return rc;
+            rows_unpack_kernel<T><<<rows_grid(D->rows_max * kp), 256, 0, st>>>(
+                D->ctl, (T*)D->xt[0], (T*)D->xt[1], nullptr, D->bounds, D->world, kp, (int64_t)slot, D->recv);
+            rows_decide_kernel<<<1, 256, 0, st>>>(D->ctl, D->recv, (int64_t)slot, (int64_t)toff, D->world, k,
+                                                  D->enorm2, D->resid, tol, iters);
+            h->launches_total += 3;
+        }
+        launched += batch;
+        CK(cudaMemcpyAsync(D->ctl_host, D->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (D->ctl_host->done) break;
+        if (launched > iters + batch) return set_error(VF_ECUDA, "ROWS solve: stop flag never set");
+    }
+    CK(cudaMemcpyAsync(D->resid_host, D->resid, (size_t)k * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *iters_done = D->ctl_host->iter;
+    double mr = 0;
+    for (int c = 0; c < k; ++c) mr = std::max(mr, D->resid_host[c]);
+    *max_resid = mr;
+    return VF_OK;
+}
+
+template <typename T>
+int solve_stage(Handle* h, int k, int kp, const void* rho, int clamp, int iters, double tol, cudaStream_t st,
+                int* iters_done, double* max_resid) {
+    if (h->dev->world > 1 || h->comm)
+        return iterate_rows<T>(h, k, kp, rho, clamp, iters, tol, st, iters_done, max_resid);
+    return iterate<T>(h, k, kp, rho, clamp, iters, tol, st, iters_done, max_resid);
+}
+
 int check_k(int nrhs) {
     if (nrhs > kMaxKp) return set_error(VF_EUNSUPPORTED, "nrhs > 2048 per call: split the batch");
     return VF_OK;
@@ -1471,7 +1673,10 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     launch_permute_in<T>(h, Xd, nrhs, kp, nullptr, D->xt[0], nullptr, nullptr, nullptr, st);
     HotArgs a = hot_args(D, kp, nrhs);
     a.Y = D->Yp;
+    const bool rows = D->world > 1 || h->comm;
+    if (rows) CK(cudaMemsetAsync(D->Yp, 0, (size_t)D->N * kp * sizeof(T), st));   // rows of other ranks: 0 ...
     if ((rc = launch_hot<T, M_MATVEC>(h, a, st))) return rc;
+    if (rows && h->comm && (rc = rows_allgather_buf<T>(h, D->Yp, kp, st))) return rc;   // ... or gathered
     launch_permute_out<T>(h, D->Yp, nrhs, kp, true, Yd, st);
     CK(cudaGetLastError());
     if ((rc = stage_out_copy(Y, Yd, vb, st))) return rc;
@@ -1501,7 +1706,7 @@ int radiosity_impl(Handle* h, const void* E, const void* rho, void* B, int nrhs,
     launch_colnorm<T>(h, D->Ep, nrhs, kp, st);
     int it = 0;
     double res = 0;
-    if ((rc = iterate<T>(h, nrhs, kp, D->pv[0], clamp, iters, tol, st, &it, &res))) return rc;
+    if ((rc = solve_stage<T>(h, nrhs, kp, D->pv[0], clamp, iters, tol, st, &it, &res))) return rc;
     h->iters1 = it; h->resid1 = res; h->iters2 = 0; h->resid2 = 0;
     launch_permute_out<T>(h, D->xt[it & 1], nrhs, kp, false, Bd, st);
     CK(cudaGetLastError());
@@ -1541,7 +1746,8 @@ int thermal_impl(Handle* h, const void* Qdir, const void* alb, const void* emi, 
     launch_colnorm<T>(h, D->Ep, nrhs, kp, st);
     int it1 = 0, it2 = 0;
     double r1 = 0, r2 = 0;
-    if ((rc = iterate<T>(h, nrhs, kp, alpha, 1, iters, tol, st, &it1, &r1))) return rc;
+    if ((rc = solve_stage<T>(h, nrhs, kp, alpha, 1, iters, tol, st, &it1, &r1))) return rc;
+    if (h->comm && (rc = rows_allgather_buf<T>(h, D->Qp, kp, st))) return rc;      // Qrefl of every rank
     // stage 2: Qvis = Qdir + Qrefl, E = (1 - alpha) Qvis, rho = 1
     const int64_t tot = D->N * kp;
     const int gb = (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, 148 * 8));
@@ -1549,7 +1755,8 @@ int thermal_impl(Handle* h, const void* Qdir, const void* alb, const void* emi, 
                                               (T*)D->Qvp, (T*)D->Ep, (T*)D->xt[0], (T*)D->xt[1]);
     h->launches_total++;
     launch_colnorm<T>(h, D->Ep, nrhs, kp, st);
-    if ((rc = iterate<T>(h, nrhs, kp, nullptr, 1, iters, tol, st, &it2, &r2))) return rc;
+    if ((rc = solve_stage<T>(h, nrhs, kp, nullptr, 1, iters, tol, st, &it2, &r2))) return rc;
+    if (h->comm && (rc = rows_allgather_buf<T>(h, D->Qp, kp, st))) return rc;      // Qir of every rank
     thermal_T_kernel<T><<<gb, 256, 0, st>>>((const T*)D->Qvp, (const T*)D->Qp, D->active, alpha, emis, D->N, nrhs,
                                             kp, (T*)D->Yp, (T*)D->Qip);
     h->launches_total++;
@@ -1595,7 +1802,7 @@ void device_free(Handle* h) {
     DeviceHMat* D = h->dev;
     if (!D) return;
     cudaSetDevice(h->device);
-    void* ptrs[] = {D->vals, D->idx, D->segs, D->p1_segptr, D->p1_rows, D->p1_scale, D->p2_segptr, D->p2_rows,
+    void* ptrs[] = {D->bounds, D->send, D->recv, D->vals, D->idx, D->segs, D->p1_segptr, D->p1_rows, D->p1_scale, D->p2_segptr, D->p2_rows,
                     D->perm, D->active, D->g1, D->g2, D->gseg, D->gvo, D->grow1, D->grow2, D->gcsr1, D->gcsr2,
                     D->xt[0], D->xt[1], D->Ep, D->Qp, D->Qdp, D->Qvp, D->Yp, D->Qip,
                     D->pv[0], D->pv[1], D->pv[2], D->partial, D->enorm2, D->resid, D->ctl,

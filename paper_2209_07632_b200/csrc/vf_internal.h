@@ -58,6 +58,15 @@ struct Handle {
     bool timing = false;
     double ms_p2 = 0, ms_p1 = 0;
     int launches_p2 = 0, launches_p1 = 0, launches_total = 0;
+    double ms_comm = 0;                  // allgather time of the last call (ROWS mode)
+    // block-row sharding (vf_shard.cpp; SURVEY §8(e) ROWS): this handle holds
+    // the leaf rows of tree rows [row_lo, row_hi) only.
+    bool sharded = false;
+    int rank = 0, world = 1;
+    int64_t row_lo = 0, row_hi = 0;
+    std::vector<int64_t> row_bounds;     // world + 1 cut points
+    std::vector<uint8_t> active_global;  // rows of the UNSHARDED F-hat with a stored entry
+    void* comm = nullptr;                // ncclComm_t (vf_comm.cpp) or null
 };
 
 // error reporting (thread-local message)
@@ -69,6 +78,17 @@ int build_handle(Handle* h, int64_t N, const double* x, const double* n, const d
                  const int64_t* tri_of, double tol, const vf_build_opts& o);
 int insolation(const Handle* h, const double* suns, int k, double S, double* Q);
 int64_t leaf_nbytes(const Leaf& L, int w);
+
+// block-row sharding (vf_shard.cpp)
+int row_partition(const Handle* h, int world, std::vector<int64_t>& bounds);
+int shard_rows(Handle* h, int rank, int world);
+std::vector<uint8_t> active_rows_of(const Handle* h);
+
+// NCCL (vf_comm.cpp; libnccl is dlopen'ed, sharing the process's copy)
+int comm_get_id(void* id128);
+int comm_init(Handle* h, int rank, int world, const void* id128);
+void comm_destroy(Handle* h);
+int comm_allgather(Handle* h, const void* send, void* recv, size_t bytes_per_rank, void* stream);
 
 // HVFM io (vf_io.cpp)
 int save_hvfm(const Handle* h, const char* path);
