@@ -90,7 +90,13 @@ typedef struct {
                             save, info work; apply/solve return VF_ENODEV)            */
     int threads;         /* host threads for the build (0 = all cores)               */
     uint64_t seed;       /* seed of the randomized truncated SVD (default 0x5eed)      */
+    int evaluator;       /* who evaluates F_ij and V_ij for Alg. 1:
+                            VF_EVAL_AUTO (default): the device when device >= 0,
+                            else the host; VF_EVAL_HOST; VF_EVAL_DEVICE.  Both take
+                            bit-identical decisions and values (reading R-VIS)     */
 } vf_build_opts;
+
+enum { VF_EVAL_AUTO = 0, VF_EVAL_HOST = 1, VF_EVAL_DEVICE = 2 };
 
 /* Fill *opts with the defaults above. */
 void vf_default_opts(vf_build_opts* opts);

@@ -26,7 +26,7 @@ __all__ = [
     "vf_upload", "vf_set_stream", "vf_matvec", "vf_solve_radiosity", "vf_solve_thermal", "vf_insolation",
     "vf_info", "vf_last_solve_stats", "vf_enable_kernel_timing", "vf_kernel_timing", "VF_F64", "VF_F32",
     "VF_VIS_RAYCAST", "VF_VIS_CULL_ONLY", "HEADER", "vf_row_partition", "vf_shard_rows", "vf_row_range",
-    "vf_get_nccl_id", "vf_comm_init",
+    "vf_get_nccl_id", "vf_comm_init", "VF_EVAL_AUTO", "VF_EVAL_HOST", "VF_EVAL_DEVICE",
 ]
 
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "vf.h")
@@ -35,6 +35,7 @@ VF_OK, VF_EINVAL, VF_ENOMEM, VF_ECUDA, VF_ENOCONV, VF_EIO, VF_ENCCL, VF_EUNSUPPO
     0, -1, -2, -3, -4, -5, -6, -7, -8
 VF_F64, VF_F32 = 1, 2
 VF_VIS_RAYCAST, VF_VIS_CULL_ONLY = 0, 1
+VF_EVAL_AUTO, VF_EVAL_HOST, VF_EVAL_DEVICE = 0, 1, 2
 _STATUS = {0: "VF_OK", -1: "VF_EINVAL", -2: "VF_ENOMEM", -3: "VF_ECUDA", -4: "VF_ENOCONV", -5: "VF_EIO",
            -6: "VF_ENCCL", -7: "VF_EUNSUPPORTED", -8: "VF_ENODEV"}
 
@@ -54,7 +55,7 @@ class vf_build_opts(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int), ("max_depth", ctypes.c_int), ("min_leaf", ctypes.c_int),
                 ("min_block", ctypes.c_int64), ("k0", ctypes.c_int), ("visibility", ctypes.c_int),
                 ("orient_up", ctypes.c_int), ("device", ctypes.c_int), ("threads", ctypes.c_int),
-                ("seed", ctypes.c_uint64)]
+                ("seed", ctypes.c_uint64), ("evaluator", ctypes.c_int)]
 
 
 class vf_info_t(ctypes.Structure):

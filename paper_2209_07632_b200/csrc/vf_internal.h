@@ -118,4 +118,12 @@ SvdResult estimate_rank(int64_t mu, int64_t nv, const double* dense, const int64
                         const int32_t* cols, const double* vals, double eps, int w, int k0,
                         int64_t target_bytes, int64_t m_full, int64_t n_full, uint64_t seed);
 
+void svd_profile_report();
+
+// device evaluator of the exact F for the build (vf_build_gpu.cu)
+struct Bvh;
+int gpu_exact_csr(int device, int64_t N, const double* x, const double* n, const double* A, const int64_t* tri,
+                  const Bvh* bvh, std::vector<int64_t>& rowptr, std::vector<int32_t>& cols,
+                  std::vector<double>& vals);
+
 }  // namespace vf
