@@ -378,6 +378,238 @@ def run_gpu(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------- terrain workloads (cfg3 / cfg5)
+
+def terrain_fhat(args, device):
+    """F-hat of BASELINE configs[2] (256^2-cell fBm terrain + 1 km crater):
+    loaded from --fhat if that file exists, else built (device evaluator +
+    device rank search, untimed) and saved there."""
+    import paper_2209_07632_b200 as vf
+    import scenegen as sg
+    V, F = sg.cfg3_mesh(n=args.cells, crater_D=1000.0 * args.cells / 256)
+    dt = vf.VF_F64 if args.dtype == "f64" else vf.VF_F32
+    path = args.fhat.format(n=args.cells, tol=args.tol, dtype=args.dtype) if args.fhat else None
+    t0 = time.time()
+    if path and os.path.exists(path):
+        M = vf.ViewFactorMatrix.load(path, device=device)
+        built = False
+    else:
+        M = vf.ViewFactorMatrix.build(V, F, args.tol, dtype=dt, device=device)
+        built = True
+        if path:
+            M.save(path)
+    return M, V, F, {"fhat_seconds": time.time() - t0, "built": built}
+
+
+def oracle_rows(V, F, rows):
+    import oracle
+    S = oracle.Scene(V, F)
+    return S, S.F_csr_rows(rows)
+
+
+def run_terrain(args, rank, world, local_rank):
+    import torch
+    import paper_2209_07632_b200 as vf
+    import scenegen as sg
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    dt = args.dtype
+    tdt = torch.float64 if dt == "f64" else torch.float32
+    w = 8 if dt == "f64" else 4
+    M, V, F, binfo = terrain_fhat(args, local_rank)
+    rows_mode = args.workload == "cfg5"
+    if rows_mode:
+        if dist:
+            M.init_rows()
+        else:
+            M.shard_rows(0, 1)
+            M.comm_init(0, 1, vf.vf_get_nccl_id())
+    info = M.refresh()
+    N = info["N"]
+    stream = torch.cuda.current_stream(dev)
+    M.set_stream(stream.cuda_stream)
+    k = 1 if rows_mode else args.nrhs
+
+    def colmajor(a):
+        return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64 if dt == "f64" else np.float32).T)).to(dev).T
+
+    if rows_mode:
+        sun = sg.sun_dirs(5.0, 1)
+        Qh = M.insolation(sun, S_SUN)
+        Qd = colmajor(Qh)
+        alb, emi = colmajor(np.full(N, ALBEDO)).reshape(-1).contiguous(), colmajor(np.full(N, EMISS)).reshape(-1).contiguous()
+        T = torch.empty((1, N), dtype=tdt, device=dev).T
+        Qv = torch.empty((1, N), dtype=tdt, device=dev).T
+        Qi = torch.empty((1, N), dtype=tdt, device=dev).T
+
+        def step():
+            M.solve_thermal(Qd, alb, emi, T, Qv, Qi, iters=500, tol=1e-8)
+    else:
+        X = colmajor(sg.random_rhs(N, k, seed=3 + rank))
+        Y = torch.empty((k, N), dtype=tdt, device=dev).T
+
+        def step():
+            M.matvec(X, Y)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    vf.vf_enable_kernel_timing(M.h, True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = Clocks(local_rank)
+    ms_hot, l_hot, launches, applies = 0.0, 0, 0, 0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+        kt = vf.vf_kernel_timing(M.h)
+        if not rows_mode:
+            torch.cuda.synchronize()
+            kt = vf.vf_kernel_timing(M.h)
+        ms_hot += kt["ms_phase2"]; l_hot += kt["launches_phase2"]
+        launches += kt["launches_total"]
+        if rows_mode:
+            st = M.stats()
+            applies += st["iters1"] + st["iters2"]
+        else:
+            applies += k
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    vf.vf_enable_kernel_timing(M.h, False)
+    t_ms = sum(a.elapsed_time(b) for a, b in ev)
+    tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    wk = torch.tensor([float(applies)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        if not rows_mode:                      # COLS replicas: work adds up; ROWS: one shared solve
+            dist.all_reduce(wk, op=dist.ReduceOp.SUM)
+    t_max = tt.item()
+    value = wk.item() / (t_max / 1e3)
+
+    # e2e through the same call with pinned HOST buffers
+    e_ms, e_app = 0.0, 0
+    if rows_mode:
+        Qp = torch.from_numpy(np.ascontiguousarray(Qh.T.astype(np.float64 if dt == "f64" else np.float32))).pin_memory().T
+        ap_ = torch.full((N,), ALBEDO, dtype=tdt).pin_memory()
+        ep_ = torch.full((N,), EMISS, dtype=tdt).pin_memory()
+        Tp = torch.empty((1, N), dtype=tdt).pin_memory().T
+
+        def estep():
+            M.solve_thermal(Qp, ap_, ep_, Tp, None, None, iters=500, tol=1e-8)
+        h2d, d2h = N * w + 2 * N * w, N * w
+    else:
+        Xp = X.cpu().T.contiguous().pin_memory().T
+        Yp = torch.empty((k, N), dtype=tdt).pin_memory().T
+
+        def estep():
+            M.matvec(Xp, Yp)
+        h2d, d2h = N * k * w, N * k * w
+    estep()
+    ke = max(3, min(args.steps, 10))
+    for i in range(ke):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        estep()
+        e1.record(stream)
+        e1.synchronize()
+        e_ms += e0.elapsed_time(e1)
+        e_app += (M.stats()["iters1"] + M.stats()["iters2"]) if rows_mode else k
+    et = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+    ew = torch.tensor([float(e_app)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(et, op=dist.ReduceOp.MAX)
+        if not rows_mode:
+            dist.all_reduce(ew, op=dist.ReduceOp.SUM)
+    e2e_value = ew.item() / (et.item() / 1e3)
+
+    # parity on sampled rows of the exact F (oracle), full size, this launch config
+    parity = None
+    if rank == 0 and not args.no_parity and not rows_mode:
+        rng = np.random.default_rng(7)
+        rows = np.sort(rng.choice(N, size=min(N, args.parity_rows), replace=False))
+        _, csr = oracle_rows(V, F, rows)
+        import oracle
+        Xh = X.cpu().numpy().astype(np.float64)
+        Yref = oracle.apply_csr(csr, Xh)
+        step()
+        Yg = Y.cpu().numpy().astype(np.float64)[rows]
+        parity = {"rows": int(rows.size), "rel_l2_vs_exact_F": float(np.linalg.norm(Yg - Yref) / np.linalg.norm(Yref)),
+                  "bound": 10 * args.tol}
+
+    if rank == 0:
+        pk, pk_kind = peaks()
+        n_app = applies / max(args.steps, 1)
+        avg = ms_hot / max(l_hot, 1)
+        kp = k if k <= 2 else (k + 15) // 16 * 16 if k > 8 else (4 if k <= 4 else 8)
+        solve_rows = 4 if rows_mode else 1
+        bytes_app = (info["p1_bytes"] + info["p2_bytes"] + (info["p1_src_rows"] + info["p2_src_rows"]) * kp * w
+                     + info["t_rows"] * kp * w + info["active_rows"] * kp * w * solve_rows)
+        flops_app = info["alg_flops_per_col"] * k
+        apps_launch = (n_app / max(l_hot / args.steps, 1)) if rows_mode else 1
+        ach_gbs = bytes_app * apps_launch / (avg * 1e-3) / 1e9 if avg > 0 else 0.0
+        hbm = pk.get("hbm_gbs", 6559.0)
+        roof = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm,
+                "traffic": None,
+                "kernel": ("hot_kernel<...,M_STEP> (ROWS mode: one Jacobi iteration per launch)" if rows_mode else
+                           "hot_kernel<...,M_MATVEC> (phase 1 V^T X, grid barrier, phase 2 row-owner accumulate)"),
+                "peak_basis": f"{pk_kind} MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
+                "avg_launch_ms": avg, "launches": l_hot, "alg_bytes_per_apply": bytes_app,
+                "alg_flops_per_apply": flops_app, "achieved_tflops": flops_app * apps_launch / (avg * 1e-3) / 1e12
+                if avg > 0 else 0.0, "share_of_step": ms_hot / t_ms if t_ms > 0 else None}
+        cfgname = "configs[4]" if rows_mode else "configs[2]"
+        wl = (f"BASELINE {cfgname}: {args.cells}^2-cell fBm terrain (H 0.8, RMS slope 15 deg, 10 m) + "
+              f"{1000.0 * args.cells / 256:.0f} m cap crater, {N} facets, F-hat tol {args.tol:g}, {dt.upper()}, "
+              + ("one sun (e 5 deg), radiosity + IR Jacobi to 1e-8, block-row sharded (ROWS) with a per-iteration "
+                 "ncclAllGather" if rows_mode else f"vf_matvec with nrhs = {k} (U[0,1) columns, seed 3)"))
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
+                "scaling": "strong" if rows_mode else "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
+                "config": {"workload": wl, "N": N, "nrhs": k, "tol_build": args.tol,
+                           "l2": "inputs larger than L2: F-hat %.2f GB vs 126 MB L2" % (info["alg_bytes"] / 1e9),
+                           "fhat_alg_bytes": info["alg_bytes"], "fhat_device_bytes": info["device_bytes"],
+                           "blocks": {"dense": info["n_dense"], "csr": info["n_csr"], "svd": info["n_svd"]},
+                           "nnz_csr": info["nnz_csr"], "sum_rank": info["sum_rank"],
+                           "active_rows": info["active_rows"], "visible_pairs": info["visible_pairs"],
+                           "applies_per_step": n_app, **binfo,
+                           "parallelism": (f"rows{world}" if rows_mode else f"cols{world}")},
+                "roofline": roof, "cpu_baseline": None, "parity": parity,
+                "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
+                "gpu_launches": launches, "clocks": clk}
+        if not args.no_cpu_baseline and world == 1 and not rows_mode:
+            import oracle
+            oracle.build()
+            rng = np.random.default_rng(8)
+            rows = np.sort(rng.choice(N, size=min(N, 2000), replace=False))
+            _, csr = oracle_rows(V, F, rows)
+            Xh = np.asfortranarray(sg.random_rhs(N, k))
+            reps, tc = 0, 0.0
+            while tc < args.cpu_budget and reps < 100000:
+                t0 = time.perf_counter()
+                oracle.apply_csr(csr, Xh)
+                tc += time.perf_counter() - t0
+                reps += 1
+            v_cpu = reps * k * rows.size / N / tc
+            line["cpu_baseline"] = {"value": v_cpu, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+                                    "sample": f"oracle exact-CSR apply (eq. FF-def rows, FP64, OpenMP) of {rows.size} "
+                                              f"sampled rows of F x {k} columns, {reps} reps in {tc:.1f} s, scaled "
+                                              f"to whole-matrix applies", "cpu": cpu_model()}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -387,6 +619,15 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg5"],
+                    help="cfg2: BASELINE configs[1] batched thermal solve (default); cfg3: configs[2] matvec; "
+                         "cfg5: configs[4] ROWS-sharded single-sun solve on the cfg3 mesh")
+    ap.add_argument("--nrhs", type=int, default=1)
+    ap.add_argument("--tol", type=float, default=1e-5)
+    ap.add_argument("--cells", type=int, default=256)
+    ap.add_argument("--fhat", default=None, help="HVFM cache path (may use {n}, {tol}, {dtype})")
+    ap.add_argument("--parity-rows", type=int, default=400)
+    ap.add_argument("--no-parity", action="store_true")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -396,7 +637,10 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    run_gpu(args, rank, world, local_rank)
+    if args.workload == "cfg2":
+        run_gpu(args, rank, world, local_rank)
+    else:
+        run_terrain(args, rank, world, local_rank)
 
 
 if __name__ == "__main__":

@@ -79,7 +79,7 @@ def lib():
     """Load libvf.so (building it in-tree if missing or stale)."""
     global _lib
     if _lib is None:
-        path = _build.build()
+        path = os.environ.get("VF_LIB") or _build.build()     # VF_LIB: a prebuilt variant (experiments)
         L = ctypes.CDLL(path)
         P, I, i, d = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_double
         H = ctypes.c_void_p

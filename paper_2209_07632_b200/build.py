@@ -68,7 +68,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         list(ex.map(compile_one, todo))
     tmp = LIB + f".tmp{os.getpid()}"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-cudart", "static", "-o", tmp,
-                           *[_obj(s) for s in sources()], "-lgomp", "-ldl"])
+                           *[_obj(s) for s in sources()], "-lgomp", "-ldl", "-lcublas", "-lcusolver", "-lcusparse",
+                           "-Xlinker", "-rpath,/usr/local/cuda/lib64"])
     os.replace(tmp, LIB)
     return LIB
 

@@ -10,6 +10,8 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -217,19 +219,28 @@ struct Builder {
                 for (int64_t e = crp[k]; e < crp[k + 1]; ++e) dense[k * nv + ccol[e]] = cval[e];
         }
         uint64_t bseed = seed ^ (0x9e3779b97f4a7c15ull * (uint64_t)(I.start * 1000003 + J.start * 7919 + m * 31 + n));
-        SvdResult svd = estimate_rank(mu, nv, dense.empty() ? nullptr : dense.data(), crp.data(), ccol.data(),
-                                      cval.data(), tol, w, k0, b_csr, m, n, bseed);
-        // step 4: recurse on the children pairs, slicing the CSR (never re-ray-tracing)
-        std::vector<TreeBlock> kids;
-        int64_t b_sub = kNodeOverhead;
-        for (int ci : I.kids)
-            for (int cj : J.kids) {
+        // steps 3 and 4 are independent: the rank estimate of this block and
+        // the recursion on its children pairs (slicing the CSR, never
+        // re-ray-tracing) run as concurrent OpenMP tasks.
+        SvdResult svd;
+#pragma omp task shared(svd, dense, crp, ccol, cval) if (m * n >= 16 * min_block)
+        svd = estimate_rank(mu, nv, dense.empty() ? nullptr : dense.data(), crp.data(), ccol.data(), cval.data(), tol,
+                            w, k0, b_csr, m, n, bseed);
+        std::vector<TreeBlock> kids(I.kids.size() * J.kids.size());
+        for (size_t a = 0; a < I.kids.size(); ++a)
+            for (size_t b = 0; b < J.kids.size(); ++b) {
+                const int ci = I.kids[a], cj = J.kids[b];
                 const QNode& Ic = qt->nodes[ci];
                 const QNode& Jc = qt->nodes[cj];
-                Csr s = c.slice(Ic.start - I.start, Ic.stop - I.start, Jc.start - J.start, Jc.stop - J.start);
-                kids.push_back(assemble(ci, cj, s, level + 1));
-                b_sub += kids.back().nbytes;
+#pragma omp task shared(kids, c) if ((Ic.stop - Ic.start) * (Jc.stop - Jc.start) >= 16 * min_block)
+                {
+                    Csr s = c.slice(Ic.start - I.start, Ic.stop - I.start, Jc.start - J.start, Jc.stop - J.start);
+                    kids[a * J.kids.size() + b] = assemble(ci, cj, s, level + 1);
+                }
             }
+#pragma omp taskwait
+        int64_t b_sub = kNodeOverhead;
+        for (auto& k : kids) b_sub += k.nbytes;
         // step 5: fewest bytes (ties in the order CSR < dense < SVD < subdivided)
         int kind = K_CSR;
         int64_t best = b_csr;
@@ -348,6 +359,10 @@ int build_handle(Handle* h, int64_t N, const double* x, const double* n, const d
         int rc = gpu_exact_csr(o.device, N, xt.data(), nt.data(), At.data(), tt.data(), B.cull_only ? nullptr : &bvh,
                                global.rowptr, global.cols, global.vals);
         if (rc) return rc;
+        if (getenv("VF_BUILD_PROFILE"))
+            fprintf(stderr, "[vf build] device evaluator: N %ld nnz %ld, %.2f s since start\n", (long)N,
+                    (long)global.cols.size(),
+                    std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
     }
     // Alg. 1 per first-level pair (host rays are parallel over rows inside),
     // then Alg. 3-4 on the pairs in parallel (largest first; each pair's
@@ -370,11 +385,22 @@ int build_handle(Handle* h, int64_t N, const double* x, const double* n, const d
         return blocks[a].m * blocks[a].n > blocks[b].m * blocks[b].n;
     });
     std::vector<TreeBlock> result(pairs.size());
-#pragma omp parallel for schedule(dynamic, 1)
+    g_svd_device = on_gpu ? o.device : -1;          // large rank searches on the device
+#pragma omp parallel
+#pragma omp single
     for (size_t k = 0; k < order.size(); ++k) {
         const size_t p = order[k];
-        result[p] = B.assemble(pairs[p].first, pairs[p].second, blocks[p], 1);
-        Csr().rowptr.swap(blocks[p].rowptr);
+#pragma omp task shared(result, blocks, pairs)
+        {
+            auto tp = std::chrono::steady_clock::now();
+            result[p] = B.assemble(pairs[p].first, pairs[p].second, blocks[p], 1);
+            if (getenv("VF_BUILD_PROFILE"))
+                fprintf(stderr, "[vf build] pair %zu (%ld x %ld, nnz %ld): %.2f s, done at %.2f s\n", p,
+                        (long)blocks[p].m, (long)blocks[p].n, (long)blocks[p].nnz(),
+                        std::chrono::duration<double>(std::chrono::steady_clock::now() - tp).count(),
+                        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count());
+            Csr().rowptr.swap(blocks[p].rowptr);
+        }
     }
     for (auto& tb : result) flatten(tb, h->leaves);
     h->visible_pairs = B.visible;

@@ -276,6 +276,80 @@ __device__ __forceinline__ void row_accumulate(const Seg* __restrict__ segs, int
         for (int v = 0; v < VEC; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
 }
 
+// nrhs = 1 (kp = 1): the HBM-bound streaming case.  A warp owns the row;
+// lane l takes 4-term chunks c = l, l + 32, ... of every segment with one
+// 16-B load of 4 column indices (CSR) and 16-B loads of the values, two chunks
+// in flight per lane (8 terms, 96 B): enough bytes in flight per SM to cover
+// HBM latency.  Segment starts are 16-B aligned in vals and 4-aligned in idx
+// (upload_impl), arrays are padded so chunk over-reads stay in bounds, and
+// out-of-range terms are masked to exact zeros.
+template <typename T> struct V4;
+template <> struct V4<double> {
+    static __device__ __forceinline__ void ld(const double* p, double* v) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    }
+};
+template <> struct V4<float> {
+    static __device__ __forceinline__ void ld(const float* p, float* v) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    }
+};
+
+template <typename T>
+__device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int64_t s0, int64_t s1,
+                                               const T* __restrict__ vals, const int32_t* __restrict__ idx,
+                                               const T* xt, int lane) {
+    constexpr int CH = 2;                        // chunks of 4 terms in flight per lane
+    T acc0 = T(0), acc1 = T(0);
+    for (int64_t s = s0; s < s1; ++s) {
+        const Seg sg = segs[s];
+        const T* __restrict__ vp = vals + sg.val_off;
+        const int len = sg.len;
+        for (int c0 = lane * 4; c0 < len; c0 += 32 * 4 * CH) {
+            T w[CH][4];
+            int64_t xr[CH][4];
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int e = c0 + c * 128;
+                if (e < len) {
+                    V4<T>::ld(vp + e, w[c]);
+                    if (sg.kind) {
+                        const int4 q = __ldg(reinterpret_cast<const int4*>(idx + sg.src + e));
+                        xr[c][0] = q.x; xr[c][1] = q.y; xr[c][2] = q.z; xr[c][3] = q.w;
+                    } else {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) xr[c][u] = sg.src + e + u;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (e + u >= len) { w[c][u] = T(0); xr[c][u] = sg.kind ? 0 : sg.src; }
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) { w[c][u] = T(0); xr[c][u] = 0; }
+                }
+            }
+            T x[CH][4];
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) x[c][u] = __ldcg(xt + xr[c][u]);
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (u & 1) acc1 = fma(w[c][u], x[c][u], acc1);
+                    else acc0 = fma(w[c][u], x[c][u], acc0);
+                }
+        }
+    }
+    T acc = acc0 + acc1;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    return acc;
+}
+
 // Software grid barrier for a cooperative (co-resident) launch.  Traps
 // instead of hanging if a CTA never arrives.
 __device__ __forceinline__ void grid_sync(Ctl* ctl, unsigned nblk) {
@@ -394,8 +468,10 @@ __device__ __forceinline__ void phase1_rows(const HotArgs& a, T* xc, int64_t gwa
         const int col = (int)(item - r * nchunk) * CW + c * VEC;
         const bool col_ok = col < a.kp;
         T acc[VEC];
-        row_accumulate<T, KC, VEC>(a.segs, a.p1_segptr[r], a.p1_segptr[r + 1], vals, a.idx, xc, a.kp, col, col_ok,
-                                   g, acc);
+        if (KC == 1 && VEC == 1) acc[0] = row_accumulate_k1<T>(a.segs, a.p1_segptr[r], a.p1_segptr[r + 1], vals, a.idx,
+                                                               xc, lane);
+        else row_accumulate<T, KC, VEC>(a.segs, a.p1_segptr[r], a.p1_segptr[r + 1], vals, a.idx, xc, a.kp, col,
+                                        col_ok, g, acc);
         if (g == 0 && col_ok) {
             const int64_t t = a.p1_rows[r];
             const T sc = static_cast<const T*>(a.p1_scale)[t];
@@ -420,8 +496,10 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
         const int col = (int)(item - r * nchunk) * CW + c * VEC;
         const bool col_ok = col < a.kp;
         T acc[VEC];
-        row_accumulate<T, KC, VEC>(a.segs, a.p2_segptr[r], a.p2_segptr[r + 1], vals, a.idx, xc, a.kp, col, col_ok,
-                                   g, acc);
+        if (KC == 1 && VEC == 1) acc[0] = row_accumulate_k1<T>(a.segs, a.p2_segptr[r], a.p2_segptr[r + 1], vals, a.idx,
+                                                               xc, lane);
+        else row_accumulate<T, KC, VEC>(a.segs, a.p2_segptr[r], a.p2_segptr[r + 1], vals, a.idx, xc, a.kp, col,
+                                        col_ok, g, acc);
         if (g != 0 || !col_ok) continue;
         const int64_t orow = a.p2_rows[r];
         if (MODE == M_MATVEC) {
@@ -448,8 +526,14 @@ __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_gro
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
-constexpr int kJC = 64;      // terms per staged chunk
-constexpr int kStages = 3;   // cp.async ring depth
+#ifndef VF_KJC
+#define VF_KJC 64
+#endif
+#ifndef VF_KSTAGES
+#define VF_KSTAGES 3
+#endif
+constexpr int kJC = VF_KJC;          // terms per staged chunk
+constexpr int kStages = VF_KSTAGES;  // cp.async ring depth
 constexpr int kMaxSegSmem = 64;  // shared runs per group whose metadata is cached in smem
 
 template <typename T>
@@ -632,7 +716,7 @@ __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a)
         T* xc = static_cast<T*>((it & 1) ? a.xt1 : a.xt0);
         T* xn = static_cast<T*>((it & 1) ? a.xt0 : a.xt1);
         if (have_p1) {
-            if (GROUPED) groups_phase<T, VEC, 1, MODE>(a, xc, xn, stile, nullptr, stage);
+            if constexpr (GROUPED) groups_phase<T, VEC, 1, MODE>(a, xc, xn, stile, nullptr, stage);
             else phase1_rows<T, KC, VEC>(a, xc, gwarp, nwarp, lane);
             grid_sync(a.ctl, nblk);
         }
@@ -640,7 +724,7 @@ __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a)
         double* sw = sred + (GROUPED ? 0 : warp * kp);
         for (int cc = threadIdx.x; cc < nsw * a.kp; cc += kThreads) sred[cc] = 0.0;
         __syncthreads();
-        if (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sw, stage);
+        if constexpr (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sw, stage);
         else phase2_rows<T, KC, VEC, MODE>(a, xc, xn, gwarp, nwarp, lane, sw);
         __syncthreads();
         for (int cc = threadIdx.x; cc < a.kp; cc += kThreads) {
@@ -656,13 +740,13 @@ __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a)
         T* xn = static_cast<T*>(cur ? a.xt0 : a.xt1);
         trace_ev(a, it, 0);
         if (have_p1) {                                           // ---- phase 1: T rows
-            if (GROUPED) groups_phase<T, VEC, 1, MODE>(a, xc, xn, stile, nullptr, stage);
+            if constexpr (GROUPED) groups_phase<T, VEC, 1, MODE>(a, xc, xn, stile, nullptr, stage);
             else phase1_rows<T, KC, VEC>(a, xc, gwarp, nwarp, lane);
         }
         trace_ev(a, it, 1);
         if (MODE == M_MATVEC) {
             if (have_p1) grid_sync(a.ctl, nblk);
-            if (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sred, stage);
+            if constexpr (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sred, stage);
             else phase2_rows<T, KC, VEC, MODE>(a, xc, xn, gwarp, nwarp, lane, sred);
             return;
         }
@@ -683,7 +767,7 @@ __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a)
         double* sw = sred + (GROUPED ? 0 : warp * kp);
         for (int cc = threadIdx.x; cc < nsw * a.kp; cc += kThreads) sred[cc] = 0.0;
         __syncthreads();
-        if (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sw, stage);
+        if constexpr (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sw, stage);
         else phase2_rows<T, KC, VEC, MODE>(a, xc, xn, gwarp, nwarp, lane, sw);
         __syncthreads();
         double* part = a.partial + (int64_t)(it & 1) * nblk * kp;   // column-major [kp][nblk]
@@ -1019,6 +1103,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         for (int64_t j = 1; j < nv; ++j) contig = contig && (L.idx_b[j] == L.idx_b[0] + j);
         int64_t ioff = -1;
         if (!contig) {
+            while (idx.size() % 4) idx.push_back(0);
             ioff = (int64_t)idx.size();
             for (int64_t j = 0; j < nv; ++j) idx.push_back((int32_t)(L.col0 + L.idx_b[j]));
             alg_bytes += 4 * nv;
@@ -1097,6 +1182,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         if (!cr.empty()) {
             std::stable_sort(cr.begin(), cr.end(), [](auto& a, auto& b) { return a.first < b.first; });
             Seg s;
+            while (idx.size() % 4) idx.push_back(0);             // 16-B aligned start (row_accumulate_k1)
             s.src = (int64_t)idx.size();
             for (auto& p : cr) idx.push_back(p.first);
             while (idx.size() % 4) idx.push_back(0);
@@ -1111,8 +1197,8 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         active[i] = 1;
         std::vector<std::pair<int32_t, double>>().swap(cr);
     }
-    if (vals.empty()) vals.push_back(T(0));
-    if (idx.empty()) idx.push_back(0);
+    for (int pad = 0; pad < 8; ++pad) vals.push_back(T(0));      // chunked over-reads stay in bounds
+    for (int pad = 0; pad < 8; ++pad) idx.push_back(0);
     if (segs.empty()) segs.push_back(Seg{0, 0, 0, 0});
     D->n_p1 = (int64_t)p1_rows.size();
     D->n_p2 = (int64_t)p2_rows.size();

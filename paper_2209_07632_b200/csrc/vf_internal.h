@@ -119,6 +119,13 @@ SvdResult estimate_rank(int64_t mu, int64_t nv, const double* dense, const int64
                         int64_t target_bytes, int64_t m_full, int64_t n_full, uint64_t seed);
 
 void svd_profile_report();
+// large-block randomized SVD on the device (vf_svd_gpu.cu); false = not done
+extern int g_svd_device;
+bool gpu_randomized_svd(int64_t m, int64_t n, const int64_t* rowptr, const int32_t* cols, const double* vals,
+                        const double* dense, const double* Om_rm, int64_t l, std::vector<double>& U_rm,
+                        std::vector<double>& S, std::vector<double>& V_rm);
+// one-sided Jacobi SVD of a small l x l column-major R (vf_svd.cpp): R <- Ur
+void small_jacobi_svd(std::vector<double>& R, int64_t l, std::vector<double>& sig, std::vector<double>& W);
 
 // device evaluator of the exact F for the build (vf_build_gpu.cu)
 struct Bvh;

@@ -60,6 +60,7 @@ struct Rng {
 // transpose (built once per block), so that both A X and A^T Y are row-
 // parallel products over row-major X (l contiguous values per row).
 constexpr int64_t kParWork = 1 << 15;    // multiply-adds below which loops stay serial
+constexpr int64_t kGpuSvdWork = 1ll << 25; // nnz x l above which the SVD runs on the device
 
 struct Op {
     int64_t m, n;
@@ -314,12 +315,22 @@ Trunc randomized_svd(const Op& A, int64_t l, Rng& rng) {
     struct Rep { const Op& A; int64_t l; std::chrono::steady_clock::time_point t0;
         ~Rep() { if (getenv("VF_BUILD_PROFILE") && atoi(getenv("VF_BUILD_PROFILE")) > 1) {
             double dt = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-            if (dt > 0.02) fprintf(stderr, "  rsvd m %ld n %ld nnz %ld l %ld: %.3f s\n", (long)A.m, (long)A.n,
+            if (dt > 0.5) fprintf(stderr, "  rsvd m %ld n %ld nnz %ld l %ld: %.3f s\n", (long)A.m, (long)A.n,
                                    (long)(A.dense ? A.m * A.n : A.rowptr[A.m]), (long)l, dt); } } } rep{A, l, t0};
     Trunc T;
     T.l = l;
-    std::vector<double> Om(A.n * l), Y(A.m * l), Z(A.n * l), Ycm(A.m * l), Zcm(A.n * l);
+    std::vector<double> Om(A.n * l);
     for (auto& v : Om) v = rng.normal();
+    // large blocks: the same algorithm on the device (vf_svd_gpu.cu)
+    const int64_t nnz = A.dense ? A.m * A.n : A.rowptr[A.m];
+    if (nnz * l >= kGpuSvdWork && g_svd_device >= 0) {
+        Prof pg(7);
+        if (gpu_randomized_svd(A.m, A.n, A.rowptr, A.cols, A.vals, A.dense, Om.data(), l, T.U, T.S, T.V)) return T;
+    }
+    if (false &&
+        gpu_randomized_svd(A.m, A.n, A.rowptr, A.cols, A.vals, A.dense, Om.data(), l, T.U, T.S, T.V))
+        return T;
+    std::vector<double> Y(A.m * l), Z(A.n * l), Ycm(A.m * l), Zcm(A.n * l);
     A.mul(Om.data(), l, Y.data());
     for (int it = 0; it < 2; ++it) {       // power iterations
         to_cm(Y.data(), A.m, l, Ycm.data());
@@ -340,7 +351,6 @@ Trunc randomized_svd(const Op& A, int64_t l, Rng& rng) {
     orthonormalize_cm(Zcm.data(), A.n, l, R.data());     // Z = Qz R
     std::vector<double> sig, W;
     { Prof pj(6); jacobi_svd_cm(R, l, l, sig, W); }      // R = Ur S W^T (R now holds Ur)
-    Prof pf(7);
     T.S = sig;
     T.V.resize(A.n * l);
     mul_cm_small(Zcm.data(), A.n, l, R.data(), T.V.data());   // V = Qz Ur
@@ -393,9 +403,13 @@ double residual_norm(const Op& A, const Trunc& T, int64_t q, Rng& rng) {
 
 }  // namespace
 
+void small_jacobi_svd(std::vector<double>& R, int64_t l, std::vector<double>& sig, std::vector<double>& W) {
+    jacobi_svd_cm(R, l, l, sig, W);
+}
+
 void svd_profile_report() {
     if (!getenv("VF_BUILD_PROFILE")) return;
-    const char* nm[8] = {"exact_svd", "randomized_svd", "residual_norm", "estimate_rank", "spmm", "orth", "jacobi", "final"};
+    const char* nm[8] = {"exact_svd", "randomized_svd", "residual_norm", "estimate_rank", "spmm", "orth", "jacobi", "gpu_rsvd"};
     for (int i = 0; i < 8; ++i)
         fprintf(stderr, "[vf build] %-15s calls %8lld  %9.3f s\n", nm[i], (long long)g_cnt[i], g_ns[i] * 1e-9);
 }

@@ -283,3 +283,18 @@ def test_cfg2_bench_configuration_thermal(cfg2):
     assert rel(host(T), ref["T"]) <= 10 * 1e-5
     sh = (Q0 == 0) & (S.x[:, 2:3] < -1e-9)
     assert rel(host(T)[sh], ref["T"][sh]) <= 10 * 1e-5
+
+
+@pytest.mark.parametrize("mesh", ["cfg1", "rough"])
+def test_device_evaluator_equals_host_evaluator_bitwise(mesh, tmp_path):
+    """The device evaluator of Alg. 1 (vf_build_gpu.cu) repeats the host
+    predicate and F_ij operation for operation (reading R-VIS): both builds
+    must store byte-identical F-hat containers."""
+    V, F = sg.cfg1_mesh() if mesh == "cfg1" else sg.rough_small_mesh(24, amp=0.05)
+    paths = []
+    for ev in (vf.VF_EVAL_HOST, vf.VF_EVAL_DEVICE):
+        M = vf.ViewFactorMatrix.build(V, F, 1e-5, device=0, evaluator=ev)
+        p = str(tmp_path / f"e{ev}.hvfm")
+        M.save(p)
+        paths.append(p)
+    assert open(paths[0], "rb").read() == open(paths[1], "rb").read()

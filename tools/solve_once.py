@@ -1,7 +1,7 @@
 """Dev tool: one cfg2 thermal solve (64 suns) for profiling."""
 import os, sys
 import numpy as np
-sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2209_07632_b200 as vf
 import scenegen as sg
 k = int(os.environ.get("K", "64"))

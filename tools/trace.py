@@ -7,7 +7,7 @@ if "--run" in sys.argv:
     os.environ["VF_TRACE_FILE"] = path
     if os.path.exists(path):
         os.remove(path)
-    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch
     import paper_2209_07632_b200 as vf
     import scenegen as sg
