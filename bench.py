@@ -392,6 +392,7 @@ def terrain_fhat(args, device):
     t0 = time.time()
     if path and os.path.exists(path):
         M = vf.ViewFactorMatrix.load(path, device=device)
+        vf.vf_set_mesh(M.h, V, F)              # geometry for vf_insolation
         built = False
     else:
         M = vf.ViewFactorMatrix.build(V, F, args.tol, dtype=dt, device=device)

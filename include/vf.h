@@ -165,6 +165,11 @@ int vf_last_solve_stats(vf_handle h, int* iters1, double* resid1, int* iters2, d
  * Qdir: N x k column-major HOST double output.  Needs a mesh-built handle. */
 int vf_insolation(vf_handle h, const double* suns, int k, double S, double* Qdir);
 
+/* Attach the mesh a loaded handle was built from (HOST arrays, copied) so
+ * that vf_insolation works on it: facet f of the mesh is facet f of the
+ * handle (nf must equal N); orient_up as in vf_build_opts. */
+int vf_set_mesh(vf_handle h, const vf_mesh* mesh, int orient_up);
+
 typedef struct {
     int64_t N;             /* facets                                               */
     int dtype;             /* VF_F64 / VF_F32                                      */

@@ -26,7 +26,7 @@ __all__ = [
     "vf_upload", "vf_set_stream", "vf_matvec", "vf_solve_radiosity", "vf_solve_thermal", "vf_insolation",
     "vf_info", "vf_last_solve_stats", "vf_enable_kernel_timing", "vf_kernel_timing", "VF_F64", "VF_F32",
     "VF_VIS_RAYCAST", "VF_VIS_CULL_ONLY", "HEADER", "vf_row_partition", "vf_shard_rows", "vf_row_range",
-    "vf_get_nccl_id", "vf_comm_init", "VF_EVAL_AUTO", "VF_EVAL_HOST", "VF_EVAL_DEVICE",
+    "vf_get_nccl_id", "vf_comm_init", "vf_set_mesh", "VF_EVAL_AUTO", "VF_EVAL_HOST", "VF_EVAL_DEVICE",
 ]
 
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "vf.h")
@@ -104,6 +104,7 @@ def lib():
             "vf_kernel_timing": ([H, ctypes.POINTER(d), ctypes.POINTER(i), ctypes.POINTER(d),
                                   ctypes.POINTER(i), ctypes.POINTER(i)], i),
             "vf_row_partition": ([H, i, P], i),
+            "vf_set_mesh": ([H, ctypes.POINTER(vf_mesh), i], i),
             "vf_shard_rows": ([H, i, i], i),
             "vf_row_range": ([H, ctypes.POINTER(I), ctypes.POINTER(I)], i),
             "vf_get_nccl_id": ([P], i),
@@ -215,6 +216,7 @@ def vf_upload(h, device: int = 0):
 
 def vf_free(h):
     if h:
+        _DIMS.pop(h.value if hasattr(h, "value") else int(h), None)
         lib().vf_free(h)
 
 
@@ -228,9 +230,29 @@ def vf_info(h) -> dict:
     return {name: getattr(info, name) for name, _ in vf_info_t._fields_}
 
 
+_DIMS: dict = {}
+
+
+def _dims(h):
+    """(N, dtype) of a handle; both are fixed for its lifetime, so they are
+    cached instead of calling vf_info (a host walk over all leaves) per call."""
+    key = h.value if hasattr(h, "value") else int(h)
+    d = _DIMS.get(key)
+    if d is None:
+        info = vf_info(h)
+        d = _DIMS[key] = (info["N"], info["dtype"])
+    return d
+
+
+def vf_set_mesh(h, V, F, orient_up: bool = True):
+    V = np.ascontiguousarray(V, dtype=np.float64)
+    F = np.ascontiguousarray(F, dtype=np.int32)
+    m = vf_mesh(V.shape[0], F.shape[0], V.ctypes.data, F.ctypes.data)
+    _check(lib().vf_set_mesh(h, ctypes.byref(m), int(bool(orient_up))))
+
+
 def vf_matvec(h, X, Y, nrhs: int | None = None):
-    info = vf_info(h)
-    N, dt = info["N"], info["dtype"]
+    N, dt = _dims(h)
     px, kx = _vec_ptr(X, N, dt, "X")
     py, ky = _vec_ptr(Y, N, dt, "Y", writable=True)
     k = nrhs or kx
@@ -240,8 +262,7 @@ def vf_matvec(h, X, Y, nrhs: int | None = None):
 
 
 def vf_solve_radiosity(h, E, rho, B, iters: int = 100, tol: float = 1e-12, clamp: bool = True):
-    info = vf_info(h)
-    N, dt = info["N"], info["dtype"]
+    N, dt = _dims(h)
     pe, k = _vec_ptr(E, N, dt, "E")
     pr, _ = _vec_ptr(rho, N, dt, "rho")
     pb, kb = _vec_ptr(B, N, dt, "B", writable=True)
@@ -251,8 +272,7 @@ def vf_solve_radiosity(h, E, rho, B, iters: int = 100, tol: float = 1e-12, clamp
 
 
 def vf_solve_thermal(h, Qdir, albedo, emiss, T, Qvis=None, Qir=None, iters: int = 100, tol: float = 1e-12):
-    info = vf_info(h)
-    N, dt = info["N"], info["dtype"]
+    N, dt = _dims(h)
     pq, k = _vec_ptr(Qdir, N, dt, "Qdir")
     pa, _ = _vec_ptr(albedo, N, dt, "albedo")
     pe, _ = _vec_ptr(emiss, N, dt, "emiss")
@@ -274,7 +294,7 @@ def vf_last_solve_stats(h) -> dict:
 def vf_insolation(h, suns, S: float = 1365.0) -> np.ndarray:
     """Host-side Q_dir: N x k column-major float64."""
     suns = np.ascontiguousarray(np.atleast_2d(suns), dtype=np.float64)
-    N = vf_info(h)["N"]
+    N = _dims(h)[0]
     Q = np.empty((N, suns.shape[0]), order="F")
     _check(lib().vf_insolation(h, suns.ctypes.data, suns.shape[0], float(S), Q.ctypes.data))
     return Q

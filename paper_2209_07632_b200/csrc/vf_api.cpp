@@ -68,6 +68,34 @@ static int finish(Handle* h, int device, vf_handle* out) {
     return VF_OK;
 }
 
+// Facet data of P:129: centroid, unit normal (right-hand rule, n_z > 0 when
+// orient_up: reading R-ORIENT), area.
+static int facet_data(const vf_mesh* mesh, int orient_up, std::vector<double>& x, std::vector<double>& n,
+                      std::vector<double>& A) {
+    const int64_t N = mesh->nf;
+    x.resize(3 * N); n.resize(3 * N); A.resize(N);
+    for (int64_t f = 0; f < N; ++f) {
+        int32_t ia = mesh->F[3 * f], ib = mesh->F[3 * f + 1], ic = mesh->F[3 * f + 2];
+        if (ia < 0 || ib < 0 || ic < 0 || ia >= mesh->nv || ib >= mesh->nv || ic >= mesh->nv)
+            return set_error(VF_EINVAL, "mesh: face index out of range");
+        const double* a = mesh->V + 3 * (int64_t)ia;
+        const double* b = mesh->V + 3 * (int64_t)ib;
+        const double* c = mesh->V + 3 * (int64_t)ic;
+        double e1[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
+        double e2[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+        double cr[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+        double len = std::sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
+        if (!(len > 0.0)) return set_error(VF_EINVAL, "mesh: zero-area face " + std::to_string(f));
+        double sgn = (orient_up && cr[2] < 0.0) ? -1.0 : 1.0;
+        for (int d = 0; d < 3; ++d) {
+            x[3 * f + d] = (a[d] + b[d] + c[d]) / 3.0;
+            n[3 * f + d] = sgn * cr[d] / len;
+        }
+        A[f] = 0.5 * len;
+    }
+    return VF_OK;
+}
+
 int vf_build(const vf_mesh* mesh, double tol, const vf_build_opts* opts, vf_handle* out) {
     GUARD({
         if (!mesh || !out || !mesh->V || !mesh->F || mesh->nf <= 0 || mesh->nv <= 0)
@@ -77,26 +105,8 @@ int vf_build(const vf_mesh* mesh, double tol, const vf_build_opts* opts, vf_hand
         int rc = check_opts(o, tol);
         if (rc) return rc;
         const int64_t N = mesh->nf;
-        std::vector<double> x(3 * N), n(3 * N), A(N);
-        for (int64_t f = 0; f < N; ++f) {
-            int32_t ia = mesh->F[3 * f], ib = mesh->F[3 * f + 1], ic = mesh->F[3 * f + 2];
-            if (ia < 0 || ib < 0 || ic < 0 || ia >= mesh->nv || ib >= mesh->nv || ic >= mesh->nv)
-                return set_error(VF_EINVAL, "vf_build: face index out of range");
-            const double* a = mesh->V + 3 * (int64_t)ia;
-            const double* b = mesh->V + 3 * (int64_t)ib;
-            const double* c = mesh->V + 3 * (int64_t)ic;
-            double e1[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]};
-            double e2[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
-            double cr[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
-            double len = std::sqrt(cr[0] * cr[0] + cr[1] * cr[1] + cr[2] * cr[2]);
-            if (!(len > 0.0)) return set_error(VF_EINVAL, "vf_build: zero-area face " + std::to_string(f));
-            double sgn = (o.orient_up && cr[2] < 0.0) ? -1.0 : 1.0;      // P:129, reading R-ORIENT
-            for (int d = 0; d < 3; ++d) {
-                x[3 * f + d] = (a[d] + b[d] + c[d]) / 3.0;
-                n[3 * f + d] = sgn * cr[d] / len;
-            }
-            A[f] = 0.5 * len;
-        }
+        std::vector<double> x, n, A;
+        if ((rc = facet_data(mesh, o.orient_up, x, n, A))) return rc;
         Handle* h = new Handle();
         rc = build_handle(h, N, x.data(), n.data(), A.data(), mesh->V, mesh->nv, mesh->F, N, nullptr, tol, o);
         if (rc) { delete h; return rc; }
@@ -276,6 +286,23 @@ int vf_kernel_timing(vf_handle hh, double* ms2, int* l2, double* ms1, int* l1, i
     if (l1) *l1 = h->launches_p1;
     if (lt) *lt = h->launches_total;
     return VF_OK;
+}
+
+int vf_set_mesh(vf_handle hh, const vf_mesh* mesh, int orient_up) {
+    GUARD({
+        if (!hh || !mesh || !mesh->V || !mesh->F) return set_error(VF_EINVAL, "vf_set_mesh: null argument");
+        Handle* h = reinterpret_cast<Handle*>(hh);
+        if (mesh->nf != h->N) return set_error(VF_EINVAL, "vf_set_mesh: mesh has a different facet count");
+        std::vector<double> x, n, A;
+        int rc = facet_data(mesh, orient_up, x, n, A);
+        if (rc) return rc;
+        h->x.swap(x); h->nrm.swap(n); h->A.swap(A);
+        h->occ_V.assign(mesh->V, mesh->V + 3 * mesh->nv);
+        h->occ_F.assign(mesh->F, mesh->F + 3 * mesh->nf);
+        h->tri_of.clear();
+        h->has_mesh = true;
+        return VF_OK;
+    })
 }
 
 int vf_row_partition(vf_handle hh, int world, int64_t* bounds) {

@@ -41,9 +41,17 @@ namespace {
 
 constexpr int kWarps = 8;               // warps per CTA (256 threads)
 constexpr int kThreads = kWarps * 32;
-constexpr int kMaxCtasPerSm = 2;
+#ifndef VF_CTAS
+#define VF_CTAS 2
+#endif
+constexpr int kMaxCtasPerSm = VF_CTAS;   // row-group (batched) kernels: smem-bound
+#ifndef VF_CTAS_ROW
+#define VF_CTAS_ROW 4
+#endif
+constexpr int kMaxCtasRow = VF_CTAS_ROW; // per-row (nrhs <= 2) kernels: latency-bound, more warps in flight
+template <bool GROUPED> __host__ __device__ constexpr int ctas_per_sm() { return GROUPED ? kMaxCtasPerSm : kMaxCtasRow; }
 constexpr int kMaxKp = 2048;
-constexpr int kMaxGrid = 512;           // CTAs of a persistent launch (<= 2 x SMs)            // columns per launch (sred: kWarps*kp doubles)
+constexpr int kMaxGrid = 1024;          // CTAs of a persistent launch
 constexpr double kSigmaSB = 5.670374419e-8;
 
 struct Seg {                            // one run of a row's terms
@@ -276,13 +284,17 @@ __device__ __forceinline__ void row_accumulate(const Seg* __restrict__ segs, int
         for (int v = 0; v < VEC; ++v) acc[v] += __shfl_xor_sync(0xffffffffu, acc[v], off);
 }
 
-// nrhs = 1 (kp = 1): the HBM-bound streaming case.  A warp owns the row;
-// lane l takes 4-term chunks c = l, l + 32, ... of every segment with one
-// 16-B load of 4 column indices (CSR) and 16-B loads of the values, two chunks
-// in flight per lane (8 terms, 96 B): enough bytes in flight per SM to cover
-// HBM latency.  Segment starts are 16-B aligned in vals and 4-aligned in idx
-// (upload_impl), arrays are padded so chunk over-reads stay in bounds, and
-// out-of-range terms are masked to exact zeros.
+// nrhs = 1 (kp = 1): the HBM-bound streaming case.  A warp owns the row and
+// works on up to 32 of its segments AT ONCE: lane l reads descriptor l, an
+// exclusive scan of the segments' 4-term chunk counts lays the chunks out in
+// one range, and lane l takes chunks l, l + 32, ... of that range (binary
+// search over the scan by warp shuffles gives each chunk its segment).  Each
+// chunk is one 16-B load of 4 column indices (CSR) and 16-B loads of 4
+// values; CH chunks are in flight per lane.  Short segments therefore do not
+// serialise memory latency.  Segment starts are 16-B aligned in vals and
+// 4-aligned in idx (upload_impl), the arrays are padded so chunk over-reads
+// stay in bounds, and out-of-range terms are masked to exact zeros.  The sum
+// order is fixed by the layout: results are bitwise reproducible.
 template <typename T> struct V4;
 template <> struct V4<double> {
     static __device__ __forceinline__ void ld(const double* p, double* v) {
@@ -297,44 +309,107 @@ template <> struct V4<float> {
     }
 };
 
-template <typename T>
+#ifndef VF_K1_CH
+#define VF_K1_CH 1
+#endif
+#ifndef VF_XVEC
+#define VF_XVEC 1
+#endif
+// 4 contiguous x values (16-B aligned): through L1 (matvec) or L2 only
+template <typename T, bool L1X> struct XV4;
+template <bool L1X> struct XV4<double, L1X> {
+    static __device__ __forceinline__ void ld(const double* p, double* v) {
+        const double2* q = reinterpret_cast<const double2*>(p);
+        const double2 a = L1X ? q[0] : __ldcg(q), b = L1X ? q[1] : __ldcg(q + 1);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    }
+};
+template <bool L1X> struct XV4<float, L1X> {
+    static __device__ __forceinline__ void ld(const float* p, float* v) {
+        const float4* q = reinterpret_cast<const float4*>(p);
+        const float4 a = L1X ? q[0] : __ldcg(q);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    }
+};
+#ifndef VF_MV_L1
+#define VF_MV_L1 1      // matvec: gather x through L1 (X read-only; T rows not cached before the barrier)
+#endif
+template <typename T, bool L1X>
 __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int64_t s0, int64_t s1,
                                                const T* __restrict__ vals, const int32_t* __restrict__ idx,
-                                               const T* xt, int lane) {
-    constexpr int CH = 2;                        // chunks of 4 terms in flight per lane
+                                               const T* xt, int lane, int64_t nx) {
+    constexpr int CH = VF_K1_CH;                 // chunks of 4 terms in flight per lane
+    constexpr unsigned FULL = 0xffffffffu;
     T acc0 = T(0), acc1 = T(0);
-    for (int64_t s = s0; s < s1; ++s) {
-        const Seg sg = segs[s];
-        const T* __restrict__ vp = vals + sg.val_off;
-        const int len = sg.len;
-        for (int c0 = lane * 4; c0 < len; c0 += 32 * 4 * CH) {
+    for (int64_t sb = s0; sb < s1; sb += 32) {
+        const int ns = (int)(s1 - sb < 32 ? s1 - sb : 32);
+        Seg my{0, 0, 0, 0};
+        if (lane < ns) my = segs[sb + lane];
+        const int nch = (my.len + 3) >> 2;
+        int incl = nch;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, off);
+            if (lane >= off) incl += v;
+        }
+        const int excl = incl - nch;
+        const int total = __shfl_sync(FULL, incl, 31);
+        for (int base = 0; base < total; base += 32 * CH) {     // warp-uniform trip count (shuffles below)
             T w[CH][4];
-            int64_t xr[CH][4];
+            int32_t xr[CH][4];                   // XT rows < 2^31 (checked at upload)
+            bool vx[CH];                         // contiguous, aligned x: vector loads
+            bool l1[CH];                         // X rows (read-only here) through L1; T rows via L2
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
-                const int e = c0 + c * 128;
-                if (e < len) {
-                    V4<T>::ld(vp + e, w[c]);
-                    if (sg.kind) {
-                        const int4 q = __ldg(reinterpret_cast<const int4*>(idx + sg.src + e));
+                const int cc = base + lane + 32 * c;
+                int g = 0;                        // last segment with excl <= cc
+#pragma unroll
+                for (int step = 16; step > 0; step >>= 1) {
+                    const int cand = g + step;
+                    const int e = __shfl_sync(FULL, excl, cand & 31);
+                    if (cand < ns && e <= cc) g = cand;
+                }
+                const int64_t g_off = __shfl_sync(FULL, my.val_off, g);
+                const int64_t g_src = __shfl_sync(FULL, my.src, g);
+                const int g_len = __shfl_sync(FULL, my.len, g);
+                const int g_kind = __shfl_sync(FULL, my.kind, g);
+                const int g_excl = __shfl_sync(FULL, excl, g);
+                if (cc < total) {
+                    const int e = (cc - g_excl) * 4;
+                    V4<T>::ld(vals + g_off + e, w[c]);
+                    vx[c] = VF_XVEC && !g_kind && e + 3 < g_len && ((g_src + e) & (16 / sizeof(T) - 1)) == 0;
+                    l1[c] = L1X && (g_kind || g_src < nx);
+                    if (g_kind) {
+                        const int4 q = __ldg(reinterpret_cast<const int4*>(idx + g_src + e));
                         xr[c][0] = q.x; xr[c][1] = q.y; xr[c][2] = q.z; xr[c][3] = q.w;
                     } else {
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) xr[c][u] = sg.src + e + u;
+                        for (int u = 0; u < 4; ++u) xr[c][u] = (int32_t)(g_src + e + u);
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
-                        if (e + u >= len) { w[c][u] = T(0); xr[c][u] = sg.kind ? 0 : sg.src; }
+                        if (e + u >= g_len) { w[c][u] = T(0); xr[c][u] = g_kind ? 0 : (int32_t)g_src; }
                 } else {
+                    vx[c] = false;
+                    l1[c] = false;
 #pragma unroll
                     for (int u = 0; u < 4; ++u) { w[c][u] = T(0); xr[c][u] = 0; }
                 }
             }
             T x[CH][4];
 #pragma unroll
-            for (int c = 0; c < CH; ++c)
+            for (int c = 0; c < CH; ++c) {
+                if (vx[c]) {
+                    if (l1[c]) XV4<T, true>::ld(xt + xr[c][0], x[c]);
+                    else XV4<T, false>::ld(xt + xr[c][0], x[c]);
+                } else if (l1[c]) {
 #pragma unroll
-                for (int u = 0; u < 4; ++u) x[c][u] = __ldcg(xt + xr[c][u]);
+                    for (int u = 0; u < 4; ++u) x[c][u] = xt[xr[c][u]];
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) x[c][u] = __ldcg(xt + xr[c][u]);
+                }
+            }
 #pragma unroll
             for (int c = 0; c < CH; ++c)
 #pragma unroll
@@ -346,7 +421,7 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
     }
     T acc = acc0 + acc1;
 #pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL, acc, off);
     return acc;
 }
 
@@ -455,6 +530,51 @@ __device__ __forceinline__ void solve_epilogue(const HotArgs& a, const T* xc, T*
     Vec<T, VEC>::st(static_cast<T*>(a.Q) + o, acc);
 }
 
+// Phase 1 (a2) for nrhs = 1: a warp per row group (up to kGroup terms t of one
+// SVD block, which share the block's V row set J_b): T_t = S_t V[:,t]^T X_J
+// as a small GEMV.  Lanes stride over J_b; each x_j is loaded once and
+// multiplied into the group's kGroup accumulators, whose V values are
+// contiguous per t (coalesced across lanes); kGroup + 1 independent loads per
+// lane and step keep HBM busy.  Fixed-order xor reductions, one store per t.
+template <typename T>
+__device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_t gwarp, int lane) {
+    const T* vals = static_cast<const T*>(a.vals);
+    for (int32_t q = a.s1_ptr[gwarp]; q < a.s1_ptr[gwarp + 1]; ++q) {
+        const int64_t gi = a.s1_items[q];
+        const Group G = a.g1[gi];
+        const GSeg sg = a.gseg[G.seg_off];
+        constexpr int H = kGroup / 2;                 // rows per pass (register budget)
+        T mine = T(0);
+        for (int h0 = 0; h0 < G.nrows; h0 += H) {
+            int32_t vo[H];                            // value offsets (< 2^31 elements)
+#pragma unroll
+            for (int r = 0; r < H; ++r) vo[r] = h0 + r < G.nrows ? (int32_t)a.gvo[G.seg_off * kGroup + h0 + r] : -1;
+            T acc[H];
+#pragma unroll
+            for (int r = 0; r < H; ++r) acc[r] = T(0);
+            for (int j = lane; j < sg.len; j += 32) {
+                const int64_t row = sg.kind ? (int64_t)__ldg(a.idx + sg.src + j) : sg.src + j;
+                const T x = __ldcg(xc + row);
+                T v[H];
+#pragma unroll
+                for (int r = 0; r < H; ++r) v[r] = vo[r] >= 0 ? __ldg(vals + vo[r] + j) : T(0);
+#pragma unroll
+                for (int r = 0; r < H; ++r) acc[r] = fma(v[r], x, acc[r]);
+            }
+#pragma unroll
+            for (int r = 0; r < H; ++r) {
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], off);
+                if (lane == h0 + r) mine = acc[r];
+            }
+        }
+        if (lane < G.nrows) {
+            const int64_t t = a.grow1[gi * kGroup + lane];
+            xc[a.N + t] = static_cast<const T*>(a.p1_scale)[t] * mine;
+        }
+    }
+}
+
 // Phase 1 (a2), per-row layout.
 template <typename T, int KC, int VEC>
 __device__ __forceinline__ void phase1_rows(const HotArgs& a, T* xc, int64_t gwarp, int64_t nwarp, int lane) {
@@ -468,8 +588,8 @@ __device__ __forceinline__ void phase1_rows(const HotArgs& a, T* xc, int64_t gwa
         const int col = (int)(item - r * nchunk) * CW + c * VEC;
         const bool col_ok = col < a.kp;
         T acc[VEC];
-        if (KC == 1 && VEC == 1) acc[0] = row_accumulate_k1<T>(a.segs, a.p1_segptr[r], a.p1_segptr[r + 1], vals, a.idx,
-                                                               xc, lane);
+        if (KC == 1 && VEC == 1) acc[0] = row_accumulate_k1<T, false>(a.segs, a.p1_segptr[r], a.p1_segptr[r + 1], vals,
+                                                                      a.idx, xc, lane, a.N);
         else row_accumulate<T, KC, VEC>(a.segs, a.p1_segptr[r], a.p1_segptr[r + 1], vals, a.idx, xc, a.kp, col,
                                         col_ok, g, acc);
         if (g == 0 && col_ok) {
@@ -496,8 +616,9 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
         const int col = (int)(item - r * nchunk) * CW + c * VEC;
         const bool col_ok = col < a.kp;
         T acc[VEC];
-        if (KC == 1 && VEC == 1) acc[0] = row_accumulate_k1<T>(a.segs, a.p2_segptr[r], a.p2_segptr[r + 1], vals, a.idx,
-                                                               xc, lane);
+        if (KC == 1 && VEC == 1)
+            acc[0] = row_accumulate_k1<T, VF_MV_L1 && MODE == M_MATVEC>(a.segs, a.p2_segptr[r], a.p2_segptr[r + 1], vals,
+                                                                         a.idx, xc, lane, a.N);
         else row_accumulate<T, KC, VEC>(a.segs, a.p2_segptr[r], a.p2_segptr[r + 1], vals, a.idx, xc, a.kp, col,
                                         col_ok, g, acc);
         if (g != 0 || !col_ok) continue;
@@ -699,7 +820,7 @@ __device__ __forceinline__ void groups_phase(const HotArgs& a, T* xc, T* xn, dou
 // column has r <= tol or `iters` is reached.  GROUPED selects the row-group
 // layout (VEC columns per lane) or the per-row layout (KC lanes x VEC).
 template <typename T, int KC, int VEC, int MODE, bool GROUPED>
-__global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a) {
+__global__ void __launch_bounds__(kThreads, ctas_per_sm<GROUPED>()) hot_kernel(HotArgs a) {
     extern __shared__ double sred[];        // [residual partials | cp.async stage ring (row groups)]
     __shared__ double stile[GROUPED ? kWarps * kGroup * 2 * VEC : 1];
     T* stage = reinterpret_cast<T*>(sred + ((a.kp + 1) & ~1));
@@ -707,7 +828,7 @@ __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a)
     const int64_t kp = a.kp;
     const int64_t gwarp = (int64_t)blockIdx.x * kWarps + warp, nwarp = (int64_t)gridDim.x * kWarps;
     const unsigned nblk = gridDim.x;
-    const bool have_p1 = GROUPED ? a.n_g1 > 0 : a.n_p1 > 0;
+    const bool have_p1 = (GROUPED || (KC == 1 && VEC == 1)) ? a.n_g1 > 0 : a.n_p1 > 0;
     if (MODE == M_STEP) {
         // ROWS mode (a6): one iteration on this rank's rows; the iterate
         // parity and the stop flag live in ctl (rows_decide_kernel).
@@ -717,6 +838,7 @@ __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a)
         T* xn = static_cast<T*>((it & 1) ? a.xt0 : a.xt1);
         if (have_p1) {
             if constexpr (GROUPED) groups_phase<T, VEC, 1, MODE>(a, xc, xn, stile, nullptr, stage);
+            else if constexpr (KC == 1 && VEC == 1) phase1_groups_k1<T>(a, xc, gwarp, lane);
             else phase1_rows<T, KC, VEC>(a, xc, gwarp, nwarp, lane);
             grid_sync(a.ctl, nblk);
         }
@@ -741,13 +863,16 @@ __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a)
         trace_ev(a, it, 0);
         if (have_p1) {                                           // ---- phase 1: T rows
             if constexpr (GROUPED) groups_phase<T, VEC, 1, MODE>(a, xc, xn, stile, nullptr, stage);
+            else if constexpr (KC == 1 && VEC == 1) phase1_groups_k1<T>(a, xc, gwarp, lane);
             else phase1_rows<T, KC, VEC>(a, xc, gwarp, nwarp, lane);
         }
         trace_ev(a, it, 1);
         if (MODE == M_MATVEC) {
             if (have_p1) grid_sync(a.ctl, nblk);
+            trace_ev(a, it, 2);
             if constexpr (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sred, stage);
             else phase2_rows<T, KC, VEC, MODE>(a, xc, xn, gwarp, nwarp, lane, sred);
+            trace_ev(a, it, 3);
             return;
         }
         grid_sync(a.ctl, nblk);                                  // B1
@@ -783,15 +908,8 @@ __global__ void __launch_bounds__(kThreads, kMaxCtasPerSm) hot_kernel(HotArgs a)
         // lanes over CTAs, all loads in flight, fixed xor tree.
         for (int c = blockIdx.x + (int)nblk * warp; c < a.k; c += (int)nblk * kWarps) {
             const double* pc = part + (int64_t)c * nblk;
-            double v[kMaxGrid / 32];
-#pragma unroll
-            for (int i = 0; i < kMaxGrid / 32; ++i) {
-                const unsigned b = lane + 32u * i;
-                v[i] = b < nblk ? __ldcg(pc + b) : 0.0;
-            }
             double sum = 0.0;
-#pragma unroll
-            for (int i = 0; i < kMaxGrid / 32; ++i) sum += v[i];
+            for (unsigned b = lane; b < nblk; b += 32u) sum += __ldcg(pc + b);
 #pragma unroll
             for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
             if (lane == 0) {
@@ -1077,8 +1195,13 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                      [&](int a, int b) { return h->leaves[a].level < h->leaves[b].level; });
     std::vector<int64_t> toff(h->leaves.size(), -1);
     int64_t NT = 0;
-    for (int b : svd_ids) { toff[b] = NT; NT += h->leaves[b].q; }
+    for (int b : svd_ids) {                  // (N + toff) % 4 == 0: aligned vector loads of T rows
+        while ((N + NT) % 4) ++NT;
+        toff[b] = NT;
+        NT += h->leaves[b].q;
+    }
     D->NT = NT;
+    if (N + NT >= INT32_MAX) return set_error(VF_EUNSUPPORTED, "N + sum of ranks must be < 2^31");
 
     std::vector<T> vals;
     std::vector<int32_t> idx;
@@ -1095,7 +1218,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     // ---- phase 1 rows: t = (b, l) ----
     std::vector<int64_t> p1_segptr(1, 0);
     std::vector<int32_t> p1_rows;
-    std::vector<T> p1_scale;
+    std::vector<T> p1_scale(std::max<int64_t>(NT, 1), T(0));
     for (int b : svd_ids) {
         const Leaf& L = h->leaves[b];
         const int64_t nv = (int64_t)L.idx_b.size(), q = L.q;
@@ -1120,7 +1243,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             segs.push_back(s);
             p1_segptr.push_back((int64_t)segs.size() - 0);
             p1_rows.push_back((int32_t)(toff[b] + l));
-            p1_scale.push_back((T)L.s[l]);
+            p1_scale[toff[b] + l] = (T)L.s[l];          // indexed by T row (with alignment gaps)
         }
         alg_bytes += (int64_t)sizeof(T) * (q * nv + q);
         alg_flops += 2 * q * nv + q;
@@ -1290,7 +1413,16 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         return c;
     };
     for (int64_t r = 0; r < (int64_t)p1_rows.size(); ++r) D->cost_p1.push_back(row_cost(p1_segptr, r));
-    for (int64_t r = 0; r < (int64_t)p2_rows.size(); ++r) D->cost_p2.push_back(row_cost(p2_segptr, r));
+    // phase-2 rows (per-row layout): time ~ rounds of 32 lanes x 2 chunks x 4 terms over
+    // batches of 32 segments (row_accumulate_k1), plus a per-row constant
+    for (int64_t r = 0; r < (int64_t)p2_rows.size(); ++r) {
+        int64_t c = 2, nch = 0, ns = 0;
+        for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1]; ++q) {
+            nch += (segs[q].len + 3) / 4;
+            if (++ns == 32 || q + 1 == p2_segptr[r + 1]) { c += 1 + (nch + 63) / 64; nch = 0; ns = 0; }
+        }
+        D->cost_p2.push_back(c * 256);
+    }
     auto group_cost = [&](const Group& G, const std::vector<int64_t>& gcsr, int64_t gi) {
         int64_t c = 16, mx = 0;
         for (int q = 0; q < G.nseg; ++q) c += gsegv[G.seg_off + q].len;
@@ -1300,7 +1432,9 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         }
         return c + mx;
     };
-    for (int64_t g = 0; g < D->n_g1; ++g) D->cost_g1.push_back(group_cost(g1v[g], gcsr1v, g));
+    // phase-1 groups: bytes scale with rows x |J_b| (the nrhs = 1 warp streams all of them)
+    for (int64_t g = 0; g < D->n_g1; ++g)
+        D->cost_g1.push_back(16 + (int64_t)g1v[g].nrows * gsegv[g1v[g].seg_off].len);
     for (int64_t g = 0; g < D->n_g2; ++g) D->cost_g2.push_back(group_cost(g2v[g], gcsr2v, g));
     if (gsegv.empty()) gsegv.push_back(GSeg{0, 0, 0});
     if (gvov.empty()) gvov.push_back(0);
@@ -1418,7 +1552,7 @@ int ensure_scratch(DeviceHMat* D, int kp) {
     for (void*& b : D->pv) CK(cudaMalloc(&b, std::max<size_t>(16, rows * D->w)));
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, D->device);
-    const int64_t nblk = (int64_t)nsm * kMaxCtasPerSm;
+    const int64_t nblk = (int64_t)nsm * std::max(kMaxCtasPerSm, kMaxCtasRow);
     if (D->partial) cudaFree(D->partial);
     CK(cudaMalloc((void**)&D->partial, (size_t)2 * nblk * kp * 8));
     CK(cudaMemset(D->partial, 0, (size_t)2 * nblk * kp * 8));
@@ -1557,19 +1691,22 @@ int launch_hot_t(Handle* h, HotArgs& a, cudaStream_t st) {
     if (per_sm < 1) return set_error(VF_ECUDA, "hot kernel cannot be resident");
     int nsm = 148;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
-    const int grid = std::min(kMaxGrid, nsm * std::min(per_sm, kMaxCtasPerSm));
+    const int grid = std::min(kMaxGrid, nsm * std::min(per_sm, ctas_per_sm<GROUPED>()));
     const int cw = GROUPED ? 2 * VEC : KC * VEC;
     const int nchunk = (a.kp + cw - 1) / cw;
     const int nworkers = GROUPED ? grid : grid * kWarps;
     DeviceHMat::Sched s1, s2;
     int rc;
-    if ((rc = get_sched(D, 1, GROUPED, nchunk, nworkers, &s1)) || (rc = get_sched(D, 2, GROUPED, nchunk, nworkers, &s2)))
+    // nrhs = 1: phase 1 runs per row group (phase1_groups_k1), one warp per group
+    const bool g1k1 = !GROUPED && KC == 1 && VEC == 1;
+    if ((rc = get_sched(D, 1, GROUPED || g1k1, g1k1 ? 1 : nchunk, nworkers, &s1)) ||
+        (rc = get_sched(D, 2, GROUPED, nchunk, nworkers, &s2)))
         return rc;
     a.s1_ptr = s1.ptr; a.s1_items = s1.items; a.s2_ptr = s2.ptr; a.s2_items = s2.items;
     static const char* trace_file = getenv("VF_TRACE_FILE");
     unsigned long long* tbuf = nullptr;
     const int tit = 64;
-    if (trace_file && MODE == M_SOLVE) {    // (M_STEP: not traced)
+    if (trace_file && MODE != M_STEP) {     // (M_STEP: not traced)
         CK(cudaMalloc(&tbuf, (size_t)tit * 5 * grid * 8));
         CK(cudaMemsetAsync(tbuf, 0, (size_t)tit * 5 * grid * 8, st));
         a.trace = tbuf;
