@@ -335,9 +335,13 @@ def run_gpu(args, rank, world, local_rank):
         ach_gbs = bytes_launch / (avg * 1e-3) / 1e9 if avg > 0 else 0.0
         roof = {"bound": "alu", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": ach_tf / peak_tf if peak_tf else None, "traffic": None,
-                "kernel": f"hot_kernel<{'double' if dt == 'f64' else 'float'},4,4,M_SOLVE> (persistent Jacobi "
-                          "solve: phase 1 V^T X, grid barrier, phase 2 row-owner accumulate + fused epilogue, "
-                          "residual decision; one launch per thermal stage)",
+                "kernel": (f"res_kernel<{'double' if dt == 'f64' else 'float'},M_SOLVE> (persistent Jacobi solve, "
+                           "F-hat resident in shared memory: phase 1 V^T X, grid barrier, phase 2 row-owner "
+                           "accumulate + fused epilogue, residual decision; one launch per thermal stage)"
+                           if info.get("resident") else
+                           f"hot_kernel<{'double' if dt == 'f64' else 'float'},1,8,M_SOLVE,grouped> (persistent "
+                           "Jacobi solve: phase 1 V^T X, grid barrier, phase 2 row-owner accumulate + fused "
+                           "epilogue, residual decision; one launch per thermal stage)"),
                 "peak_basis": f"derived: 148 SM x {64 if dt == 'f64' else 128} {dt.upper()} FMA/clk x 2 x "
                               f"{smax:.0f} MHz (sm_max of {pk_kind} MEASURED_PEAKS.json); DESIGN.md §Roofline",
                 "avg_launch_ms": avg, "launches": l2, "applies_per_launch": n_iters / max(l2, 1),

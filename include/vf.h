@@ -196,6 +196,8 @@ typedef struct {
     int64_t p2_src_rows;   /* distinct X/T rows phase 2 reads                        */
     int64_t p1_flops_per_col, p2_flops_per_col;
     int64_t groups1, groups2;  /* row groups of the batched layout (phase 1 / 2)      */
+    int64_t resident;      /* 1: batched applies (nrhs >= 9) keep F-hat in shared
+                              memory across iterations (res_kernel); 0: streamed    */
 } vf_info_t;
 
 int vf_info(vf_handle h, vf_info_t* out);

@@ -31,6 +31,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <type_traits>
 #include <vector>
 
 #include "vf_internal.h"
@@ -815,6 +816,302 @@ __device__ __forceinline__ void groups_phase(const HotArgs& a, T* xc, T* xn, dou
     }
 }
 
+// ---- resident batched path (nrhs >= 9, kp a multiple of 16).  The row
+// groups of both phases are assigned to CTAs once (one CTA per SM, static
+// LPT by bytes under the shared-memory capacity) and each CTA keeps the F-hat
+// values of its groups in SHARED MEMORY for the whole persistent launch: a
+// Jacobi solve streams F-hat from HBM once per stage, not once per iteration.
+// A group's weights are one [K][16] block over the union of its rows'
+// sources: the shared dense-leaf / U (phase 2) or V (phase 1) runs, then the
+// union of the rows' merged-CSR columns (rows without an entry hold zeros),
+// so every source row of XT is staged once per item and no term is gathered
+// serially.  Per iteration a work item (group, 16-column chunk) walks K in
+// slices of kKS source rows: slice s+1 is staged with cp.async (XT rows from
+// L2; source row indices from smem) while thread (r, c) of the 16 x 16 tile
+// sums W[j][r] X[j][c] over slice s; then the fused epilogue.  Sum order is
+// fixed: bitwise reproducible.
+#ifndef VF_RKS
+#define VF_RKS 256
+#endif
+#ifndef VF_RST
+#define VF_RST 2
+#endif
+constexpr int kKS = VF_RKS;        // source rows per staged slice
+constexpr int kRS = VF_RST;        // staging ring depth (slices in flight: kRS - 1)
+struct RGroup {
+    int32_t nrows;     // <= 16
+    int32_t K;         // source rows (shared runs + CSR column union)
+    int32_t w_off;     // [K][16] weights at this element offset of the CTA's smem blob
+    int32_t s_off;     // K source XT rows at this int offset of the CTA's smem index area
+    int64_t out_off;   // 16 output rows (tree rows or T rows) at outrow[out_off ..]
+};
+struct ResArgs {
+    const RGroup* groups;
+    const int32_t* outrow;
+    const void* wblob;            // all CTAs' value blobs, concatenated
+    const int64_t* cta_woff;      // [grid + 1] element offsets of each CTA's value blob
+    const int32_t* sblob;         // all CTAs' source-row lists, concatenated
+    const int64_t* cta_soff;      // [grid + 1]
+    const int32_t* p1_ptr;        // [grid + 1] phase-1 groups of each CTA in p1_list
+    const int32_t* p1_list;
+    const int32_t* p2_ptr;
+    const int32_t* p2_list;
+    int wcap;                     // smem elements reserved for the value blob
+    int scap;                     // smem ints reserved for the source rows
+};
+
+// stage X[src_j, cb .. cb+16) for j in [j0, j0 + n) into Xs[j - j0][16]
+template <typename T>
+__device__ __forceinline__ void res_stage(const int32_t* S, int j0, int n, const T* xc, int64_t kp, int cb, T* Xs) {
+    constexpr int EPL = 16 / (int)sizeof(T);          // elements per 16-B copy
+    constexpr int OPS = 16 / EPL;                     // copies per staged row
+    for (int op = threadIdx.x; op < n * OPS; op += kThreads) {
+        const int j = op / OPS, part = op - j * OPS;
+        const int64_t row = S[j0 + j];
+        cpa<16>(Xs + j * 16 + part * EPL, xc + row * kp + cb + part * EPL, 16);
+    }
+}
+
+// FP64 tensor-core MMA (DMMA, mma.sync m8n8k4; FP64 has no tcgen05 kind on
+// sm_100a): D(8x8) += A(8x4, row) B(4x8, col).  Fragments: a = A[lane/4][lane%4],
+// b = B[lane%4][lane/4], d[i] = D[lane/4][2 (lane%4) + i].
+__device__ __forceinline__ void dmma884(double* d, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
+                 : "+d"(d[0]), "+d"(d[1])
+                 : "d"(a), "d"(b));
+}
+
+struct ResCursor {
+    int g, ch, sl;
+    RGroup G;
+};
+
+template <typename T, int PHASE, int MODE>
+__device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, const T* W, const int32_t* S, T* Xs,
+                                          T* xc, T* xn, double* sred, double* tile, double* red) {
+    const int32_t* ptr = PHASE == 1 ? r.p1_ptr : r.p2_ptr;
+    const int32_t* lst = PHASE == 1 ? r.p1_list : r.p2_list;
+    const int g0 = ptr[blockIdx.x], g1 = ptr[blockIdx.x + 1];
+    if (g0 == g1) return;
+    const int nchunk = a.kp / 16;
+    const int t = threadIdx.x, rr = t >> 4, cc = t & 15;
+    const int64_t kp = a.kp;
+    // steps = (group, 16-column chunk, K slice) in order
+    int total = 0;
+    for (int g = g0; g < g1; ++g) total += nchunk * ((r.groups[lst[g]].K + kKS - 1) / kKS);
+    auto advance = [&](ResCursor& c) {
+        if (++c.sl * kKS < c.G.K) return;
+        c.sl = 0;
+        if (++c.ch < nchunk) return;
+        c.ch = 0;
+        if (++c.g < g1) c.G = r.groups[lst[c.g]];
+    };
+    auto stage = [&](const ResCursor& c, T* dst) {
+        const int j0 = c.sl * kKS;
+        res_stage<T>(S + c.G.s_off, j0, min(kKS, c.G.K - j0), xc, kp, c.ch * 16, dst);
+    };
+    ResCursor cur{g0, 0, 0, r.groups[lst[g0]]};
+    ResCursor nxt = cur;
+#pragma unroll
+    for (int p = 0; p < kRS - 1; ++p) {                // prologue: kRS - 1 slices in flight
+        if (p < total) {
+            stage(nxt, Xs + p * kKS * 16);
+            advance(nxt);
+        }
+        cpa_commit();
+    }
+    T acc0 = T(0), acc1 = T(0);
+    double dacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};   // DMMA tiles (double)
+    T e_pre = T(0), b_pre = T(0);                      // epilogue operands, fetched at an item's first slice
+    for (int step = 0; step < total; ++step) {
+        if (step + kRS - 1 < total) {
+            stage(nxt, Xs + ((step + kRS - 1) % kRS) * kKS * 16);
+            advance(nxt);
+        }
+        cpa_commit();
+        if (PHASE == 2 && MODE != M_MATVEC && cur.sl == 0 && rr < cur.G.nrows) {
+            const int64_t o = (int64_t)__ldg(r.outrow + cur.G.out_off + rr) * kp + cur.ch * 16 + cc;
+            e_pre = __ldcg(static_cast<const T*>(a.E) + o);
+            b_pre = __ldcg(xc + o);
+        }
+        cpa_wait<kRS - 1>();
+        __syncthreads();
+        const T* X = Xs + (step % kRS) * kKS * 16;
+        const RGroup& G = cur.G;
+        const int j0 = cur.sl * kKS, n = min(kKS, G.K - j0);
+        if constexpr (std::is_same<T, double>::value) {
+            // the 16 x 16 tile as 4 DMMA 8x8 tiles; warp w takes k-blocks
+            // w, w + 8, ... of the slice (A = W^T from the resident block, B = the
+            // staged XT rows); partial tiles are summed over warps at the item end
+            const int lane = t & 31, warp = t >> 5;
+            const int kr = lane & 3, mn = lane >> 2;
+            const double* wb = W + G.w_off + (int64_t)j0 * 16;
+            for (int kb = warp * 4; kb < n; kb += 32) {
+                const int j = kb + kr;
+                const bool ok = j < n;
+                const double a0 = ok ? wb[j * 16 + mn] : 0.0, a1 = ok ? wb[j * 16 + 8 + mn] : 0.0;
+                const double b0 = ok ? X[j * 16 + mn] : 0.0, b1 = ok ? X[j * 16 + 8 + mn] : 0.0;
+                dmma884(dacc[0], a0, b0);
+                dmma884(dacc[1], a0, b1);
+                dmma884(dacc[2], a1, b0);
+                dmma884(dacc[3], a1, b1);
+            }
+        } else if (rr < G.nrows) {
+            // 8 independent smem load pairs in flight per thread
+            const T* w = W + G.w_off + (int64_t)j0 * 16 + rr;
+            const T* x = X + cc;
+            T a2 = T(0), a3 = T(0);
+            int j = 0;
+            for (; j + 7 < n; j += 8) {
+                T wv[8], xv[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) { wv[u] = w[(j + u) * 16]; xv[u] = x[(j + u) * 16]; }
+                acc0 = fma(wv[0], xv[0], acc0);
+                acc1 = fma(wv[1], xv[1], acc1);
+                a2 = fma(wv[2], xv[2], a2);
+                a3 = fma(wv[3], xv[3], a3);
+                acc0 = fma(wv[4], xv[4], acc0);
+                acc1 = fma(wv[5], xv[5], acc1);
+                a2 = fma(wv[6], xv[6], a2);
+                a3 = fma(wv[7], xv[7], a3);
+            }
+            for (; j < n; ++j) acc0 = fma(w[j * 16], x[j * 16], acc0);
+            acc0 += a2;
+            acc1 += a3;
+        }
+        if (j0 + n >= G.K) {                               // last slice: epilogue of item (G, chunk)
+            T q = acc0 + acc1;
+            acc0 = acc1 = T(0);
+            if constexpr (std::is_same<T, double>::value) {   // sum the warps' DMMA tiles in warp order
+                const int lane = t & 31, warp = t >> 5;
+#pragma unroll
+                for (int tl = 0; tl < 4; ++tl) {
+                    red[((warp * 4 + tl) * 32 + lane) * 2] = dacc[tl][0];
+                    red[((warp * 4 + tl) * 32 + lane) * 2 + 1] = dacc[tl][1];
+                    dacc[tl][0] = dacc[tl][1] = 0.0;
+                }
+                __syncthreads();
+                const int tl = (rr >> 3) * 2 + (cc >> 3);
+                const int ln = (rr & 7) * 4 + ((cc & 7) >> 1), ii = cc & 1;
+                double sum = 0.0;
+                for (int w2 = 0; w2 < kWarps; ++w2) sum += red[((w2 * 4 + tl) * 32 + ln) * 2 + ii];
+                q = sum;
+            }
+            const int col = cur.ch * 16 + cc;
+            double d2 = 0.0;
+            if (rr < G.nrows) {
+                const int64_t orow = __ldg(r.outrow + G.out_off + rr);
+                if (PHASE == 1) {
+                    xc[(a.N + orow) * kp + col] = static_cast<const T*>(a.p1_scale)[orow] * q;
+                } else if (MODE == M_MATVEC) {
+                    static_cast<T*>(a.Y)[orow * kp + col] = q;
+                } else {
+                    const int64_t o = orow * kp + col;
+                    if (a.clamp) q = q > T(0) ? q : T(0);
+                    const T rh = a.rho ? static_cast<const T*>(a.rho)[orow] : T(1);
+                    const T bn = e_pre + rh * q;                                        // eq. (1)
+                    const double d = (double)bn - (double)b_pre;
+                    d2 = col < a.k ? d * d : 0.0;
+                    xn[o] = bn;
+                    static_cast<T*>(a.Q)[o] = q;
+                }
+            }
+            if (PHASE == 2 && MODE != M_MATVEC) {          // per-column partials, rows in fixed order
+                tile[t] = d2;
+                __syncthreads();
+                if (t < 16) {
+                    double sum = 0.0;
+                    for (int q2 = 0; q2 < 16; ++q2) sum += tile[q2 * 16 + t];
+                    sred[cur.ch * 16 + t] += sum;
+                }
+            }
+        }
+        __syncthreads();                                   // slot (step % kRS) free for step + kRS
+        advance(cur);
+    }
+    cpa_wait<0>();
+}
+
+template <typename T, int MODE>
+__global__ void __launch_bounds__(kThreads, 1) res_kernel(HotArgs a, ResArgs r) {
+    extern __shared__ __align__(16) unsigned char smraw[];
+    T* W = reinterpret_cast<T*>(smraw);
+    int32_t* S = reinterpret_cast<int32_t*>(W + r.wcap);
+    T* Xs = reinterpret_cast<T*>(S + r.scap);
+    double* sred = reinterpret_cast<double*>(Xs + kRS * kKS * 16);
+    double* tile = sred + a.kp;
+    double* red = tile + 256;                          // [8 warps][4 tiles][32 lanes][2] DMMA partials
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const unsigned nblk = gridDim.x;
+    {   // this CTA's F-hat values and source-row lists -> smem, once per launch
+        const int64_t w0 = r.cta_woff[blockIdx.x], w1 = r.cta_woff[blockIdx.x + 1];
+        constexpr int EPL = 16 / (int)sizeof(T);
+        const T* src = static_cast<const T*>(r.wblob) + w0;
+        for (int64_t e = (int64_t)threadIdx.x * EPL; e < w1 - w0; e += (int64_t)kThreads * EPL)
+            cpa<16>(W + e, src + e, 16);
+        const int64_t s0 = r.cta_soff[blockIdx.x], s1 = r.cta_soff[blockIdx.x + 1];
+        for (int64_t e = (int64_t)threadIdx.x * 4; e < s1 - s0; e += (int64_t)kThreads * 4)
+            cpa<16>(S + e, r.sblob + s0 + e, 16);
+        cpa_commit();
+        cpa_wait<0>();
+        __syncthreads();
+    }
+    const bool have_p1 = a.n_g1 > 0;
+    int cur = 0;
+    if (MODE == M_STEP) {
+        if (*(volatile int*)&a.ctl->done) return;
+        cur = *(volatile int*)&a.ctl->iter & 1;
+    }
+    for (int it = 0;; ++it) {
+        T* xc = static_cast<T*>(cur ? a.xt1 : a.xt0);
+        T* xn = static_cast<T*>(cur ? a.xt0 : a.xt1);
+        trace_ev(a, it, 0);
+        if (have_p1) res_phase<T, 1, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red);
+        trace_ev(a, it, 1);
+        if (MODE == M_MATVEC) {
+            if (have_p1) grid_sync(a.ctl, nblk);
+            trace_ev(a, it, 2);
+            res_phase<T, 2, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red);
+            trace_ev(a, it, 3);
+            return;
+        }
+        if (MODE == M_SOLVE || have_p1) grid_sync(a.ctl, nblk);        // B1
+        trace_ev(a, it, 2);
+        if (MODE == M_SOLVE && it > 0) {
+            const int bad = *(volatile int*)&a.ctl->bad[(it - 1) & 1];
+            if (!bad || it >= a.iters) {
+                if (blockIdx.x == 0 && threadIdx.x == 0) { a.ctl->iter = it; a.ctl->done = 1; }
+                return;
+            }
+        }
+        for (int c = threadIdx.x; c < a.kp; c += kThreads) sred[c] = 0.0;
+        __syncthreads();
+        res_phase<T, 2, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red);
+        __syncthreads();
+        double* part = a.partial + (MODE == M_STEP ? 0 : (int64_t)(it & 1) * nblk * a.kp);   // [kp][nblk]
+        for (int c = threadIdx.x; c < a.kp; c += kThreads) part[(int64_t)c * nblk + blockIdx.x] = sred[c];
+        if (MODE == M_STEP) return;
+        trace_ev(a, it, 3);
+        grid_sync(a.ctl, nblk);                                        // B2
+        trace_ev(a, it, 4);
+        for (int c = blockIdx.x + (int)nblk * warp; c < a.k; c += (int)nblk * kWarps) {
+            const double* pc = part + (int64_t)c * nblk;
+            double sum = 0.0;
+            for (unsigned b = lane; b < nblk; b += 32u) sum += __ldcg(pc + b);
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off);
+            if (lane == 0) {
+                const double en = a.enorm2[c];
+                const double rr = en > 0.0 ? sqrt(sum) / sqrt(en) : 0.0;
+                a.resid[c] = rr;
+                if (!(rr <= a.tol)) atomicOr(&a.ctl->bad[it & 1], 1);
+            }
+        }
+        if (blockIdx.x == 0 && threadIdx.x == 0) a.ctl->bad[(it + 1) & 1] = 0;
+        cur ^= 1;
+    }
+}
+
 // The persistent hot-path kernel (a2-a5).  MODE = M_MATVEC: phase 1, grid
 // barrier, phase 2 -> Y.  MODE = M_SOLVE: Jacobi iterations until every
 // column has r <= tol or `iters` is reached.  GROUPED selects the row-group
@@ -924,25 +1221,50 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm<GROUPED>()) hot_kernel(H
     }
 }
 
-// Column sums of squares of V (tree order, N x kp): one CTA per column block
-// of 1 column, fixed-order tree reduction -> out[c].
+// Column sums of squares of V (tree order, N x kp, row-major): ||E_c||^2 for
+// the stop rule.  Pass 1: CTA b sums rows [b R, (b+1) R) for every column
+// (threads = column x row-lane, coalesced rows), fixed order -> part[b][c];
+// pass 2: column c sums the CTAs' partials in CTA order.  Deterministic.
 template <typename T>
-__global__ void colnorm_kernel(const T* V, int64_t N, int kp, int k, double* out) {
-    const int c = blockIdx.x;
-    if (c >= k) return;
+__global__ void colnorm_partial_kernel(const T* V, int64_t N, int kp, int64_t rows_per_cta, double* part) {
     __shared__ double sh[kThreads];
-    double s = 0.0;
-    for (int64_t r = threadIdx.x; r < N; r += kThreads) {
-        const double v = (double)V[r * kp + c];
-        s += v * v;
-    }
-    sh[threadIdx.x] = s;
-    __syncthreads();
-    for (int off = kThreads / 2; off > 0; off >>= 1) {
-        if (threadIdx.x < off) sh[threadIdx.x] += sh[threadIdx.x + off];
+    const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta, r1 = r0 + rows_per_cta < N ? r0 + rows_per_cta : N;
+    for (int c0 = 0; c0 < kp; c0 += kThreads) {
+        const int lanes = min(kThreads, kp - c0);           // columns this pass
+        const int nl = kThreads / lanes;                     // row lanes
+        const int c = c0 + threadIdx.x % lanes, rl = threadIdx.x / lanes;
+        double s = 0.0;
+        if (rl < nl) {
+            int64_t r = r0 + rl;
+            double s1 = 0.0;
+            for (; r + nl < r1; r += 2 * nl) {
+                const double v0 = (double)V[r * kp + c], v1 = (double)V[(r + nl) * kp + c];
+                s += v0 * v0;
+                s1 += v1 * v1;
+            }
+            if (r < r1) { const double v0 = (double)V[r * kp + c]; s += v0 * v0; }
+            s += s1;
+        }
+        sh[threadIdx.x] = rl < nl ? s : 0.0;
+        __syncthreads();
+        if (threadIdx.x < lanes) {
+            double t = 0.0;
+            for (int q = 0; q < nl; ++q) t += sh[q * lanes + threadIdx.x];
+            part[(int64_t)blockIdx.x * kp + c0 + threadIdx.x] = t;
+        }
         __syncthreads();
     }
-    if (threadIdx.x == 0) out[c] = sh[0];
+}
+// pass 2: warp per column, lanes stride over the CTAs' partials, fixed xor tree
+__global__ void colnorm_final_kernel(const double* part, int nb, int kp, int k, double* out) {
+    const int lane = threadIdx.x & 31;
+    const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (c >= k) return;
+    double t = 0.0;
+    for (int b = lane; b < nb; b += 32) t += part[(int64_t)b * kp + c];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) t += __shfl_xor_sync(0xffffffffu, t, off);
+    if (lane == 0) out[c] = t;
 }
 
 // Caller order (column-major N x k, ld N) -> tree order (N x kp, row-major):
@@ -1167,6 +1489,14 @@ struct DeviceHMat {
     std::vector<int64_t> cost_p1, cost_p2, cost_g1, cost_g2;
     struct Sched { int32_t* ptr = nullptr; int32_t* items = nullptr; };
     std::map<std::array<int64_t, 4>, Sched> sched;
+    // resident batched layout (res_kernel); res_ok = false -> streaming path
+    bool res_ok = false;
+    int res_grid = 0, res_wcap = 0, res_scap = 0;
+    RGroup* r_groups = nullptr;
+    int32_t *r_outrow = nullptr, *r_sblob = nullptr;
+    void* r_wblob = nullptr;
+    int64_t *r_cta_woff = nullptr, *r_cta_soff = nullptr;
+    int32_t *r_p1_ptr = nullptr, *r_p1_list = nullptr, *r_p2_ptr = nullptr, *r_p2_list = nullptr;
     // ROWS mode (sharded handle): cut points and the allgather buffers
     int64_t* bounds = nullptr;
     int64_t row_lo = 0, row_hi = 0, rows_max = 0;
@@ -1476,6 +1806,132 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         if ((rc = up((void**)&D->bounds, h->row_bounds.data(), h->row_bounds.size() * 8))) return rc;
     }
     if ((rc = up((void**)&D->active, active.data(), active.size()))) return rc;
+
+    // ---- resident batched layout: groups -> CTAs (one per SM), each CTA's
+    // F-hat values ([K][16] weight blocks over the union of its groups'
+    // sources) and source-row lists packed for its shared memory.
+    {
+        int nsm = 148, smem_optin = 0;
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, D->device);
+        cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, D->device);
+        constexpr int EPL = 16 / (int)sizeof(T);
+        struct HG { int phase; int64_t g; int64_t K; std::vector<int32_t> ucols; };
+        std::vector<HG> hg;
+        for (int64_t g = 0; g < (int64_t)g1v.size(); ++g) hg.push_back({1, g, gsegv[g1v[g].seg_off].len, {}});
+        for (int64_t g = 0; g < (int64_t)g2v.size(); ++g) {
+            HG x{2, g, 0, {}};
+            for (int q = 0; q < g2v[g].nseg; ++q) x.K += gsegv[g2v[g].seg_off + q].len;
+            for (int r = 0; r < g2v[g].nrows; ++r) {
+                const int64_t cs = gcsr2v[g * kGroup + r];
+                if (cs >= 0)
+                    for (int32_t e = 0; e < segs[cs].len; ++e) x.ucols.push_back(idx[segs[cs].src + e]);
+            }
+            std::sort(x.ucols.begin(), x.ucols.end());
+            x.ucols.erase(std::unique(x.ucols.begin(), x.ucols.end()), x.ucols.end());
+            x.K += (int64_t)x.ucols.size();
+            hg.push_back(std::move(x));
+        }
+        const int64_t fixed = (int64_t)kRS * kKS * 16 * (int64_t)sizeof(T) + 256 * 8 + (int64_t)kMaxKp * 8 + 256 +
+                              (int64_t)kWarps * 4 * 32 * 2 * 8;
+        const int64_t budget = smem_optin - fixed;                 // bytes for values + source rows
+        auto need = [&](const HG& x) { return (x.K * kGroup + EPL) * (int64_t)sizeof(T) + (x.K + 4) * 4; };
+        bool ok = budget > 0 && !hg.empty();
+        std::vector<int> owner(hg.size(), -1);
+        std::vector<int64_t> used(nsm, 0), load1(nsm, 0), load2(nsm, 0);
+        if (ok) {
+            std::vector<size_t> ord(hg.size());
+            std::iota(ord.begin(), ord.end(), 0);
+            std::stable_sort(ord.begin(), ord.end(), [&](size_t x, size_t y) { return hg[x].K > hg[y].K; });
+            for (size_t q : ord) {
+                const int64_t nb = need(hg[q]);
+                std::vector<int64_t>& ld = hg[q].phase == 1 ? load1 : load2;
+                int best = -1;
+                for (int c = 0; c < nsm; ++c)
+                    if (used[c] + nb <= budget && (best < 0 || ld[c] < ld[best])) best = c;
+                if (best < 0) { ok = false; break; }
+                owner[q] = best;
+                used[best] += nb;
+                ld[best] += hg[q].K * (int64_t)(kGroup + 1) + 256;   // slice time ~ K
+            }
+        }
+        if (ok) {
+            std::vector<RGroup> rg;
+            std::vector<int32_t> outrow, sblob, p1_ptr(nsm + 1, 0), p1_list, p2_ptr(nsm + 1, 0), p2_list;
+            std::vector<T> blob;
+            std::vector<int64_t> cta_woff(nsm + 1, 0), cta_soff(nsm + 1, 0);
+            int64_t wmax = 0, smax = 0;
+            for (int c = 0; c < nsm; ++c) {
+                cta_woff[c] = (int64_t)blob.size();
+                cta_soff[c] = (int64_t)sblob.size();
+                const int64_t wbase = (int64_t)blob.size(), sbase = (int64_t)sblob.size();
+                for (int ph = 1; ph <= 2; ++ph) {
+                    for (size_t q = 0; q < hg.size(); ++q) {
+                        if (owner[q] != c || hg[q].phase != ph) continue;
+                        const Group& G = ph == 1 ? g1v[hg[q].g] : g2v[hg[q].g];
+                        const int64_t g = hg[q].g;
+                        RGroup R{};
+                        R.nrows = G.nrows;
+                        R.K = (int32_t)hg[q].K;
+                        R.w_off = (int32_t)((int64_t)blob.size() - wbase);
+                        R.s_off = (int32_t)((int64_t)sblob.size() - sbase);
+                        blob.resize(blob.size() + (size_t)hg[q].K * kGroup, T(0));
+                        T* Wg = blob.data() + wbase + R.w_off;
+                        int64_t j0 = 0;
+                        for (int sgi = 0; sgi < G.nseg; ++sgi) {
+                            const GSeg& sg = gsegv[G.seg_off + sgi];
+                            for (int64_t e = 0; e < sg.len; ++e) {
+                                sblob.push_back((int32_t)(sg.kind ? idx[sg.src + e] : sg.src + e));
+                                for (int r = 0; r < G.nrows; ++r)
+                                    Wg[(j0 + e) * kGroup + r] = vals[gvov[(G.seg_off + sgi) * kGroup + r] + e];
+                            }
+                            j0 += sg.len;
+                        }
+                        const std::vector<int32_t>& U = hg[q].ucols;
+                        for (int32_t col : U) sblob.push_back(col);
+                        for (int r = 0; ph == 2 && r < G.nrows; ++r) {
+                            const int64_t cs = gcsr2v[g * kGroup + r];
+                            if (cs < 0) continue;
+                            for (int32_t e = 0; e < segs[cs].len; ++e) {
+                                const int32_t col = idx[segs[cs].src + e];
+                                const int64_t pos = std::lower_bound(U.begin(), U.end(), col) - U.begin();
+                                Wg[(j0 + pos) * kGroup + r] = vals[segs[cs].val_off + e];
+                            }
+                        }
+                        R.out_off = (int64_t)outrow.size();
+                        for (int r = 0; r < kGroup; ++r)
+                            outrow.push_back(r < G.nrows ? (ph == 1 ? grow1v[g * kGroup + r] : grow2v[g * kGroup + r]) : 0);
+                        (ph == 1 ? p1_list : p2_list).push_back((int32_t)rg.size());
+                        rg.push_back(R);
+                    }
+                    (ph == 1 ? p1_ptr : p2_ptr)[c + 1] = (int32_t)(ph == 1 ? p1_list : p2_list).size();
+                }
+                while (blob.size() % EPL) blob.push_back(T(0));
+                while (sblob.size() % 4) sblob.push_back(0);
+                wmax = std::max(wmax, (int64_t)blob.size() - wbase);
+                smax = std::max(smax, (int64_t)sblob.size() - sbase);
+            }
+            cta_woff[nsm] = (int64_t)blob.size();
+            cta_soff[nsm] = (int64_t)sblob.size();
+            if (sblob.empty()) sblob.resize(4, 0);
+            if (p1_list.empty()) p1_list.push_back(0);
+            if (p2_list.empty()) p2_list.push_back(0);
+            if ((rc = up((void**)&D->r_groups, rg.data(), rg.size() * sizeof(RGroup))) ||
+                (rc = up((void**)&D->r_outrow, outrow.data(), outrow.size() * 4)) ||
+                (rc = up(&D->r_wblob, blob.data(), blob.size() * sizeof(T))) ||
+                (rc = up((void**)&D->r_cta_woff, cta_woff.data(), cta_woff.size() * 8)) ||
+                (rc = up((void**)&D->r_sblob, sblob.data(), sblob.size() * 4)) ||
+                (rc = up((void**)&D->r_cta_soff, cta_soff.data(), cta_soff.size() * 8)) ||
+                (rc = up((void**)&D->r_p1_ptr, p1_ptr.data(), p1_ptr.size() * 4)) ||
+                (rc = up((void**)&D->r_p1_list, p1_list.data(), p1_list.size() * 4)) ||
+                (rc = up((void**)&D->r_p2_ptr, p2_ptr.data(), p2_ptr.size() * 4)) ||
+                (rc = up((void**)&D->r_p2_list, p2_list.data(), p2_list.size() * 4)))
+                return rc;
+            D->res_ok = !getenv("VF_NO_RESIDENT");
+            D->res_grid = nsm;
+            D->res_wcap = (int)std::max<int64_t>(wmax, EPL);
+            D->res_scap = (int)std::max<int64_t>(smax, 4);
+        }
+    }
     CK(cudaMalloc((void**)&D->ctl, sizeof(Ctl)));
     CK(cudaMallocHost((void**)&D->ctl_host, sizeof(Ctl)));
     D->evpool.resize(2048);
@@ -1633,8 +2089,11 @@ void launch_permute_out(Handle* h, const void* src, int k, int kp, bool use_acti
 template <typename T>
 void launch_colnorm(Handle* h, const void* V, int k, int kp, cudaStream_t st) {
     DeviceHMat* D = h->dev;
-    colnorm_kernel<T><<<k, kThreads, 0, st>>>((const T*)V, D->N, kp, k, D->enorm2);
-    h->launches_total++;
+    const int64_t rows = std::max<int64_t>(8, (D->N + 591) / 592);
+    const int nb = (int)((D->N + rows - 1) / rows);      // <= 592 partial rows: fit D->partial
+    colnorm_partial_kernel<T><<<nb, kThreads, 0, st>>>((const T*)V, D->N, kp, rows, D->partial);
+    colnorm_final_kernel<<<(k * 32 + 255) / 256, 256, 0, st>>>(D->partial, nb, kp, k, D->enorm2);
+    h->launches_total += 2;
 }
 
 // Longest-processing-time-first static schedule of nunits x nchunk items
@@ -1736,9 +2195,60 @@ int launch_hot_t(Handle* h, HotArgs& a, cudaStream_t st) {
     return VF_OK;
 }
 
+// Cooperative launch of the resident batched kernel (one CTA per SM).
+template <typename T, int MODE>
+int launch_res(Handle* h, HotArgs& a, cudaStream_t st) {
+    DeviceHMat* D = h->dev;
+    auto fn = res_kernel<T, MODE>;
+    const size_t smem = (size_t)D->res_wcap * sizeof(T) + (size_t)D->res_scap * 4 + (size_t)kRS * kKS * 16 * sizeof(T) +
+                        (size_t)a.kp * 8 + 256 * 8 + (size_t)kWarps * 4 * 32 * 2 * 8;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
+    if (per_sm < 1) return set_error(VF_ECUDA, "resident kernel cannot be resident");
+    ResArgs r{D->r_groups, D->r_outrow, D->r_wblob, D->r_cta_woff, D->r_sblob, D->r_cta_soff,
+              D->r_p1_ptr, D->r_p1_list, D->r_p2_ptr, D->r_p2_list, D->res_wcap, D->res_scap};
+    const int grid = D->res_grid;
+    static const char* trace_file = getenv("VF_TRACE_FILE");
+    unsigned long long* tbuf = nullptr;
+    const int tit = 64;
+    if (trace_file && MODE != M_STEP) {
+        CK(cudaMalloc(&tbuf, (size_t)tit * 5 * grid * 8));
+        CK(cudaMemsetAsync(tbuf, 0, (size_t)tit * 5 * grid * 8, st));
+        a.trace = tbuf;
+        a.trace_iters = tit;
+    }
+    void* args[] = {&a, &r};
+    if (MODE != M_STEP) CK(cudaMemsetAsync(a.ctl, 0, offsetof(Ctl, bar_gen), st));
+    {
+        Timer tm(h, st, 2);
+        CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kThreads), args, smem, st));
+    }
+    h->launches_total++;
+    D->last_grid = grid;
+    if (tbuf) {
+        std::vector<unsigned long long> hb((size_t)tit * 5 * grid);
+        CK(cudaMemcpyAsync(hb.data(), tbuf, hb.size() * 8, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        cudaFree(tbuf);
+        a.trace = nullptr;
+        if (FILE* f = fopen(trace_file, "ab")) {
+            int32_t hdr[4] = {grid, tit, (int32_t)a.kp, 2};
+            fwrite(hdr, 4, 4, f);
+            fwrite(hb.data(), 8, hb.size(), f);
+            fclose(f);
+        }
+    }
+    return VF_OK;
+}
+
 template <typename T, int MODE>
 int launch_hot(Handle* h, HotArgs& a, cudaStream_t st) {
     const int kp = a.kp;
+    if (kp >= 16 && kp % 16 == 0 && h->dev->res_ok &&
+        (size_t)h->dev->res_wcap * sizeof(T) + (size_t)h->dev->res_scap * 4 + (size_t)kRS * kKS * 16 * sizeof(T) +
+                (size_t)kp * 8 + 2048 + (size_t)kWarps * 4 * 32 * 2 * 8 <= (size_t)232448)
+        return launch_res<T, MODE>(h, a, st);
     if (kp == 1) return launch_hot_t<T, 1, 1, MODE, false>(h, a, st);
     if (kp == 2) return launch_hot_t<T, 1, 2, MODE, false>(h, a, st);
     if (kp == 4) return launch_hot_t<T, 1, 2, MODE, true>(h, a, st);
@@ -2025,7 +2535,8 @@ void device_free(Handle* h) {
     DeviceHMat* D = h->dev;
     if (!D) return;
     cudaSetDevice(h->device);
-    void* ptrs[] = {D->bounds, D->send, D->recv, D->vals, D->idx, D->segs, D->p1_segptr, D->p1_rows, D->p1_scale, D->p2_segptr, D->p2_rows,
+    void* ptrs[] = {D->r_groups, D->r_outrow, D->r_wblob, D->r_cta_woff, D->r_sblob, D->r_cta_soff,
+                    D->r_p1_ptr, D->r_p1_list, D->r_p2_ptr, D->r_p2_list, D->bounds, D->send, D->recv, D->vals, D->idx, D->segs, D->p1_segptr, D->p1_rows, D->p1_scale, D->p2_segptr, D->p2_rows,
                     D->perm, D->active, D->g1, D->g2, D->gseg, D->gvo, D->grow1, D->grow2, D->gcsr1, D->gcsr2,
                     D->xt[0], D->xt[1], D->Ep, D->Qp, D->Qdp, D->Qvp, D->Yp, D->Qip,
                     D->pv[0], D->pv[1], D->pv[2], D->partial, D->enorm2, D->resid, D->ctl,
@@ -2061,7 +2572,8 @@ int64_t device_alg_flops(const Handle* h) { return h->dev ? h->dev->alg_flops_pe
 int64_t device_active_rows(const Handle* h) { return h->dev ? h->dev->n_p2 : -1; }
 void device_phase_info(const Handle* h, int64_t* out9) {
     const DeviceHMat* D = h->dev;
-    if (!D) { for (int i = 0; i < 9; ++i) out9[i] = 0; return; }
+    if (!D) { for (int i = 0; i < 10; ++i) out9[i] = 0; return; }
+    out9[9] = D->res_ok ? 1 : 0;
     out9[0] = D->NT; out9[1] = D->p1_bytes; out9[2] = D->p2_bytes; out9[3] = D->p1_src; out9[4] = D->p2_src;
     out9[5] = D->p1_flops; out9[6] = D->p2_flops; out9[7] = D->n_g1; out9[8] = D->n_g2;
 }

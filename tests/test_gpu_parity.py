@@ -298,3 +298,44 @@ def test_device_evaluator_equals_host_evaluator_bitwise(mesh, tmp_path):
         M.save(p)
         paths.append(p)
     assert open(paths[0], "rb").read() == open(paths[1], "rb").read()
+
+
+@pytest.fixture(scope="module")
+def cfg2_small():
+    V, F = sg.cfg2_mesh(n_side=40)               # the configs[1] scene at ~3k facets
+    S = oracle.Scene(V, F)
+    return V, F, S, S.F_dense()
+
+
+@pytest.mark.parametrize("k", [16, 64, 130])
+def test_resident_and_streaming_batched_paths(cfg2_small, rough, tmp_path_factory, k, monkeypatch):
+    """nrhs >= 9 runs the shared-memory-resident kernel (res_kernel) when the
+    layout fits; VF_NO_RESIDENT forces the streaming grouped kernel.  Both must
+    match the oracle's Alg. 5 on the same blocks (matvec) and its Jacobi solve
+    (identical iteration counts)."""
+    for which in ("cfg2", "rough"):
+        V, F, S, Fd = cfg2_small if which == "cfg2" else rough
+        H = hm.compress(S.x, Fd, 1e-6, min_size=2048)
+        p = str(tmp_path_factory.mktemp("res") / f"{which}{k}.hvfm")
+        hm.write_hvfm(H, p)
+        X = sg.random_rhs(S.N, k, seed=5)
+        Yref = hm.hmatvec(H, X)
+        rng = np.random.default_rng(3)
+        E = np.asfortranarray(100 * rng.random((S.N, k)))
+        rho = np.full(S.N, 0.5 / max(1.0, np.abs(Fd).sum(1).max()))
+        B0, _, it0, _ = oracle.jacobi(lambda Z: hm.hmatvec(H, Z), E, rho, 1e-13, 200)
+        for resident in (True, False):
+            if resident:
+                monkeypatch.delenv("VF_NO_RESIDENT", raising=False)
+            else:
+                monkeypatch.setenv("VF_NO_RESIDENT", "1")
+            M = vf.ViewFactorMatrix.load(p, device=0)
+            if which == "cfg2" or not resident:
+                assert bool(M.refresh()["resident"]) == resident
+            Y = empty(S.N, k)
+            M.matvec(dev(X), Y)
+            assert rel(host(Y), Yref) <= 1e-12
+            B = empty(S.N, k)
+            M.solve_radiosity(dev(E), dev(rho), B, iters=200, tol=1e-13)
+            assert M.stats()["iters1"] == it0
+            assert rel(host(B), B0) <= 1e-12
