@@ -844,6 +844,8 @@ struct RGroup {
     int32_t w_off;     // [K][16] weights at this element offset of the CTA's smem blob
     int32_t s_off;     // K source XT rows at this int offset of the CTA's smem index area
     int64_t out_off;   // 16 output rows (tree rows or T rows) at outrow[out_off ..]
+    int32_t ch0, chstep;  // 16-column chunks ch0, ch0 + chstep, ... of this copy (phase-1
+                          // groups are replicated over CTAs, each copy taking every chstep-th chunk)
 };
 struct ResArgs {
     const RGroup* groups;
@@ -898,19 +900,31 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
     const int64_t kp = a.kp;
     // steps = (group, 16-column chunk, K slice) in order
     int total = 0;
-    for (int g = g0; g < g1; ++g) total += nchunk * ((r.groups[lst[g]].K + kKS - 1) / kKS);
+    for (int g = g0; g < g1; ++g) {
+        const RGroup& Gq = r.groups[lst[g]];
+        const int nch_g = Gq.ch0 < nchunk ? (nchunk - Gq.ch0 + Gq.chstep - 1) / Gq.chstep : 0;
+        total += nch_g * ((Gq.K + kKS - 1) / kKS);
+    }
+    if (total == 0) return;
+    // first group with a chunk of its own (a copy may own none for small kp)
+    int gs = g0;
+    while (r.groups[lst[gs]].ch0 >= nchunk) ++gs;
     auto advance = [&](ResCursor& c) {
         if (++c.sl * kKS < c.G.K) return;
         c.sl = 0;
-        if (++c.ch < nchunk) return;
-        c.ch = 0;
-        if (++c.g < g1) c.G = r.groups[lst[c.g]];
+        c.ch += c.G.chstep;
+        if (c.ch < nchunk) return;
+        while (++c.g < g1) {
+            c.G = r.groups[lst[c.g]];
+            c.ch = c.G.ch0;
+            if (c.ch < nchunk) return;
+        }
     };
     auto stage = [&](const ResCursor& c, T* dst) {
         const int j0 = c.sl * kKS;
         res_stage<T>(S + c.G.s_off, j0, min(kKS, c.G.K - j0), xc, kp, c.ch * 16, dst);
     };
-    ResCursor cur{g0, 0, 0, r.groups[lst[g0]]};
+    ResCursor cur{gs, r.groups[lst[gs]].ch0, 0, r.groups[lst[gs]]};
     ResCursor nxt = cur;
 #pragma unroll
     for (int p = 0; p < kRS - 1; ++p) {                // prologue: kRS - 1 slices in flight
@@ -1815,11 +1829,15 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, D->device);
         cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, D->device);
         constexpr int EPL = 16 / (int)sizeof(T);
-        struct HG { int phase; int64_t g; int64_t K; std::vector<int32_t> ucols; };
+        struct HG { int phase; int64_t g; int64_t K; std::vector<int32_t> ucols; int ch0 = 0, chstep = 1; };
         std::vector<HG> hg;
-        for (int64_t g = 0; g < (int64_t)g1v.size(); ++g) hg.push_back({1, g, gsegv[g1v[g].seg_off].len, {}});
+        // phase-1 groups are few and short: each is replicated kP1Copies times so
+        // that its column chunks run on different SMs (copy i takes chunks i, i + kP1Copies, ...)
+        const int kP1Copies = 4;
+        for (int64_t g = 0; g < (int64_t)g1v.size(); ++g)
+            for (int cpy = 0; cpy < kP1Copies; ++cpy) hg.push_back({1, g, gsegv[g1v[g].seg_off].len, {}, cpy, kP1Copies});
         for (int64_t g = 0; g < (int64_t)g2v.size(); ++g) {
-            HG x{2, g, 0, {}};
+            HG x{2, g, 0, {}, 0, 1};
             for (int q = 0; q < g2v[g].nseg; ++q) x.K += gsegv[g2v[g].seg_off + q].len;
             for (int r = 0; r < g2v[g].nrows; ++r) {
                 const int64_t cs = gcsr2v[g * kGroup + r];
@@ -1851,7 +1869,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                 if (best < 0) { ok = false; break; }
                 owner[q] = best;
                 used[best] += nb;
-                ld[best] += hg[q].K * (int64_t)(kGroup + 1) + 256;   // slice time ~ K
+                ld[best] += hg[q].K * (int64_t)(kGroup + 1) / hg[q].chstep + 256;   // time ~ K x chunks taken
             }
         }
         if (ok) {
@@ -1872,6 +1890,8 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                         RGroup R{};
                         R.nrows = G.nrows;
                         R.K = (int32_t)hg[q].K;
+                        R.ch0 = hg[q].ch0;
+                        R.chstep = hg[q].chstep;
                         R.w_off = (int32_t)((int64_t)blob.size() - wbase);
                         R.s_off = (int32_t)((int64_t)sblob.size() - sbase);
                         blob.resize(blob.size() + (size_t)hg[q].K * kGroup, T(0));
