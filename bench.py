@@ -333,7 +333,8 @@ def run_gpu(args, rank, world, local_rank):
         peak_tf = fp64_peak_tflops(smax) if dt == "f64" else fp32_peak_tflops(smax)
         ach_tf = flops_launch / (avg * 1e-3) / 1e12 if avg > 0 else 0.0
         ach_gbs = bytes_launch / (avg * 1e-3) / 1e9 if avg > 0 else 0.0
-        roof = {"bound": "alu", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
+        dmma = bool(info.get("resident")) and dt == "f64"     # res_kernel contracts on FP64 tensor cores (DMMA)
+        roof = {"bound": "tensor" if dmma else "alu", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": ach_tf / peak_tf if peak_tf else None, "traffic": None,
                 "kernel": (f"res_kernel<{'double' if dt == 'f64' else 'float'},M_SOLVE> (persistent Jacobi solve, "
                            "F-hat resident in shared memory: phase 1 V^T X, grid barrier, phase 2 row-owner "
@@ -342,8 +343,9 @@ def run_gpu(args, rank, world, local_rank):
                            f"hot_kernel<{'double' if dt == 'f64' else 'float'},1,8,M_SOLVE,grouped> (persistent "
                            "Jacobi solve: phase 1 V^T X, grid barrier, phase 2 row-owner accumulate + fused "
                            "epilogue, residual decision; one launch per thermal stage)"),
-                "peak_basis": f"derived: 148 SM x {64 if dt == 'f64' else 128} {dt.upper()} FMA/clk x 2 x "
-                              f"{smax:.0f} MHz (sm_max of {pk_kind} MEASURED_PEAKS.json); DESIGN.md §Roofline",
+                "peak_basis": (("derived FP64 DMMA peak (= the DFMA rate on B200): " if dmma else "derived: ")
+                               + f"148 SM x {64 if dt == 'f64' else 128} {dt.upper()} FMA/clk x 2 x "
+                               f"{smax:.0f} MHz (sm_max of {pk_kind} MEASURED_PEAKS.json); DESIGN.md §7"),
                 "avg_launch_ms": avg, "launches": l2, "applies_per_launch": n_iters / max(l2, 1),
                 "flops_per_apply": flops_iter, "flops_per_launch": flops_launch,
                 "alg_bytes_per_apply": bytes_iter, "alg_bytes_per_launch": bytes_launch,
