@@ -338,7 +338,8 @@ template <bool L1X> struct XV4<float, L1X> {
 template <typename T, bool L1X>
 __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int64_t s0, int64_t s1,
                                                const T* __restrict__ vals, const int32_t* __restrict__ idx,
-                                               const T* xt, int lane, int64_t nx) {
+                                               const T* xt, int lane, int64_t nx,
+                                               const int32_t* tready = nullptr, const int32_t* seg_blk = nullptr) {
     constexpr int CH = VF_K1_CH;                 // chunks of 4 terms in flight per lane
     constexpr unsigned FULL = 0xffffffffu;
     T acc0 = T(0), acc1 = T(0);
@@ -346,6 +347,14 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
         const int ns = (int)(s1 - sb < 32 ? s1 - sb : 32);
         Seg my{0, 0, 0, 0};
         if (lane < ns) my = segs[sb + lane];
+        if (tready && lane < ns) {                   // barrier-free matvec: this lane's U run needs block b's T rows
+            const int32_t b = __ldg(seg_blk + sb + lane);
+            if (b >= 0) {
+                while (*(volatile int32_t*)(tready + b) < my.len) __nanosleep(64);
+                __threadfence();
+            }
+        }
+        __syncwarp();
         const int nch = (my.len + 3) >> 2;
         int incl = nch;
 #pragma unroll
@@ -495,6 +504,14 @@ struct HotArgs {
     const int32_t* s1_items;
     const int32_t* s2_ptr;
     const int32_t* s2_items;
+    // nrhs = 1 matvec without the phase barrier: per-SVD-block counters of
+    // finished T rows, the SVD block of every segment (-1: X source) and of every
+    // phase-1 group, and a dynamic queue over the phase-2 rows (LPT order)
+    int32_t* tready;
+    const int32_t* seg_blk;
+    const int32_t* g1_blk;
+    int32_t* qctr;
+    const int32_t* p2_order;
     unsigned long long* trace;    // optional: [iter][event][cta] globaltimer (VF_TRACE_FILE)
     int trace_iters;
 };
@@ -573,6 +590,11 @@ __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_
             const int64_t t = a.grow1[gi * kGroup + lane];
             xc[a.N + t] = static_cast<const T*>(a.p1_scale)[t] * mine;
         }
+        if (a.tready) {                               // publish: these T rows of block b are final
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(a.tready + a.g1_blk[gi], G.nrows);
+        }
     }
 }
 
@@ -611,6 +633,24 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
     const int g = lane / KC, c = lane % KC;
     const int nchunk = (a.kp + CW - 1) / CW;
     const T* vals = static_cast<const T*>(a.vals);
+    if (KC == 1 && VEC == 1 && MODE == M_MATVEC && a.qctr) {
+        // nrhs = 1 matvec: rows from a global queue in LPT order (dynamic
+        // balance; each row is still summed by one warp in a fixed order);
+        // the next ticket is fetched while the current row streams
+        int nxt = 0;
+        if (lane == 0) nxt = atomicAdd(a.qctr, 1);
+        nxt = __shfl_sync(0xffffffffu, nxt, 0);
+        while (nxt < a.n_p2) {
+            const int64_t r = a.p2_order[nxt];
+            int fut = 0;
+            if (lane == 0) fut = atomicAdd(a.qctr, 1);
+            const T acc = row_accumulate_k1<T, VF_MV_L1 != 0>(a.segs, a.p2_segptr[r], a.p2_segptr[r + 1], vals, a.idx,
+                                                              xc, lane, a.N, a.tready, a.seg_blk);
+            if (lane == 0) static_cast<T*>(a.Y)[a.p2_rows[r]] = acc;
+            nxt = __shfl_sync(0xffffffffu, fut, 0);
+        }
+        return;
+    }
     for (int32_t q = a.s2_ptr[gwarp]; q < a.s2_ptr[gwarp + 1]; ++q) {
         const int64_t item = a.s2_items[q];
         const int64_t r = item / nchunk;
@@ -1083,7 +1123,7 @@ __global__ void __launch_bounds__(kThreads, 1) res_kernel(HotArgs a, ResArgs r) 
         if (have_p1) res_phase<T, 1, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red);
         trace_ev(a, it, 1);
         if (MODE == M_MATVEC) {
-            if (have_p1) grid_sync(a.ctl, nblk);
+            if (have_p1 && !a.tready) grid_sync(a.ctl, nblk);   // nrhs = 1: per-block T flags instead
             trace_ev(a, it, 2);
             res_phase<T, 2, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red);
             trace_ev(a, it, 3);
@@ -1179,7 +1219,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm<GROUPED>()) hot_kernel(H
         }
         trace_ev(a, it, 1);
         if (MODE == M_MATVEC) {
-            if (have_p1) grid_sync(a.ctl, nblk);
+            if (have_p1 && !a.tready) grid_sync(a.ctl, nblk);   // nrhs = 1: per-block T flags instead
             trace_ev(a, it, 2);
             if constexpr (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sred, stage);
             else phase2_rows<T, KC, VEC, MODE>(a, xc, xn, gwarp, nwarp, lane, sred);
@@ -1503,6 +1543,9 @@ struct DeviceHMat {
     std::vector<int64_t> cost_p1, cost_p2, cost_g1, cost_g2;
     struct Sched { int32_t* ptr = nullptr; int32_t* items = nullptr; };
     std::map<std::array<int64_t, 4>, Sched> sched;
+    // barrier-free nrhs = 1 matvec (tready[n_svd] = the dynamic queue counter)
+    int32_t *tready = nullptr, *seg_blk = nullptr, *g1_blk = nullptr, *p2_order = nullptr;
+    int64_t n_svd = 0;
     // resident batched layout (res_kernel); res_ok = false -> streaming path
     bool res_ok = false;
     int res_grid = 0, res_wcap = 0, res_scap = 0;
@@ -1692,10 +1735,20 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     std::vector<int64_t> gvov, gcsr1v, gcsr2v;
     std::vector<int32_t> grow1v, grow2v;
     auto same_src = [](const Seg& x, const Seg& y) { return x.kind == y.kind && x.src == y.src && x.len == y.len; };
+    // SVD block (index in svd_ids order) of every T row and of every U segment
+    std::vector<int32_t> t_blk(std::max<int64_t>(NT, 1), -1), g1_blk;
+    for (size_t bi = 0; bi < svd_ids.size(); ++bi)
+        for (int64_t l = 0; l < h->leaves[svd_ids[bi]].q; ++l) t_blk[toff[svd_ids[bi]] + l] = (int32_t)bi;
+    std::vector<int32_t> seg_blk(segs.size(), -1);
+    for (size_t q = 0; q < segs.size(); ++q)
+        if (segs[q].kind == 0 && segs[q].src >= N) seg_blk[q] = t_blk[segs[q].src - N];
     for (int64_t r = 0; r < (int64_t)p1_rows.size();) {
         const Seg& s0 = segs[p1_segptr[r]];
         int64_t e = r + 1;
-        while (e < (int64_t)p1_rows.size() && e - r < kGroup && same_src(segs[p1_segptr[e]], s0)) ++e;
+        while (e < (int64_t)p1_rows.size() && e - r < kGroup && same_src(segs[p1_segptr[e]], s0) &&
+               t_blk[p1_rows[e]] == t_blk[p1_rows[r]])
+            ++e;
+        g1_blk.push_back(t_blk[p1_rows[r]]);
         Group G{(int32_t)(e - r), 1, (int64_t)gsegv.size()};
         gsegv.push_back(GSeg{s0.src, s0.len, s0.kind});
         for (int q = 0; q < kGroup; ++q) {
@@ -1820,6 +1873,19 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         if ((rc = up((void**)&D->bounds, h->row_bounds.data(), h->row_bounds.size() * 8))) return rc;
     }
     if ((rc = up((void**)&D->active, active.data(), active.size()))) return rc;
+    {   // barrier-free nrhs = 1 matvec: block flags, segment/group blocks, LPT row order
+        if (g1_blk.empty()) g1_blk.push_back(0);
+        std::vector<int32_t> order(D->cost_p2.size());
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return D->cost_p2[x] > D->cost_p2[y]; });
+        if (order.empty()) order.push_back(0);
+        D->n_svd = (int64_t)svd_ids.size();
+        if ((rc = up((void**)&D->seg_blk, seg_blk.data(), seg_blk.size() * 4)) ||
+            (rc = up((void**)&D->g1_blk, g1_blk.data(), g1_blk.size() * 4)) ||
+            (rc = up((void**)&D->p2_order, order.data(), order.size() * 4)) ||
+            (rc = up((void**)&D->tready, nullptr, (size_t)std::max<int64_t>(D->n_svd + 1, 2) * 4)))
+            return rc;
+    }
 
     // ---- resident batched layout: groups -> CTAs (one per SM), each CTA's
     // F-hat values ([K][16] weight blocks over the union of its groups'
@@ -2426,6 +2492,11 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     launch_permute_in<T>(h, Xd, nrhs, kp, nullptr, D->xt[0], nullptr, nullptr, nullptr, st);
     HotArgs a = hot_args(D, kp, nrhs);
     a.Y = D->Yp;
+    if (kp == 1 && !getenv("VF_MV_BARRIER")) {          // phase-1 -> phase-2 by per-block flags, dynamic rows
+        CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
+        a.tready = D->tready; a.seg_blk = D->seg_blk; a.g1_blk = D->g1_blk;
+        a.qctr = D->tready + D->n_svd; a.p2_order = D->p2_order;
+    }
     const bool rows = D->world > 1 || h->comm;
     if (rows) CK(cudaMemsetAsync(D->Yp, 0, (size_t)D->N * kp * sizeof(T), st));   // rows of other ranks: 0 ...
     if ((rc = launch_hot<T, M_MATVEC>(h, a, st))) return rc;
@@ -2555,7 +2626,7 @@ void device_free(Handle* h) {
     DeviceHMat* D = h->dev;
     if (!D) return;
     cudaSetDevice(h->device);
-    void* ptrs[] = {D->r_groups, D->r_outrow, D->r_wblob, D->r_cta_woff, D->r_sblob, D->r_cta_soff,
+    void* ptrs[] = {D->tready, D->seg_blk, D->g1_blk, D->p2_order, D->r_groups, D->r_outrow, D->r_wblob, D->r_cta_woff, D->r_sblob, D->r_cta_soff,
                     D->r_p1_ptr, D->r_p1_list, D->r_p2_ptr, D->r_p2_list, D->bounds, D->send, D->recv, D->vals, D->idx, D->segs, D->p1_segptr, D->p1_rows, D->p1_scale, D->p2_segptr, D->p2_rows,
                     D->perm, D->active, D->g1, D->g2, D->gseg, D->gvo, D->grow1, D->grow2, D->gcsr1, D->gcsr2,
                     D->xt[0], D->xt[1], D->Ep, D->Qp, D->Qdp, D->Qvp, D->Yp, D->Qip,

@@ -165,3 +165,27 @@ def test_flat_plane_is_empty():
     M = vf.ViewFactorMatrix.build(*sg.flat_plane_mesh(10), 1e-5, device=-1)
     i = M.info
     assert i["n_dense"] + i["n_csr"] + i["n_svd"] == 0 and i["active_rows"] == 0
+
+
+def test_set_mesh_gives_loaded_handles_insolation(tmp_path):
+    """vf_set_mesh attaches the geometry of a saved F-hat so vf_insolation
+     works on a loaded handle and equals the built handle's."""
+    V, F = sg.rough_small_mesh(10)
+    M = vf.ViewFactorMatrix.build(V, F, 1e-5, device=-1)
+    p = str(tmp_path / "m.hvfm")
+    M.save(p)
+    L = vf.ViewFactorMatrix.load(p, device=-1)
+    suns = sg.sun_dirs(20.0, 3)
+    with pytest.raises(vf.VFError):
+        L.insolation(suns)
+    vf.vf_set_mesh(L.h, V, F)
+    np.testing.assert_array_equal(L.insolation(suns), M.insolation(suns))
+    with pytest.raises(vf.VFError):
+        vf.vf_set_mesh(L.h, V, F[:-1])
+
+
+def test_device_evaluator_needs_a_device():
+    V, F = sg.rough_small_mesh(6)
+    with pytest.raises(vf.VFError) as e:
+        vf.vf_build(V, F, 1e-5, device=-1, evaluator=vf.VF_EVAL_DEVICE)
+    assert e.value.code == vf.VF_EINVAL

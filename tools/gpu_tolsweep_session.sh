@@ -6,6 +6,6 @@ O=gpurun_out/${TAG:-tolsweep}
 mkdir -p $O
 for tol in ${TOLS:-1e-3 1e-7}; do
   timeout 2400 python tools/build_time.py 256 --tol $tol --save /tmp/cfg3_256_$tol.hvfm > $O/build_$tol.log 2>&1
-  timeout 900 python bench.py --workload cfg3 --nrhs 1 --steps 100 --warmup 5 --tol $tol --fhat /tmp/cfg3_{n}_{tol}.hvfm --no-cpu-baseline > $O/bench_cfg3_k1_$tol.log 2>&1
+  timeout 900 python bench.py --workload cfg3 --nrhs 1 --steps 100 --warmup 5 --tol $tol --fhat /tmp/cfg3_256_$tol.hvfm --no-cpu-baseline > $O/bench_cfg3_k1_$tol.log 2>&1
 done
 echo done > $O/done
