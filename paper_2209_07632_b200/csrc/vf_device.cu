@@ -658,8 +658,11 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
         const bool col_ok = col < a.kp;
         T acc[VEC];
         if (KC == 1 && VEC == 1)
-            acc[0] = row_accumulate_k1<T, VF_MV_L1 && MODE == M_MATVEC>(a.segs, a.p2_segptr[r], a.p2_segptr[r + 1], vals,
-                                                                         a.idx, xc, lane, a.N);
+            // X rows through L1 where they are read-only for the whole launch:
+            // matvec, and the one-iteration M_STEP launch (the persistent solve
+            // re-writes both buffers across iterations: L2 only)
+            acc[0] = row_accumulate_k1<T, VF_MV_L1 && (MODE == M_MATVEC || MODE == M_STEP)>(
+                a.segs, a.p2_segptr[r], a.p2_segptr[r + 1], vals, a.idx, xc, lane, a.N);
         else row_accumulate<T, KC, VEC>(a.segs, a.p2_segptr[r], a.p2_segptr[r + 1], vals, a.idx, xc, a.kp, col,
                                         col_ok, g, acc);
         if (g != 0 || !col_ok) continue;
@@ -1374,6 +1377,15 @@ __global__ void permute_out_kernel(const T* src, const int32_t* perm, const uint
 }
 
 template <typename T>
+__global__ void gather2_kernel(const T* a, const T* b, const int32_t* perm, int64_t N, T* da, T* db) {
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t p = perm[r];
+        da[r] = a[p];
+        db[r] = b[p];
+    }
+}
+
+template <typename T>
 __global__ void gather_vec_kernel(const T* src, const int32_t* perm, int64_t N, T* dst) {
     for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < N; r += (int64_t)gridDim.x * blockDim.x)
         dst[r] = src[perm[r]];
@@ -1400,19 +1412,42 @@ __global__ void thermal_mid_kernel(const T* Qdir, const T* Q, const uint8_t* act
     }
 }
 
-// T = (((1 - alpha) Qvis + eps Qir) / (eps sigma))^(1/4)   (eq. 3d-equilbr)
+// Fused thermal output (a7 end): per 32 x 32 tile of tree rows x columns,
+// Qir = last Q (0 on rows F-hat does not touch), T = (((1 - alpha) Qvis +
+// eps Qir) / (eps sigma))^(1/4) (eq. 3d-equilbr), and T, Qvis, Qir
+// written straight to caller order (column-major N x k) through a
+// shared-memory transpose.  Qvis_out / Qir_out may be null.
 template <typename T>
-__global__ void thermal_T_kernel(const T* Qvis, const T* Q, const uint8_t* active, const T* alpha, const T* emis,
-                                 int64_t N, int k, int kp, T* Tout, T* Qir) {
-    const int64_t tot = N * kp;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / kp;
-        const int c = (int)(i - r * kp);
-        if (c >= k) { Tout[i] = T(0); Qir[i] = T(0); continue; }
-        const T qir = active[r] ? Q[i] : T(0);
-        const T qabs = (T(1) - alpha[r]) * Qvis[i] + emis[r] * qir;
-        Tout[i] = (T)sqrt(sqrt((double)qabs / ((double)emis[r] * kSigmaSB)));
-        Qir[i] = qir;
+__global__ void thermal_out_kernel(const T* Qvis, const T* Q, const uint8_t* active, const T* alpha, const T* emis,
+                                   const int32_t* perm, int64_t N, int k, int kp, T* Tout, T* Qvis_out, T* Qir_out) {
+    __shared__ T tT[32][33], tV[32][33], tI[32][33];
+    const int64_t r0 = (int64_t)blockIdx.x * 32;
+    const int c0 = blockIdx.y * 32;
+    for (int rr = threadIdx.y; rr < 32; rr += blockDim.y) {
+        const int64_t r = r0 + rr;
+        const int c = c0 + threadIdx.x;
+        T t = T(0), qv = T(0), qi = T(0);
+        if (r < N && c < k) {
+            const int64_t i = r * kp + c;
+            qv = Qvis[i];
+            qi = active[r] ? Q[i] : T(0);
+            const T qabs = (T(1) - alpha[r]) * qv + emis[r] * qi;
+            t = (T)sqrt(sqrt((double)qabs / ((double)emis[r] * kSigmaSB)));
+        }
+        tT[rr][threadIdx.x] = t;
+        tV[rr][threadIdx.x] = qv;
+        tI[rr][threadIdx.x] = qi;
+    }
+    __syncthreads();
+    for (int cc = threadIdx.y; cc < 32; cc += blockDim.y) {
+        const int64_t r = r0 + threadIdx.x;
+        const int c = c0 + cc;
+        if (r < N && c < k) {
+            const int64_t o = (int64_t)perm[r] + (int64_t)c * N;
+            Tout[o] = tT[threadIdx.x][cc];
+            if (Qvis_out) Qvis_out[o] = tV[threadIdx.x][cc];
+            if (Qir_out) Qir_out[o] = tI[threadIdx.x][cc];
+        }
     }
 }
 
@@ -2019,7 +2054,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         }
     }
     CK(cudaMalloc((void**)&D->ctl, sizeof(Ctl)));
-    CK(cudaMallocHost((void**)&D->ctl_host, sizeof(Ctl)));
+    CK(cudaMallocHost((void**)&D->ctl_host, 2 * sizeof(Ctl)));      // one per thermal stage
     D->evpool.resize(2048);
     D->evwhich.resize(1024);
     for (auto& e : D->evpool) CK(cudaEventCreate(&e));
@@ -2104,7 +2139,7 @@ int ensure_scratch(DeviceHMat* D, int kp) {
     CK(cudaMalloc((void**)&D->resid, (size_t)kp * 8));
     CK(cudaMemset(D->resid, 0, (size_t)kp * 8));
     if (D->resid_host) cudaFreeHost(D->resid_host);
-    CK(cudaMallocHost((void**)&D->resid_host, (size_t)kp * 8));
+    CK(cudaMallocHost((void**)&D->resid_host, (size_t)2 * kp * 8));
     D->kp_cap = kp;
     return VF_OK;
 }
@@ -2358,23 +2393,27 @@ HotArgs hot_args(DeviceHMat* D, int kp, int k) {
 // One Jacobi solve on the current XT/E state: one persistent launch.
 template <typename T>
 int iterate(Handle* h, int k, int kp, const void* rho, int clamp, int iters, double tol, cudaStream_t st,
-            int* iters_done, double* max_resid) {
+            int slot) {
     DeviceHMat* D = h->dev;
-    *iters_done = 0;
-    *max_resid = 0;
+    D->ctl_host[slot] = Ctl{};
     if (iters <= 0) return VF_OK;
     HotArgs a = hot_args(D, kp, k);
     a.E = D->Ep; a.rho = rho; a.Q = D->Qp; a.iters = iters; a.clamp = clamp; a.tol = tol;
     int rc = launch_hot<T, M_SOLVE>(h, a, st);
     if (rc) return rc;
-    CK(cudaMemcpyAsync(D->ctl_host, D->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(D->resid_host, D->resid, (size_t)k * 8, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    *iters_done = D->ctl_host->iter;
-    double mr = 0;
-    for (int c = 0; c < k; ++c) mr = std::max(mr, D->resid_host[c]);
-    *max_resid = mr;
+    // stage statistics -> pinned slot, read after the call's final synchronisation
+    // (no host round trip between the stages of a thermal solve)
+    CK(cudaMemcpyAsync(D->ctl_host + slot, D->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(D->resid_host + (size_t)slot * D->kp_cap, D->resid, (size_t)k * 8, cudaMemcpyDeviceToHost, st));
     return VF_OK;
+}
+
+// after the stream synchronisation: iterations and max residual of a stage
+void stage_stats(DeviceHMat* D, int slot, int k, int* iters_done, double* max_resid) {
+    *iters_done = D->ctl_host[slot].iter;
+    double mr = 0;
+    for (int c = 0; c < k; ++c) mr = std::max(mr, D->resid_host[(size_t)slot * D->kp_cap + c]);
+    *max_resid = mr;
 }
 
 // ---- ROWS mode host side -------------------------------------------------
@@ -2462,12 +2501,20 @@ int iterate_rows(Handle* h, int k, int kp, const void* rho, int clamp, int iters
     return VF_OK;
 }
 
+// One Jacobi stage.  Persistent path: statistics are deferred to slot and
+// read by stage_stats after the caller's final synchronisation (*deferred =
+// true); ROWS path: synchronous, statistics returned directly.
 template <typename T>
 int solve_stage(Handle* h, int k, int kp, const void* rho, int clamp, int iters, double tol, cudaStream_t st,
-                int* iters_done, double* max_resid) {
-    if (h->dev->world > 1 || h->comm)
+                int slot, int* iters_done, double* max_resid, bool* deferred) {
+    *iters_done = 0;
+    *max_resid = 0;
+    if (h->dev->world > 1 || h->comm) {
+        *deferred = false;
         return iterate_rows<T>(h, k, kp, rho, clamp, iters, tol, st, iters_done, max_resid);
-    return iterate<T>(h, k, kp, rho, clamp, iters, tol, st, iters_done, max_resid);
+    }
+    *deferred = true;
+    return iterate<T>(h, k, kp, rho, clamp, iters, tol, st, slot);
 }
 
 int check_k(int nrhs) {
@@ -2530,7 +2577,12 @@ int radiosity_impl(Handle* h, const void* E, const void* rho, void* B, int nrhs,
     launch_colnorm<T>(h, D->Ep, nrhs, kp, st);
     int it = 0;
     double res = 0;
-    if ((rc = solve_stage<T>(h, nrhs, kp, D->pv[0], clamp, iters, tol, st, &it, &res))) return rc;
+    bool deferred = false;
+    if ((rc = solve_stage<T>(h, nrhs, kp, D->pv[0], clamp, iters, tol, st, 0, &it, &res, &deferred))) return rc;
+    if (deferred) {                              // the result buffer depends on the iteration count
+        CK(cudaStreamSynchronize(st));
+        stage_stats(D, 0, nrhs, &it, &res);
+    }
     h->iters1 = it; h->resid1 = res; h->iters2 = 0; h->resid2 = 0;
     launch_permute_out<T>(h, D->xt[it & 1], nrhs, kp, false, Bd, st);
     CK(cudaGetLastError());
@@ -2562,15 +2614,15 @@ int thermal_impl(Handle* h, const void* Qdir, const void* alb, const void* emi, 
     if ((rc = stage_out_buf(h, 5, Qir, vb, &Qid))) return rc;
     T* alpha = (T*)D->pv[0];
     T* emis = (T*)D->pv[1];
-    gather_vec_kernel<T><<<148, 256, 0, st>>>((const T*)ad, D->perm, D->N, alpha);
-    gather_vec_kernel<T><<<148, 256, 0, st>>>((const T*)ed, D->perm, D->N, emis);
-    h->launches_total += 2;
+    gather2_kernel<T><<<148, 256, 0, st>>>((const T*)ad, (const T*)ed, D->perm, D->N, alpha, emis);
+    h->launches_total += 1;
     // stage 1: E = alpha Qdir, rho = alpha (reading R-A14)
     launch_permute_in<T>(h, Qd, nrhs, kp, ad, D->Ep, D->xt[0], D->xt[1], D->Qdp, st);
     launch_colnorm<T>(h, D->Ep, nrhs, kp, st);
     int it1 = 0, it2 = 0;
     double r1 = 0, r2 = 0;
-    if ((rc = solve_stage<T>(h, nrhs, kp, alpha, 1, iters, tol, st, &it1, &r1))) return rc;
+    bool def1 = false, def2 = false;
+    if ((rc = solve_stage<T>(h, nrhs, kp, alpha, 1, iters, tol, st, 0, &it1, &r1, &def1))) return rc;
     if (h->comm && (rc = rows_allgather_buf<T>(h, D->Qp, kp, st))) return rc;      // Qrefl of every rank
     // stage 2: Qvis = Qdir + Qrefl, E = (1 - alpha) Qvis, rho = 1
     const int64_t tot = D->N * kp;
@@ -2579,19 +2631,21 @@ int thermal_impl(Handle* h, const void* Qdir, const void* alb, const void* emi, 
                                               (T*)D->Qvp, (T*)D->Ep, (T*)D->xt[0], (T*)D->xt[1]);
     h->launches_total++;
     launch_colnorm<T>(h, D->Ep, nrhs, kp, st);
-    if ((rc = solve_stage<T>(h, nrhs, kp, nullptr, 1, iters, tol, st, &it2, &r2))) return rc;
+    if ((rc = solve_stage<T>(h, nrhs, kp, nullptr, 1, iters, tol, st, 1, &it2, &r2, &def2))) return rc;
     if (h->comm && (rc = rows_allgather_buf<T>(h, D->Qp, kp, st))) return rc;      // Qir of every rank
-    thermal_T_kernel<T><<<gb, 256, 0, st>>>((const T*)D->Qvp, (const T*)D->Qp, D->active, alpha, emis, D->N, nrhs,
-                                            kp, (T*)D->Yp, (T*)D->Qip);
-    h->launches_total++;
-    launch_permute_out<T>(h, D->Yp, nrhs, kp, false, Td, st);
-    if (Qvd) launch_permute_out<T>(h, D->Qvp, nrhs, kp, false, Qvd, st);
-    if (Qid) launch_permute_out<T>(h, D->Qip, nrhs, kp, false, Qid, st);
+    {
+        dim3 g((unsigned)((D->N + 31) / 32), (unsigned)((nrhs + 31) / 32));
+        thermal_out_kernel<T><<<g, dim3(32, 8), 0, st>>>((const T*)D->Qvp, (const T*)D->Qp, D->active, alpha, emis,
+                                                          D->perm, D->N, nrhs, kp, (T*)Td, (T*)Qvd, (T*)Qid);
+        h->launches_total++;
+    }
     CK(cudaGetLastError());
     if ((rc = stage_out_copy(Tout, Td, vb, st))) return rc;
     if ((rc = stage_out_copy(Qvis, Qvd, vb, st))) return rc;
     if ((rc = stage_out_copy(Qir, Qid, vb, st))) return rc;
     CK(cudaStreamSynchronize(st));
+    if (def1) stage_stats(D, 0, nrhs, &it1, &r1);
+    if (def2) stage_stats(D, 1, nrhs, &it2, &r2);
     if (h->timing) collect_timing(h);
     h->iters1 = it1; h->resid1 = r1; h->iters2 = it2; h->resid2 = r2;
     if (iters > 0 && (!(r1 <= tol) || !(r2 <= tol)))
