@@ -1682,29 +1682,23 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         D->p1_src = std::count(used.begin(), used.end(), 1);
     }
 
-    // ---- phase 2 rows: per tree row, its segments ----
-    std::vector<std::vector<Seg>> rowsegs(N);
+    // ---- phase 2 rows: per tree row, its segments.  Values are packed ROW BY
+    // ROW (a row's runs back to back, each 16-B aligned), so a warp streaming a
+    // row reads one contiguous range: no partial sectors between its runs.
+    struct PSeg { const double* p; int64_t src; int32_t len; };
+    std::vector<std::vector<PSeg>> rowsegs(N);
     // CSR leaves merged per row: collect (global col, value)
     std::vector<std::vector<std::pair<int32_t, double>>> csr_rows(N);
     for (int b = 0; b < (int)h->leaves.size(); ++b) {
         const Leaf& L = h->leaves[b];
         if (L.kind == K_DENSE) {
-            for (int64_t r = 0; r < L.m; ++r) {
-                Seg s;
-                s.val_off = push_vals(L.a.data() + r * L.n, L.n);
-                s.src = L.col0; s.len = (int32_t)L.n; s.kind = 0;
-                rowsegs[L.row0 + r].push_back(s);
-            }
+            for (int64_t r = 0; r < L.m; ++r) rowsegs[L.row0 + r].push_back({L.a.data() + r * L.n, L.col0, (int32_t)L.n});
             alg_bytes += (int64_t)sizeof(T) * L.m * L.n;
             alg_flops += 2 * L.m * L.n;
         } else if (L.kind == K_SVD) {
             const int64_t mu = (int64_t)L.idx_a.size();
-            for (int64_t r = 0; r < mu; ++r) {
-                Seg s;
-                s.val_off = push_vals(L.a.data() + r * L.q, L.q);
-                s.src = N + toff[b]; s.len = (int32_t)L.q; s.kind = 0;
-                rowsegs[L.row0 + L.idx_a[r]].push_back(s);
-            }
+            for (int64_t r = 0; r < mu; ++r)
+                rowsegs[L.row0 + L.idx_a[r]].push_back({L.a.data() + r * L.q, N + toff[b], (int32_t)L.q});
             alg_bytes += (int64_t)sizeof(T) * L.q * mu + 4 * mu;
             alg_flops += 2 * L.q * mu;
         } else if (L.kind == K_CSR) {
@@ -1723,7 +1717,13 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     for (int64_t i = 0; i < N; ++i) {
         auto& cr = csr_rows[i];
         if (rowsegs[i].empty() && cr.empty()) continue;
-        for (auto& s : rowsegs[i]) segs.push_back(s);
+        for (auto& ps : rowsegs[i]) {
+            Seg s;
+            s.val_off = push_vals(ps.p, ps.len);
+            s.src = ps.src; s.len = ps.len; s.kind = 0;
+            segs.push_back(s);
+        }
+        std::vector<PSeg>().swap(rowsegs[i]);
         if (!cr.empty()) {
             std::stable_sort(cr.begin(), cr.end(), [](auto& a, auto& b) { return a.first < b.first; });
             Seg s;
