@@ -52,6 +52,18 @@ def peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
+def ncu_traffic(key):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu
+    `--set full` capture (profiles/traffic.json, written from the capture's
+    dram__bytes_read.sum + dram__bytes_write.sum); None if absent."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        d = json.load(open(p))[key]
+        return d["dram_bytes_per_launch"], d["source"]
+    except Exception:
+        return None, None
+
+
 def fp64_peak_tflops(sm_mhz):
     # B200: 148 SMs x 64 FP64 FMA/clk/SM x 2 flop (DESIGN.md §Roofline)
     return 148 * 64 * 2 * sm_mhz * 1e6 / 1e12
@@ -336,8 +348,9 @@ def run_gpu(args, rank, world, local_rank):
         ach_tf = flops_launch / (avg * 1e-3) / 1e12 if avg > 0 else 0.0
         ach_gbs = bytes_launch / (avg * 1e-3) / 1e9 if avg > 0 else 0.0
         dmma = bool(info.get("resident")) and dt == "f64"     # res_kernel contracts on FP64 tensor cores (DMMA)
+        traffic, traffic_src = ncu_traffic(f"cfg2_{dt}")
         roof = {"bound": "tensor" if dmma else "alu", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": ach_tf / peak_tf if peak_tf else None, "traffic": None,
+                "frac": ach_tf / peak_tf if peak_tf else None, "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": (f"res_kernel<{'double' if dt == 'f64' else 'float'},M_SOLVE> (persistent Jacobi solve, "
                            "F-hat resident in shared memory: phase 1 V^T X, grid barrier, phase 2 row-owner "
                            "accumulate + fused epilogue, residual decision; one launch per thermal stage)"
@@ -568,8 +581,9 @@ def run_terrain(args, rank, world, local_rank):
         apps_launch = (n_app / max(l_hot / args.steps, 1)) if rows_mode else 1
         ach_gbs = bytes_app * apps_launch / (avg * 1e-3) / 1e9 if avg > 0 else 0.0
         hbm = pk.get("hbm_gbs", 6559.0)
+        traffic, traffic_src = ncu_traffic(f"{args.workload}_k{k}_{dt}")
         roof = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm,
-                "traffic": None,
+                "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": ("hot_kernel<...,M_STEP> (ROWS mode: one Jacobi iteration per launch)" if rows_mode else
                            "hot_kernel<...,M_MATVEC> (phase 1 V^T X, grid barrier, phase 2 row-owner accumulate)"),
                 "peak_basis": f"{pk_kind} MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",

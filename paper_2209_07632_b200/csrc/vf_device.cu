@@ -879,7 +879,11 @@ __device__ __forceinline__ void groups_phase(const HotArgs& a, T* xc, T* xn, dou
 #ifndef VF_RST
 #define VF_RST 2
 #endif
+#ifndef VF_RES_WARPS
+#define VF_RES_WARPS 16
+#endif
 constexpr int kKS = VF_RKS;        // source rows per staged slice
+constexpr int kRW = VF_RES_WARPS;  // warps of a res_kernel CTA (one CTA per SM)
 constexpr int kRS = VF_RST;        // staging ring depth (slices in flight: kRS - 1)
 struct RGroup {
     int32_t nrows;     // <= 16
@@ -910,7 +914,7 @@ template <typename T>
 __device__ __forceinline__ void res_stage(const int32_t* S, int j0, int n, const T* xc, int64_t kp, int cb, T* Xs) {
     constexpr int EPL = 16 / (int)sizeof(T);          // elements per 16-B copy
     constexpr int OPS = 16 / EPL;                     // copies per staged row
-    for (int op = threadIdx.x; op < n * OPS; op += kThreads) {
+    for (int op = threadIdx.x; op < n * OPS; op += kRW * 32) {
         const int j = op / OPS, part = op - j * OPS;
         const int64_t row = S[j0 + j];
         cpa<16>(Xs + j * 16 + part * EPL, xc + row * kp + cb + part * EPL, 16);
@@ -1003,7 +1007,7 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
             const int lane = t & 31, warp = t >> 5;
             const int kr = lane & 3, mn = lane >> 2;
             const double* wb = W + G.w_off + (int64_t)j0 * 16;
-            for (int kb = warp * 4; kb < n; kb += 32) {
+            for (int kb = warp * 4; kb < n; kb += 4 * kRW) {
                 const int j = kb + kr;
                 const bool ok = j < n;
                 const double a0 = ok ? wb[j * 16 + mn] : 0.0, a1 = ok ? wb[j * 16 + 8 + mn] : 0.0;
@@ -1048,11 +1052,13 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
                     dacc[tl][0] = dacc[tl][1] = 0.0;
                 }
                 __syncthreads();
-                const int tl = (rr >> 3) * 2 + (cc >> 3);
-                const int ln = (rr & 7) * 4 + ((cc & 7) >> 1), ii = cc & 1;
-                double sum = 0.0;
-                for (int w2 = 0; w2 < kWarps; ++w2) sum += red[((w2 * 4 + tl) * 32 + ln) * 2 + ii];
-                q = sum;
+                if (rr < 16) {
+                    const int tl = (rr >> 3) * 2 + (cc >> 3);
+                    const int ln = (rr & 7) * 4 + ((cc & 7) >> 1), ii = cc & 1;
+                    double sum = 0.0;
+                    for (int w2 = 0; w2 < kRW; ++w2) sum += red[((w2 * 4 + tl) * 32 + ln) * 2 + ii];
+                    q = sum;
+                }
             }
             const int col = cur.ch * 16 + cc;
             double d2 = 0.0;
@@ -1074,7 +1080,7 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
                 }
             }
             if (PHASE == 2 && MODE != M_MATVEC) {          // per-column partials, rows in fixed order
-                tile[t] = d2;
+                if (t < 256) tile[t] = d2;
                 __syncthreads();
                 if (t < 16) {
                     double sum = 0.0;
@@ -1090,24 +1096,24 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
 }
 
 template <typename T, int MODE>
-__global__ void __launch_bounds__(kThreads, 1) res_kernel(HotArgs a, ResArgs r) {
+__global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) {
     extern __shared__ __align__(16) unsigned char smraw[];
     T* W = reinterpret_cast<T*>(smraw);
     int32_t* S = reinterpret_cast<int32_t*>(W + r.wcap);
     T* Xs = reinterpret_cast<T*>(S + r.scap);
     double* sred = reinterpret_cast<double*>(Xs + kRS * kKS * 16);
     double* tile = sred + a.kp;
-    double* red = tile + 256;                          // [8 warps][4 tiles][32 lanes][2] DMMA partials
+    double* red = tile + 256;                          // [kRW warps][4 tiles][32 lanes][2] DMMA partials
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned nblk = gridDim.x;
     {   // this CTA's F-hat values and source-row lists -> smem, once per launch
         const int64_t w0 = r.cta_woff[blockIdx.x], w1 = r.cta_woff[blockIdx.x + 1];
         constexpr int EPL = 16 / (int)sizeof(T);
         const T* src = static_cast<const T*>(r.wblob) + w0;
-        for (int64_t e = (int64_t)threadIdx.x * EPL; e < w1 - w0; e += (int64_t)kThreads * EPL)
+        for (int64_t e = (int64_t)threadIdx.x * EPL; e < w1 - w0; e += (int64_t)blockDim.x * EPL)
             cpa<16>(W + e, src + e, 16);
         const int64_t s0 = r.cta_soff[blockIdx.x], s1 = r.cta_soff[blockIdx.x + 1];
-        for (int64_t e = (int64_t)threadIdx.x * 4; e < s1 - s0; e += (int64_t)kThreads * 4)
+        for (int64_t e = (int64_t)threadIdx.x * 4; e < s1 - s0; e += (int64_t)blockDim.x * 4)
             cpa<16>(S + e, r.sblob + s0 + e, 16);
         cpa_commit();
         cpa_wait<0>();
@@ -1141,17 +1147,17 @@ __global__ void __launch_bounds__(kThreads, 1) res_kernel(HotArgs a, ResArgs r) 
                 return;
             }
         }
-        for (int c = threadIdx.x; c < a.kp; c += kThreads) sred[c] = 0.0;
+        for (int c = threadIdx.x; c < a.kp; c += blockDim.x) sred[c] = 0.0;
         __syncthreads();
         res_phase<T, 2, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red);
         __syncthreads();
         double* part = a.partial + (MODE == M_STEP ? 0 : (int64_t)(it & 1) * nblk * a.kp);   // [kp][nblk]
-        for (int c = threadIdx.x; c < a.kp; c += kThreads) part[(int64_t)c * nblk + blockIdx.x] = sred[c];
+        for (int c = threadIdx.x; c < a.kp; c += blockDim.x) part[(int64_t)c * nblk + blockIdx.x] = sred[c];
         if (MODE == M_STEP) return;
         trace_ev(a, it, 3);
         grid_sync(a.ctl, nblk);                                        // B2
         trace_ev(a, it, 4);
-        for (int c = blockIdx.x + (int)nblk * warp; c < a.k; c += (int)nblk * kWarps) {
+        for (int c = blockIdx.x + (int)nblk * warp; c < a.k; c += (int)nblk * kRW) {
             const double* pc = part + (int64_t)c * nblk;
             double sum = 0.0;
             for (unsigned b = lane; b < nblk; b += 32u) sum += __ldcg(pc + b);
@@ -1951,7 +1957,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             hg.push_back(std::move(x));
         }
         const int64_t fixed = (int64_t)kRS * kKS * 16 * (int64_t)sizeof(T) + 256 * 8 + (int64_t)kMaxKp * 8 + 256 +
-                              (int64_t)kWarps * 4 * 32 * 2 * 8;
+                              (int64_t)kRW * 4 * 32 * 2 * 8;
         const int64_t budget = smem_optin - fixed;                 // bytes for values + source rows
         auto need = [&](const HG& x) { return (x.K * kGroup + EPL) * (int64_t)sizeof(T) + (x.K + 4) * 4; };
         bool ok = budget > 0 && !hg.empty();
@@ -2322,10 +2328,10 @@ int launch_res(Handle* h, HotArgs& a, cudaStream_t st) {
     DeviceHMat* D = h->dev;
     auto fn = res_kernel<T, MODE>;
     const size_t smem = (size_t)D->res_wcap * sizeof(T) + (size_t)D->res_scap * 4 + (size_t)kRS * kKS * 16 * sizeof(T) +
-                        (size_t)a.kp * 8 + 256 * 8 + (size_t)kWarps * 4 * 32 * 2 * 8;
+                        (size_t)a.kp * 8 + 256 * 8 + (size_t)kRW * 4 * 32 * 2 * 8;
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kRW * 32, smem));
     if (per_sm < 1) return set_error(VF_ECUDA, "resident kernel cannot be resident");
     ResArgs r{D->r_groups, D->r_outrow, D->r_wblob, D->r_cta_woff, D->r_sblob, D->r_cta_soff,
               D->r_p1_ptr, D->r_p1_list, D->r_p2_ptr, D->r_p2_list, D->res_wcap, D->res_scap};
@@ -2343,7 +2349,7 @@ int launch_res(Handle* h, HotArgs& a, cudaStream_t st) {
     if (MODE != M_STEP) CK(cudaMemsetAsync(a.ctl, 0, offsetof(Ctl, bar_gen), st));
     {
         Timer tm(h, st, 2);
-        CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kThreads), args, smem, st));
+        CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kRW * 32), args, smem, st));
     }
     h->launches_total++;
     D->last_grid = grid;
@@ -2368,7 +2374,7 @@ int launch_hot(Handle* h, HotArgs& a, cudaStream_t st) {
     const int kp = a.kp;
     if (kp >= 16 && kp % 16 == 0 && h->dev->res_ok &&
         (size_t)h->dev->res_wcap * sizeof(T) + (size_t)h->dev->res_scap * 4 + (size_t)kRS * kKS * 16 * sizeof(T) +
-                (size_t)kp * 8 + 2048 + (size_t)kWarps * 4 * 32 * 2 * 8 <= (size_t)232448)
+                (size_t)kp * 8 + 2048 + (size_t)kRW * 4 * 32 * 2 * 8 <= (size_t)232448)
         return launch_res<T, MODE>(h, a, st);
     if (kp == 1) return launch_hot_t<T, 1, 1, MODE, false>(h, a, st);
     if (kp == 2) return launch_hot_t<T, 1, 2, MODE, false>(h, a, st);

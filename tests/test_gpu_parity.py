@@ -339,3 +339,27 @@ def test_resident_and_streaming_batched_paths(cfg2_small, rough, tmp_path_factor
             M.solve_radiosity(dev(E), dev(rho), B, iters=200, tol=1e-13)
             assert M.stats()["iters1"] == it0
             assert rel(host(B), B0) <= 1e-12
+
+
+def test_k1_matvec_flags_equal_barrier_bitwise(rough, tmp_path_factory, monkeypatch):
+    """nrhs = 1 matvec: the barrier-free schedule (per-block T flags, dynamic
+    row queue) sums every row in the same fixed order as the grid-barrier
+    schedule, so the two must agree bit for bit (and match the oracle)."""
+    V, F, S, Fd = rough
+    H = hm.compress(S.x, Fd, 1e-6, min_size=2048)
+    p = str(tmp_path_factory.mktemp("k1") / "r.hvfm")
+    hm.write_hvfm(H, p)
+    X = sg.random_rhs(S.N, 1, seed=9)
+    out = []
+    for barrier in (False, True):
+        if barrier:
+            monkeypatch.setenv("VF_MV_BARRIER", "1")
+        else:
+            monkeypatch.delenv("VF_MV_BARRIER", raising=False)
+        M = vf.ViewFactorMatrix.load(p, device=0)
+        Y = empty(S.N, 1)
+        for _ in range(3):                       # repeated launches reset the flags and the queue
+            M.matvec(dev(X), Y)
+        out.append(host(Y))
+    assert np.array_equal(out[0], out[1])
+    assert rel(out[0], hm.hmatvec(H, X)) <= 1e-12
