@@ -880,7 +880,7 @@ __device__ __forceinline__ void groups_phase(const HotArgs& a, T* xc, T* xn, dou
 #define VF_RST 2
 #endif
 #ifndef VF_RES_WARPS
-#define VF_RES_WARPS 16
+#define VF_RES_WARPS 8
 #endif
 constexpr int kKS = VF_RKS;        // source rows per staged slice
 constexpr int kRW = VF_RES_WARPS;  // warps of a res_kernel CTA (one CTA per SM)
@@ -2545,7 +2545,10 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     launch_permute_in<T>(h, Xd, nrhs, kp, nullptr, D->xt[0], nullptr, nullptr, nullptr, st);
     HotArgs a = hot_args(D, kp, nrhs);
     a.Y = D->Yp;
-    if (kp == 1 && !getenv("VF_MV_BARRIER")) {          // phase-1 -> phase-2 by per-block flags, dynamic rows
+    // optional (VF_MV_FLAGS=1): phase 1 -> phase 2 by per-block flags and a dynamic
+    // row queue instead of the grid barrier.  Measured slower on cfg3-shaped
+    // F-hat (flag spinning + queue atomics > barrier wait), so off by default.
+    if (kp == 1 && getenv("VF_MV_FLAGS") && !getenv("VF_MV_BARRIER")) {
         CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
         a.tready = D->tready; a.seg_blk = D->seg_blk; a.g1_blk = D->g1_blk;
         a.qctr = D->tready + D->n_svd; a.p2_order = D->p2_order;

@@ -353,9 +353,9 @@ def test_k1_matvec_flags_equal_barrier_bitwise(rough, tmp_path_factory, monkeypa
     out = []
     for barrier in (False, True):
         if barrier:
-            monkeypatch.setenv("VF_MV_BARRIER", "1")
+            monkeypatch.delenv("VF_MV_FLAGS", raising=False)
         else:
-            monkeypatch.delenv("VF_MV_BARRIER", raising=False)
+            monkeypatch.setenv("VF_MV_FLAGS", "1")
         M = vf.ViewFactorMatrix.load(p, device=0)
         Y = empty(S.N, 1)
         for _ in range(3):                       # repeated launches reset the flags and the queue
