@@ -445,8 +445,26 @@ SvdResult estimate_rank(int64_t mu, int64_t nv, const double* dense, const int64
             if (nxt / s1 < eps) { q = qq; break; }
         }
         if (q > 0 && !T.exact) {                              // verify the randomized truncation
-            while (q < kk && 1.2 * residual_norm(A, T, q, rng) >= eps * s1) ++q;
-            if (1.2 * residual_norm(A, T, q, rng) >= eps * s1) q = 0;
+            // smallest q' in [q, kk] whose residual passes (the residual norm is
+            // non-increasing in q'): exponential probe, then bisection
+            auto pass = [&](int64_t qq) { return 1.2 * residual_norm(A, T, qq, rng) < eps * s1; };
+            if (!pass(q)) {
+                int64_t lo = q, hi = -1, step = 1;           // lo fails
+                while (hi < 0) {
+                    const int64_t c = std::min<int64_t>(kk, lo + step);
+                    if (pass(c)) hi = c;
+                    else if (c == kk) break;
+                    else { lo = c; step *= 2; }
+                }
+                if (hi < 0) q = 0;
+                else {
+                    while (hi - lo > 1) {
+                        const int64_t mid = (lo + hi) / 2;
+                        if (pass(mid)) hi = mid; else lo = mid;
+                    }
+                    q = hi;
+                }
+            }
         }
         if (q > 0) {
             if (svd_bytes(q) >= target_bytes) return R;         // eq. nbytes-comparison fails
