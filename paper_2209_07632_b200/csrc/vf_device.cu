@@ -2380,6 +2380,19 @@ int launch_hot(Handle* h, HotArgs& a, cudaStream_t st) {
     if (kp == 2) return launch_hot_t<T, 1, 2, MODE, false>(h, a, st);
     if (kp == 4) return launch_hot_t<T, 1, 2, MODE, true>(h, a, st);
     if (kp == 8) return launch_hot_t<T, 1, 4, MODE, true>(h, a, st);
+    // wide batches whose F-hat does not fit the resident layout (e.g. cfg3,
+    // 3.7 GB): the per-row layout with a warp across the columns -- every
+    // lane reads the same F-hat term (broadcast) and its own VEC contiguous
+    // columns of the source row, so F-hat streams from HBM once per column
+    // chunk of 32 VEC and the XT rows come from L2 as full 128-B lines.
+    // (VF_WIDE=0 selects the row-group path instead.)
+    static const bool wide = !getenv("VF_WIDE") || atoi(getenv("VF_WIDE")) != 0;
+    if (wide) {
+        if (kp % 128 == 0) return launch_hot_t<T, 32, 4, MODE, false>(h, a, st);
+        if (kp % 64 == 0) return launch_hot_t<T, 32, 2, MODE, false>(h, a, st);
+        if (kp % 32 == 0) return launch_hot_t<T, 32, 1, MODE, false>(h, a, st);
+        return launch_hot_t<T, 16, 1, MODE, false>(h, a, st);
+    }
     return launch_hot_t<T, 1, 8, MODE, true>(h, a, st);
 }
 
