@@ -316,19 +316,26 @@ template <> struct V4<float> {
 #ifndef VF_XVEC
 #define VF_XVEC 1
 #endif
+// read-only X gathers: through L1 with the default load, or the non-coherent
+// texture path (VF_X_LDG=1); X is not written during the launches that use it
+#if defined(VF_X_LDG) && VF_X_LDG
+#define XLD(p) __ldg(p)
+#else
+#define XLD(p) (*(p))
+#endif
 // 4 contiguous x values (16-B aligned): through L1 (matvec) or L2 only
 template <typename T, bool L1X> struct XV4;
 template <bool L1X> struct XV4<double, L1X> {
     static __device__ __forceinline__ void ld(const double* p, double* v) {
         const double2* q = reinterpret_cast<const double2*>(p);
-        const double2 a = L1X ? q[0] : __ldcg(q), b = L1X ? q[1] : __ldcg(q + 1);
+        const double2 a = L1X ? XLD(q) : __ldcg(q), b = L1X ? XLD(q + 1) : __ldcg(q + 1);
         v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
     }
 };
 template <bool L1X> struct XV4<float, L1X> {
     static __device__ __forceinline__ void ld(const float* p, float* v) {
         const float4* q = reinterpret_cast<const float4*>(p);
-        const float4 a = L1X ? q[0] : __ldcg(q);
+        const float4 a = L1X ? XLD(q) : __ldcg(q);
         v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
     }
 };
@@ -414,7 +421,7 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
                     else XV4<T, false>::ld(xt + xr[c][0], x[c]);
                 } else if (l1[c]) {
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) x[c][u] = xt[xr[c][u]];
+                    for (int u = 0; u < 4; ++u) x[c][u] = XLD(xt + xr[c][u]);
                 } else {
 #pragma unroll
                     for (int u = 0; u < 4; ++u) x[c][u] = __ldcg(xt + xr[c][u]);
