@@ -900,6 +900,9 @@ struct RGroup {
     int64_t out_off;   // 16 output rows (tree rows or T rows) at outrow[out_off ..]
     int32_t ch0, chstep;  // 16-column chunks ch0, ch0 + chstep, ... of this copy (phase-1
                           // groups are replicated over CTAs, each copy taking every chstep-th chunk)
+    int32_t role;         // -1: whole group; 0 / 1: K-half of a group split over the two CTAs of
+                          // a cluster pair (rank 1 sends its partial tile to rank 0 through DSMEM)
+    int32_t pad_;
 };
 struct ResArgs {
     const RGroup* groups;
@@ -914,6 +917,7 @@ struct ResArgs {
     const int32_t* p2_list;
     int wcap;                     // smem elements reserved for the value blob
     int scap;                     // smem ints reserved for the source rows
+    int split;                    // groups split over cluster pairs (launch with cluster dim 2)
 };
 
 // stage X[src_j, cb .. cb+16) for j in [j0, j0 + n) into Xs[j - j0][16]
@@ -937,6 +941,15 @@ __device__ __forceinline__ void dmma884(double* d, double a, double b) {
                  : "d"(a), "d"(b));
 }
 
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void st_cluster_f64(const double* local_smem, unsigned rank, double v) {
+    unsigned laddr = static_cast<unsigned>(__cvta_generic_to_shared(local_smem)), raddr;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(raddr) : "r"(laddr), "r"(rank));
+    asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(raddr), "d"(v) : "memory");
+}
+
 struct ResCursor {
     int g, ch, sl;
     RGroup G;
@@ -944,7 +957,8 @@ struct ResCursor {
 
 template <typename T, int PHASE, int MODE>
 __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, const T* W, const int32_t* S, T* Xs,
-                                          T* xc, T* xn, double* sred, double* tile, double* red) {
+                                          T* xc, T* xn, double* sred, double* tile, double* red, double* xch,
+                                          int& xpar) {
     const int32_t* ptr = PHASE == 1 ? r.p1_ptr : r.p2_ptr;
     const int32_t* lst = PHASE == 1 ? r.p1_list : r.p2_list;
     const int g0 = ptr[blockIdx.x], g1 = ptr[blockIdx.x + 1];
@@ -997,7 +1011,7 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
             advance(nxt);
         }
         cpa_commit();
-        if (PHASE == 2 && MODE != M_MATVEC && cur.sl == 0 && rr < cur.G.nrows) {
+        if (PHASE == 2 && MODE != M_MATVEC && cur.sl == 0 && rr < cur.G.nrows && cur.G.role != 1) {
             const int64_t o = (int64_t)__ldg(r.outrow + cur.G.out_off + rr) * kp + cur.ch * 16 + cc;
             e_pre = __ldcg(static_cast<const T*>(a.E) + o);
             b_pre = __ldcg(xc + o);
@@ -1067,9 +1081,16 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
                     q = sum;
                 }
             }
+            if (PHASE == 2 && G.role >= 0) {                 // K split over the cluster pair
+                double* xb = xch + xpar * 256;
+                if (G.role == 1 && t < 256) st_cluster_f64(xb + t, 0u, (double)q);
+                cluster_sync_all();
+                xpar ^= 1;
+                if (G.role == 0 && t < 256) q = (T)((double)q + xb[t]);   // rank 0's half + rank 1's half
+            }
             const int col = cur.ch * 16 + cc;
             double d2 = 0.0;
-            if (rr < G.nrows) {
+            if (rr < G.nrows && G.role != 1) {
                 const int64_t orow = __ldg(r.outrow + G.out_off + rr);
                 if (PHASE == 1) {
                     xc[(a.N + orow) * kp + col] = static_cast<const T*>(a.p1_scale)[orow] * q;
@@ -1111,6 +1132,8 @@ __global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) 
     double* sred = reinterpret_cast<double*>(Xs + kRS * kKS * 16);
     double* tile = sred + a.kp;
     double* red = tile + 256;                          // [kRW warps][4 tiles][32 lanes][2] DMMA partials
+    double* xch = red + kRW * 4 * 32 * 2;              // [2][256] partner tiles (DSMEM, cluster pairs)
+    int xpar = 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned nblk = gridDim.x;
     {   // this CTA's F-hat values and source-row lists -> smem, once per launch
@@ -1126,6 +1149,7 @@ __global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) 
         cpa_wait<0>();
         __syncthreads();
     }
+    if (r.split) cluster_sync_all();                   // the pair partner is resident before any DSMEM store
     const bool have_p1 = a.n_g1 > 0;
     int cur = 0;
     if (MODE == M_STEP) {
@@ -1136,12 +1160,12 @@ __global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) 
         T* xc = static_cast<T*>(cur ? a.xt1 : a.xt0);
         T* xn = static_cast<T*>(cur ? a.xt0 : a.xt1);
         trace_ev(a, it, 0);
-        if (have_p1) res_phase<T, 1, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red);
+        if (have_p1) res_phase<T, 1, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red, xch, xpar);
         trace_ev(a, it, 1);
         if (MODE == M_MATVEC) {
             if (have_p1 && !a.tready) grid_sync(a.ctl, nblk);   // nrhs = 1: per-block T flags instead
             trace_ev(a, it, 2);
-            res_phase<T, 2, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red);
+            res_phase<T, 2, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red, xch, xpar);
             trace_ev(a, it, 3);
             return;
         }
@@ -1156,7 +1180,7 @@ __global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) 
         }
         for (int c = threadIdx.x; c < a.kp; c += blockDim.x) sred[c] = 0.0;
         __syncthreads();
-        res_phase<T, 2, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red);
+        res_phase<T, 2, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red, xch, xpar);
         __syncthreads();
         double* part = a.partial + (MODE == M_STEP ? 0 : (int64_t)(it & 1) * nblk * a.kp);   // [kp][nblk]
         for (int c = threadIdx.x; c < a.kp; c += blockDim.x) part[(int64_t)c * nblk + blockIdx.x] = sred[c];
@@ -1597,6 +1621,7 @@ struct DeviceHMat {
     // resident batched layout (res_kernel); res_ok = false -> streaming path
     bool res_ok = false;
     int res_grid = 0, res_wcap = 0, res_scap = 0;
+    bool res_split = false;
     RGroup* r_groups = nullptr;
     int32_t *r_outrow = nullptr, *r_sblob = nullptr;
     void* r_wblob = nullptr;
@@ -1943,7 +1968,10 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, D->device);
         cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, D->device);
         constexpr int EPL = 16 / (int)sizeof(T);
-        struct HG { int phase; int64_t g; int64_t K; std::vector<int32_t> ucols; int ch0 = 0, chstep = 1; };
+        struct HG {
+            int phase; int64_t g; int64_t K; std::vector<int32_t> ucols; int ch0 = 0, chstep = 1;
+            int role = -1; int64_t kb = 0;                 // K-half [kb, kb + K) of a split group
+        };
         std::vector<HG> hg;
         // phase-1 groups are few and short: each is replicated kP1Copies times so
         // that its column chunks run on different SMs (copy i takes chunks i, i + kP1Copies, ...)
@@ -1963,8 +1991,28 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             x.K += (int64_t)x.ucols.size();
             hg.push_back(std::move(x));
         }
+        // phase-2 groups with a long K are split over the two CTAs of a cluster
+        // pair (K halves; rank 1 sends its partial tile to rank 0): the largest
+        // per-SM FP64 work item halves.  VF_RES_SPLIT=0 disables.
+        const bool split = (nsm % 2 == 0) && (!getenv("VF_RES_SPLIT") || atoi(getenv("VF_RES_SPLIT")) != 0);
+        if (split) {
+            std::vector<HG> out;
+            for (auto& x : hg) {
+                if (x.phase == 2 && x.K >= 192) {
+                    const int64_t Ka = (x.K + 1) / 2;
+                    HG a0 = x, a1 = x;
+                    a0.role = 0; a0.kb = 0; a0.K = Ka;
+                    a1.role = 1; a1.kb = Ka; a1.K = x.K - Ka;
+                    out.push_back(std::move(a0));
+                    out.push_back(std::move(a1));
+                } else {
+                    out.push_back(std::move(x));
+                }
+            }
+            hg.swap(out);
+        }
         const int64_t fixed = (int64_t)kRS * kKS * 16 * (int64_t)sizeof(T) + 256 * 8 + (int64_t)kMaxKp * 8 + 256 +
-                              (int64_t)kRW * 4 * 32 * 2 * 8;
+                              (int64_t)kRW * 4 * 32 * 2 * 8 + 2 * 256 * 8;
         const int64_t budget = smem_optin - fixed;                 // bytes for values + source rows
         auto need = [&](const HG& x) { return (x.K * kGroup + EPL) * (int64_t)sizeof(T) + (x.K + 4) * 4; };
         bool ok = budget > 0 && !hg.empty();
@@ -1974,7 +2022,25 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             std::vector<size_t> ord(hg.size());
             std::iota(ord.begin(), ord.end(), 0);
             std::stable_sort(ord.begin(), ord.end(), [&](size_t x, size_t y) { return hg[x].K > hg[y].K; });
+            // split halves: half 0 of a group at index q, half 1 at q + 1 (adjacent in hg); a
+            // pair p = (2p, 2p + 1) takes both, rank 0 the first half
             for (size_t q : ord) {
+                if (hg[q].role != 0) continue;
+                const int64_t n0 = need(hg[q]), n1 = need(hg[q + 1]);
+                int best = -1;
+                for (int c = 0; c + 1 < nsm; c += 2)
+                    if (used[c] + n0 <= budget && used[c + 1] + n1 <= budget &&
+                        (best < 0 || load2[c] + load2[c + 1] < load2[best] + load2[best + 1]))
+                        best = c;
+                if (best < 0) { ok = false; break; }
+                owner[q] = best; owner[q + 1] = best + 1;
+                used[best] += n0; used[best + 1] += n1;
+                load2[best] += hg[q].K * (int64_t)(kGroup + 1) + 256;
+                load2[best + 1] += hg[q + 1].K * (int64_t)(kGroup + 1) + 256;
+            }
+            for (size_t q : ord) {
+                if (!ok) break;
+                if (hg[q].role >= 0) continue;
                 const int64_t nb = need(hg[q]);
                 std::vector<int64_t>& ld = hg[q].phase == 1 ? load1 : load2;
                 int best = -1;
@@ -1997,8 +2063,14 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                 cta_soff[c] = (int64_t)sblob.size();
                 const int64_t wbase = (int64_t)blob.size(), sbase = (int64_t)sblob.size();
                 for (int ph = 1; ph <= 2; ++ph) {
-                    for (size_t q = 0; q < hg.size(); ++q) {
-                        if (owner[q] != c || hg[q].phase != ph) continue;
+                    // phase 2: the pair's split halves first, in the same (hg) order on both
+                    // CTAs of the pair, so their DSMEM exchanges happen in lockstep
+                    std::vector<size_t> qs;
+                    for (size_t q = 0; q < hg.size(); ++q)
+                        if (owner[q] == c && hg[q].phase == ph && hg[q].role >= 0) qs.push_back(q);
+                    for (size_t q = 0; q < hg.size(); ++q)
+                        if (owner[q] == c && hg[q].phase == ph && hg[q].role < 0) qs.push_back(q);
+                    for (size_t q : qs) {
                         const Group& G = ph == 1 ? g1v[hg[q].g] : g2v[hg[q].g];
                         const int64_t g = hg[q].g;
                         RGroup R{};
@@ -2006,29 +2078,36 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                         R.K = (int32_t)hg[q].K;
                         R.ch0 = hg[q].ch0;
                         R.chstep = hg[q].chstep;
+                        R.role = hg[q].role;
                         R.w_off = (int32_t)((int64_t)blob.size() - wbase);
                         R.s_off = (int32_t)((int64_t)sblob.size() - sbase);
                         blob.resize(blob.size() + (size_t)hg[q].K * kGroup, T(0));
                         T* Wg = blob.data() + wbase + R.w_off;
+                        // source j of the full group (shared runs, then the CSR column
+                        // union) lands at row j - kb of this block if kb <= j < kb + K
+                        const int64_t kb = hg[q].kb, ke = hg[q].kb + hg[q].K;
                         int64_t j0 = 0;
                         for (int sgi = 0; sgi < G.nseg; ++sgi) {
                             const GSeg& sg = gsegv[G.seg_off + sgi];
                             for (int64_t e = 0; e < sg.len; ++e) {
+                                const int64_t j = j0 + e;
+                                if (j < kb || j >= ke) continue;
                                 sblob.push_back((int32_t)(sg.kind ? idx[sg.src + e] : sg.src + e));
                                 for (int r = 0; r < G.nrows; ++r)
-                                    Wg[(j0 + e) * kGroup + r] = vals[gvov[(G.seg_off + sgi) * kGroup + r] + e];
+                                    Wg[(j - kb) * kGroup + r] = vals[gvov[(G.seg_off + sgi) * kGroup + r] + e];
                             }
                             j0 += sg.len;
                         }
                         const std::vector<int32_t>& U = hg[q].ucols;
-                        for (int32_t col : U) sblob.push_back(col);
+                        for (size_t u = 0; u < U.size(); ++u)
+                            if (j0 + (int64_t)u >= kb && j0 + (int64_t)u < ke) sblob.push_back(U[u]);
                         for (int r = 0; ph == 2 && r < G.nrows; ++r) {
                             const int64_t cs = gcsr2v[g * kGroup + r];
                             if (cs < 0) continue;
                             for (int32_t e = 0; e < segs[cs].len; ++e) {
                                 const int32_t col = idx[segs[cs].src + e];
-                                const int64_t pos = std::lower_bound(U.begin(), U.end(), col) - U.begin();
-                                Wg[(j0 + pos) * kGroup + r] = vals[segs[cs].val_off + e];
+                                const int64_t j = j0 + (std::lower_bound(U.begin(), U.end(), col) - U.begin());
+                                if (j >= kb && j < ke) Wg[(j - kb) * kGroup + r] = vals[segs[cs].val_off + e];
                             }
                         }
                         R.out_off = (int64_t)outrow.size();
@@ -2061,6 +2140,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                 (rc = up((void**)&D->r_p2_list, p2_list.data(), p2_list.size() * 4)))
                 return rc;
             D->res_ok = !getenv("VF_NO_RESIDENT");
+            D->res_split = split;
             D->res_grid = nsm;
             D->res_wcap = (int)std::max<int64_t>(wmax, EPL);
             D->res_scap = (int)std::max<int64_t>(smax, 4);
@@ -2335,13 +2415,14 @@ int launch_res(Handle* h, HotArgs& a, cudaStream_t st) {
     DeviceHMat* D = h->dev;
     auto fn = res_kernel<T, MODE>;
     const size_t smem = (size_t)D->res_wcap * sizeof(T) + (size_t)D->res_scap * 4 + (size_t)kRS * kKS * 16 * sizeof(T) +
-                        (size_t)a.kp * 8 + 256 * 8 + (size_t)kRW * 4 * 32 * 2 * 8;
+                        (size_t)a.kp * 8 + 256 * 8 + (size_t)kRW * 4 * 32 * 2 * 8 + 2 * 256 * 8;
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kRW * 32, smem));
     if (per_sm < 1) return set_error(VF_ECUDA, "resident kernel cannot be resident");
     ResArgs r{D->r_groups, D->r_outrow, D->r_wblob, D->r_cta_woff, D->r_sblob, D->r_cta_soff,
-              D->r_p1_ptr, D->r_p1_list, D->r_p2_ptr, D->r_p2_list, D->res_wcap, D->res_scap};
+              D->r_p1_ptr, D->r_p1_list, D->r_p2_ptr, D->r_p2_list, D->res_wcap, D->res_scap,
+              D->res_split ? 1 : 0};
     const int grid = D->res_grid;
     static const char* trace_file = getenv("VF_TRACE_FILE");
     unsigned long long* tbuf = nullptr;
@@ -2356,7 +2437,29 @@ int launch_res(Handle* h, HotArgs& a, cudaStream_t st) {
     if (MODE != M_STEP) CK(cudaMemsetAsync(a.ctl, 0, offsetof(Ctl, bar_gen), st));
     {
         Timer tm(h, st, 2);
-        CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kRW * 32), args, smem, st));
+        if (r.split) {
+            // cluster pairs (K-split groups exchange partial tiles through DSMEM).  The
+            // software grid barrier needs every CTA resident: check that all pairs fit.
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(grid);
+            cfg.blockDim = dim3(kRW * 32);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            int nclusters = 0;
+            CK(cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg));
+            if (nclusters * 2 < grid) {                // not all pairs co-resident: use the streaming path
+                D->res_ok = false;
+                return 1;
+            }
+            CK(cudaLaunchKernelEx(&cfg, fn, a, r));
+        } else {
+            CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(kRW * 32), args, smem, st));
+        }
     }
     h->launches_total++;
     D->last_grid = grid;
@@ -2381,8 +2484,11 @@ int launch_hot(Handle* h, HotArgs& a, cudaStream_t st) {
     const int kp = a.kp;
     if (kp >= 16 && kp % 16 == 0 && h->dev->res_ok &&
         (size_t)h->dev->res_wcap * sizeof(T) + (size_t)h->dev->res_scap * 4 + (size_t)kRS * kKS * 16 * sizeof(T) +
-                (size_t)kp * 8 + 2048 + (size_t)kRW * 4 * 32 * 2 * 8 <= (size_t)232448)
-        return launch_res<T, MODE>(h, a, st);
+                (size_t)kp * 8 + 2048 + (size_t)kRW * 4 * 32 * 2 * 8 + 4096 <= (size_t)232448)
+    {
+        const int rc = launch_res<T, MODE>(h, a, st);
+        if (rc != 1) return rc;                       // 1: resident layout unusable here, fall through
+    }
     if (kp == 1) return launch_hot_t<T, 1, 1, MODE, false>(h, a, st);
     if (kp == 2) return launch_hot_t<T, 1, 2, MODE, false>(h, a, st);
     if (kp == 4) return launch_hot_t<T, 1, 2, MODE, true>(h, a, st);

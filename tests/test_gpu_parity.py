@@ -307,12 +307,15 @@ def cfg2_small():
     return V, F, S, S.F_dense()
 
 
+@pytest.mark.parametrize("split", ["1", "0"])
 @pytest.mark.parametrize("k", [16, 64, 130])
-def test_resident_and_streaming_batched_paths(cfg2_small, rough, tmp_path_factory, k, monkeypatch):
+def test_resident_and_streaming_batched_paths(cfg2_small, rough, tmp_path_factory, k, split, monkeypatch):
     """nrhs >= 9 runs the shared-memory-resident kernel (res_kernel) when the
     layout fits; VF_NO_RESIDENT forces the streaming grouped kernel.  Both must
     match the oracle's Alg. 5 on the same blocks (matvec) and its Jacobi solve
-    (identical iteration counts)."""
+    (identical iteration counts).  split = 1: long groups are split over
+    cluster pairs (DSMEM exchange of partial tiles); 0: one CTA per group."""
+    monkeypatch.setenv("VF_RES_SPLIT", split)
     for which in ("cfg2", "rough"):
         V, F, S, Fd = cfg2_small if which == "cfg2" else rough
         H = hm.compress(S.x, Fd, 1e-6, min_size=2048)
