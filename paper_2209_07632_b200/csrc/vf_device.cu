@@ -1991,10 +1991,12 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             x.K += (int64_t)x.ucols.size();
             hg.push_back(std::move(x));
         }
-        // phase-2 groups with a long K are split over the two CTAs of a cluster
-        // pair (K halves; rank 1 sends its partial tile to rank 0): the largest
-        // per-SM FP64 work item halves.  VF_RES_SPLIT=0 disables.
-        const bool split = (nsm % 2 == 0) && (!getenv("VF_RES_SPLIT") || atoi(getenv("VF_RES_SPLIT")) != 0);
+        // phase-2 groups with a long K can be split over the two CTAs of a cluster
+        // pair (K halves; rank 1 sends its partial tile to rank 0 through DSMEM).
+        // Opt-in (VF_RES_SPLIT=1): with about as many groups as SMs (cfg2: 125 on
+        // 148) the halves only double the items per CTA -- measured 35 vs 25 us
+        // per iteration -- so it pays only when SMs would otherwise idle.
+        const bool split = (nsm % 2 == 0) && getenv("VF_RES_SPLIT") && atoi(getenv("VF_RES_SPLIT")) != 0;
         if (split) {
             std::vector<HG> out;
             for (auto& x : hg) {
