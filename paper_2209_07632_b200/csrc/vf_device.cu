@@ -928,7 +928,9 @@ __device__ __forceinline__ void res_stage(const int32_t* S, int j0, int n, const
     for (int op = threadIdx.x; op < n * OPS; op += kRW * 32) {
         const int j = op / OPS, part = op - j * OPS;
         const int64_t row = S[j0 + j];
-        cpa<16>(Xs + j * 16 + part * EPL, xc + row * kp + cb + part * EPL, 16);
+        // column c of staged row j lives at j*16 + (c ^ 4 (j & 3)): the DMMA fragment
+        // loads (4 k-rows x 8 columns per half-warp phase) hit 16 distinct bank pairs
+        cpa<16>(Xs + j * 16 + ((part * EPL) ^ (4 * (j & 3))), xc + row * kp + cb + part * EPL, 16);
     }
 }
 
@@ -1031,8 +1033,9 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
             for (int kb = warp * 4; kb < n; kb += 4 * kRW) {
                 const int j = kb + kr;
                 const bool ok = j < n;
-                const double a0 = ok ? wb[j * 16 + mn] : 0.0, a1 = ok ? wb[j * 16 + 8 + mn] : 0.0;
-                const double b0 = ok ? X[j * 16 + mn] : 0.0, b1 = ok ? X[j * 16 + 8 + mn] : 0.0;
+                const int sw = 4 * kr;                      // (j & 3) == kr: swizzled columns
+                const double a0 = ok ? wb[j * 16 + (mn ^ sw)] : 0.0, a1 = ok ? wb[j * 16 + ((8 + mn) ^ sw)] : 0.0;
+                const double b0 = ok ? X[j * 16 + (mn ^ sw)] : 0.0, b1 = ok ? X[j * 16 + ((8 + mn) ^ sw)] : 0.0;
                 dmma884(dacc[0], a0, b0);
                 dmma884(dacc[1], a0, b1);
                 dmma884(dacc[2], a1, b0);
@@ -1040,14 +1043,18 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
             }
         } else if (rr < G.nrows) {
             // 8 independent smem load pairs in flight per thread
-            const T* w = W + G.w_off + (int64_t)j0 * 16 + rr;
-            const T* x = X + cc;
+            const T* w = W + G.w_off + (int64_t)j0 * 16;
+            const T* x = X;
             T a2 = T(0), a3 = T(0);
             int j = 0;
             for (; j + 7 < n; j += 8) {
                 T wv[8], xv[8];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) { wv[u] = w[(j + u) * 16]; xv[u] = x[(j + u) * 16]; }
+                for (int u = 0; u < 8; ++u) {
+                    const int sw = 4 * ((j + u) & 3);
+                    wv[u] = w[(j + u) * 16 + (rr ^ sw)];
+                    xv[u] = x[(j + u) * 16 + (cc ^ sw)];
+                }
                 acc0 = fma(wv[0], xv[0], acc0);
                 acc1 = fma(wv[1], xv[1], acc1);
                 a2 = fma(wv[2], xv[2], a2);
@@ -1057,7 +1064,7 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
                 a2 = fma(wv[6], xv[6], a2);
                 a3 = fma(wv[7], xv[7], a3);
             }
-            for (; j < n; ++j) acc0 = fma(w[j * 16], x[j * 16], acc0);
+            for (; j < n; ++j) acc0 = fma(w[j * 16 + (rr ^ (4 * (j & 3)))], x[j * 16 + (cc ^ (4 * (j & 3)))], acc0);
             acc0 += a2;
             acc1 += a3;
         }
@@ -2096,7 +2103,8 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                                 if (j < kb || j >= ke) continue;
                                 sblob.push_back((int32_t)(sg.kind ? idx[sg.src + e] : sg.src + e));
                                 for (int r = 0; r < G.nrows; ++r)
-                                    Wg[(j - kb) * kGroup + r] = vals[gvov[(G.seg_off + sgi) * kGroup + r] + e];
+                                    Wg[(j - kb) * kGroup + (r ^ (4 * ((j - kb) & 3)))] =
+                                        vals[gvov[(G.seg_off + sgi) * kGroup + r] + e];
                             }
                             j0 += sg.len;
                         }
@@ -2109,7 +2117,8 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                             for (int32_t e = 0; e < segs[cs].len; ++e) {
                                 const int32_t col = idx[segs[cs].src + e];
                                 const int64_t j = j0 + (std::lower_bound(U.begin(), U.end(), col) - U.begin());
-                                if (j >= kb && j < ke) Wg[(j - kb) * kGroup + r] = vals[segs[cs].val_off + e];
+                                if (j >= kb && j < ke)
+                                    Wg[(j - kb) * kGroup + (r ^ (4 * ((j - kb) & 3)))] = vals[segs[cs].val_off + e];
                             }
                         }
                         R.out_off = (int64_t)outrow.size();
