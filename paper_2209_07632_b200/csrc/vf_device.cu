@@ -514,6 +514,13 @@ struct HotArgs {
     // nrhs = 1 matvec without the phase barrier: per-SVD-block counters of
     // finished T rows, the SVD block of every segment (-1: X source) and of every
     // phase-1 group, and a dynamic queue over the phase-2 rows (LPT order)
+    const int32_t* pp_group;      // nrhs = 1 phase-1 parts: group, first V row, length,
+    const int32_t* pp_begin;      // index of the part within its group, parts of the group
+    const int32_t* pp_len;
+    const int32_t* pp_idx;
+    const int32_t* pp_n;
+    int32_t* pp_cnt;              // per group: parts finished (cumulative over launches)
+    double* pp_scratch;           // [part][kGroup] partial sums (part-major, group parts contiguous)
     int32_t* tready;
     const int32_t* seg_blk;
     const int32_t* g1_blk;
@@ -565,11 +572,14 @@ template <typename T>
 __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_t gwarp, int lane) {
     const T* vals = static_cast<const T*>(a.vals);
     for (int32_t q = a.s1_ptr[gwarp]; q < a.s1_ptr[gwarp + 1]; ++q) {
-        const int64_t gi = a.s1_items[q];
+        const int64_t pi = a.s1_items[q];                 // part item
+        const int64_t gi = a.pp_group[pi];
+        const int j0 = a.pp_begin[pi], jn = j0 + a.pp_len[pi];
+        const int np = a.pp_n[pi];
         const Group G = a.g1[gi];
         const GSeg sg = a.gseg[G.seg_off];
         constexpr int H = kGroup / 2;                 // rows per pass (register budget)
-        T mine = T(0);
+        double mine = 0.0;
         for (int h0 = 0; h0 < G.nrows; h0 += H) {
             int32_t vo[H];                            // value offsets (< 2^31 elements)
 #pragma unroll
@@ -577,7 +587,7 @@ __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_
             T acc[H];
 #pragma unroll
             for (int r = 0; r < H; ++r) acc[r] = T(0);
-            for (int j = lane; j < sg.len; j += 32) {
+            for (int j = j0 + lane; j < jn; j += 32) {
                 const int64_t row = sg.kind ? (int64_t)__ldg(a.idx + sg.src + j) : sg.src + j;
                 const T x = __ldcg(xc + row);
                 T v[H];
@@ -590,14 +600,30 @@ __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_
             for (int r = 0; r < H; ++r) {
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], off);
-                if (lane == h0 + r) mine = acc[r];
+                if (lane == h0 + r) mine = (double)acc[r];
             }
         }
-        if (lane < G.nrows) {
-            const int64_t t = a.grow1[gi * kGroup + lane];
-            xc[a.N + t] = static_cast<const T*>(a.p1_scale)[t] * mine;
+        bool finish = np == 1;
+        if (!finish) {                                // publish this part; the last one combines
+            const int64_t base = (pi - a.pp_idx[pi]) * kGroup;   // part 0 of the group
+            if (lane < G.nrows) a.pp_scratch[base + (int64_t)a.pp_idx[pi] * kGroup + lane] = mine;
+            __threadfence();
+            __syncwarp();
+            int last = 0;
+            if (lane == 0) last = (atomicAdd(a.pp_cnt + gi, 1) + 1) % np == 0;
+            finish = __shfl_sync(0xffffffffu, last, 0);
+            if (finish) {
+                __threadfence();
+                mine = 0.0;
+                if (lane < G.nrows)
+                    for (int pp = 0; pp < np; ++pp) mine += __ldcg(a.pp_scratch + base + (int64_t)pp * kGroup + lane);
+            }
         }
-        if (a.tready) {                               // publish: these T rows of block b are final
+        if (finish && lane < G.nrows) {
+            const int64_t t = a.grow1[gi * kGroup + lane];
+            xc[a.N + t] = static_cast<const T*>(a.p1_scale)[t] * (T)mine;
+        }
+        if (finish && a.tready) {                     // publish: these T rows of block b are final
             __threadfence();
             __syncwarp();
             if (lane == 0) atomicAdd(a.tready + a.g1_blk[gi], G.nrows);
@@ -1619,7 +1645,12 @@ struct DeviceHMat {
     int device = 0;
     int last_grid = 0;
     // work-item costs (terms per unit) for the static LPT schedules
-    std::vector<int64_t> cost_p1, cost_p2, cost_g1, cost_g2;
+    std::vector<int64_t> cost_p1, cost_p2, cost_g1, cost_g2, cost_p1parts;
+    // nrhs = 1 phase 1: items (group, part of its V rows) -- long V columns are
+    // split over warps; part sums meet in scratch, the last part combines them
+    int32_t *pp_group = nullptr, *pp_begin = nullptr, *pp_len = nullptr, *pp_idx = nullptr, *pp_n = nullptr;
+    int32_t* pp_cnt = nullptr;
+    double* pp_scratch = nullptr;
     struct Sched { int32_t* ptr = nullptr; int32_t* items = nullptr; };
     std::map<std::array<int64_t, 4>, Sched> sched;
     // barrier-free nrhs = 1 matvec (tready[n_svd] = the dynamic queue counter)
@@ -1909,6 +1940,22 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         }
         return c + mx;
     };
+    // nrhs = 1 phase-1 parts: V rows of a group in pieces of <= kPart (the
+    // warp streams nrows x part values); costs for the LPT schedule
+    std::vector<int32_t> pp_group, pp_begin, pp_len, pp_idx, pp_n;
+    {
+        constexpr int kPart = 2048;
+        for (int64_t g = 0; g < (int64_t)g1v.size(); ++g) {
+            const int len = gsegv[g1v[g].seg_off].len;
+            const int np = std::max(1, (len + kPart - 1) / kPart);
+            for (int p = 0; p < np; ++p) {
+                const int b = (int)((int64_t)len * p / np), e = (int)((int64_t)len * (p + 1) / np);
+                pp_group.push_back((int32_t)g); pp_begin.push_back(b); pp_len.push_back(e - b);
+                pp_idx.push_back(p); pp_n.push_back(np);
+                D->cost_p1parts.push_back(16 + (int64_t)g1v[g].nrows * (e - b));
+            }
+        }
+    }
     // phase-1 groups: bytes scale with rows x |J_b| (the nrhs = 1 warp streams all of them)
     for (int64_t g = 0; g < D->n_g1; ++g)
         D->cost_g1.push_back(16 + (int64_t)g1v[g].nrows * gsegv[g1v[g].seg_off].len);
@@ -1953,6 +2000,19 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         if ((rc = up((void**)&D->bounds, h->row_bounds.data(), h->row_bounds.size() * 8))) return rc;
     }
     if ((rc = up((void**)&D->active, active.data(), active.size()))) return rc;
+    {
+        const size_t npp = std::max<size_t>(pp_group.size(), 1);
+        if (pp_group.empty()) { pp_group.push_back(0); pp_begin.push_back(0); pp_len.push_back(0); pp_idx.push_back(0); pp_n.push_back(1); }
+        if ((rc = up((void**)&D->pp_group, pp_group.data(), npp * 4)) ||
+            (rc = up((void**)&D->pp_begin, pp_begin.data(), npp * 4)) ||
+            (rc = up((void**)&D->pp_len, pp_len.data(), npp * 4)) ||
+            (rc = up((void**)&D->pp_idx, pp_idx.data(), npp * 4)) ||
+            (rc = up((void**)&D->pp_n, pp_n.data(), npp * 4)) ||
+            (rc = up((void**)&D->pp_scratch, nullptr, npp * kGroup * 8)))
+            return rc;
+        std::vector<int32_t> zero(std::max<size_t>(g1v.size(), 1), 0);
+        if ((rc = up((void**)&D->pp_cnt, zero.data(), zero.size() * 4))) return rc;
+    }
     {   // barrier-free nrhs = 1 matvec: block flags, segment/group blocks, LPT row order
         if (g1_blk.empty()) g1_blk.push_back(0);
         std::vector<int32_t> order(D->cost_p2.size());
@@ -2328,7 +2388,9 @@ int get_sched(DeviceHMat* D, int phase, bool grouped, int nchunk, int nworkers, 
     std::array<int64_t, 4> key{phase, grouped ? 1 : 0, nchunk, nworkers};
     auto it = D->sched.find(key);
     if (it != D->sched.end()) { *out = it->second; return VF_OK; }
-    const std::vector<int64_t>& cu = grouped ? (phase == 1 ? D->cost_g1 : D->cost_g2) : (phase == 1 ? D->cost_p1 : D->cost_p2);
+    const std::vector<int64_t>& cu = phase == 3 ? D->cost_p1parts
+                                     : grouped ? (phase == 1 ? D->cost_g1 : D->cost_g2)
+                                               : (phase == 1 ? D->cost_p1 : D->cost_p2);
     const int64_t nitems = (int64_t)cu.size() * nchunk;
     if (nitems >= INT32_MAX) return set_error(VF_EUNSUPPORTED, "too many work items");
     std::vector<int32_t> order(nitems);
@@ -2383,7 +2445,7 @@ int launch_hot_t(Handle* h, HotArgs& a, cudaStream_t st) {
     int rc;
     // nrhs = 1: phase 1 runs per row group (phase1_groups_k1), one warp per group
     const bool g1k1 = !GROUPED && KC == 1 && VEC == 1;
-    if ((rc = get_sched(D, 1, GROUPED || g1k1, g1k1 ? 1 : nchunk, nworkers, &s1)) ||
+    if ((rc = get_sched(D, g1k1 ? 3 : 1, GROUPED || g1k1, g1k1 ? 1 : nchunk, nworkers, &s1)) ||
         (rc = get_sched(D, 2, GROUPED, nchunk, nworkers, &s2)))
         return rc;
     a.s1_ptr = s1.ptr; a.s1_items = s1.items; a.s2_ptr = s2.ptr; a.s2_items = s2.items;
@@ -2530,6 +2592,8 @@ HotArgs hot_args(DeviceHMat* D, int kp, int k) {
     a.xt0 = D->xt[0]; a.xt1 = D->xt[1];
     a.partial = D->partial; a.enorm2 = D->enorm2; a.resid = D->resid; a.ctl = D->ctl;
     a.N = D->N; a.kp = kp; a.k = k;
+    a.pp_group = D->pp_group; a.pp_begin = D->pp_begin; a.pp_len = D->pp_len; a.pp_idx = D->pp_idx;
+    a.pp_n = D->pp_n; a.pp_cnt = D->pp_cnt; a.pp_scratch = D->pp_scratch;
     return a;
 }
 
@@ -2826,7 +2890,8 @@ void device_free(Handle* h) {
     DeviceHMat* D = h->dev;
     if (!D) return;
     cudaSetDevice(h->device);
-    void* ptrs[] = {D->tready, D->seg_blk, D->g1_blk, D->p2_order, D->r_groups, D->r_outrow, D->r_wblob, D->r_cta_woff, D->r_sblob, D->r_cta_soff,
+    void* ptrs[] = {D->pp_group, D->pp_begin, D->pp_len, D->pp_idx, D->pp_n, D->pp_cnt, D->pp_scratch,
+                    D->tready, D->seg_blk, D->g1_blk, D->p2_order, D->r_groups, D->r_outrow, D->r_wblob, D->r_cta_woff, D->r_sblob, D->r_cta_soff,
                     D->r_p1_ptr, D->r_p1_list, D->r_p2_ptr, D->r_p2_list, D->bounds, D->send, D->recv, D->vals, D->idx, D->segs, D->p1_segptr, D->p1_rows, D->p1_scale, D->p2_segptr, D->p2_rows,
                     D->perm, D->active, D->g1, D->g2, D->gseg, D->gvo, D->grow1, D->grow2, D->gcsr1, D->gcsr2,
                     D->xt[0], D->xt[1], D->Ep, D->Qp, D->Qdp, D->Qvp, D->Yp, D->Qip,
