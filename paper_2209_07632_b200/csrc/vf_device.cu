@@ -316,6 +316,9 @@ template <> struct V4<float> {
 #ifndef VF_XVEC
 #define VF_XVEC 1
 #endif
+#ifndef VF_CSRVEC
+#define VF_CSRVEC 1
+#endif
 // read-only X gathers: through L1 with the default load, or the non-coherent
 // texture path (VF_X_LDG=1); X is not written during the launches that use it
 #if defined(VF_X_LDG) && VF_X_LDG
@@ -399,6 +402,9 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
                     if (g_kind) {
                         const int4 q = __ldg(reinterpret_cast<const int4*>(idx + g_src + e));
                         xr[c][0] = q.x; xr[c][1] = q.y; xr[c][2] = q.z; xr[c][3] = q.w;
+                        // sorted CSR columns often run consecutively (tree order keeps
+                        // near-field neighbours together): one aligned vector load then
+                        vx[c] = VF_XVEC && VF_CSRVEC && e + 3 < g_len && q.w - q.x == 3 && (q.x & (16 / sizeof(T) - 1)) == 0;
                     } else {
 #pragma unroll
                         for (int u = 0; u < 4; ++u) xr[c][u] = (int32_t)(g_src + e + u);

@@ -26,6 +26,10 @@ KEYS = [
     ("l1tex__t_sector_hit_rate.pct", "L1 sector hit rate %"),
     ("lts__t_sector_hit_rate.pct", "L2 sector hit rate %"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "FP64 pipe active %"),
+    ("sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active", "FP64 (DFMA) inst % of peak"),
+    ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "DMMA tensor subpipe inst % of peak"),
+    ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+     "tensor pipe active % (elapsed)"),
 ]
 
 
