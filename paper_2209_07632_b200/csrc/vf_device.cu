@@ -317,7 +317,7 @@ template <> struct V4<float> {
 #define VF_XVEC 1
 #endif
 #ifndef VF_CSRVEC
-#define VF_CSRVEC 1
+#define VF_CSRVEC 0   // measured slower (60.1 vs 62.3 % on cfg3)
 #endif
 // read-only X gathers: through L1 with the default load, or the non-coherent
 // texture path (VF_X_LDG=1); X is not written during the launches that use it
