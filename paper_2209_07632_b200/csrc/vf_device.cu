@@ -992,10 +992,10 @@ struct ResCursor {
 template <typename T, int PHASE, int MODE>
 __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, const T* W, const int32_t* S, T* Xs,
                                           T* xc, T* xn, double* sred, double* tile, double* red, double* xch,
-                                          int& xpar) {
-    const int32_t* ptr = PHASE == 1 ? r.p1_ptr : r.p2_ptr;
-    const int32_t* lst = PHASE == 1 ? r.p1_list : r.p2_list;
-    const int g0 = ptr[blockIdx.x], g1 = ptr[blockIdx.x + 1];
+                                          int& xpar, const RGroup* gs1, int ng1, const RGroup* gs2, int ng2) {
+    // this CTA's group descriptors of the phase, cached in smem at launch (GS[0 .. g1))
+    const RGroup* GS = PHASE == 1 ? gs1 : gs2;
+    const int g0 = 0, g1 = PHASE == 1 ? ng1 : ng2;
     if (g0 == g1) return;
     const int nchunk = a.kp / 16;
     const int t = threadIdx.x, rr = t >> 4, cc = t & 15;
@@ -1003,21 +1003,21 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
     // steps = (group, 16-column chunk, K slice) in order
     int total = 0;
     for (int g = g0; g < g1; ++g) {
-        const RGroup& Gq = r.groups[lst[g]];
+        const RGroup& Gq = GS[g];
         const int nch_g = Gq.ch0 < nchunk ? (nchunk - Gq.ch0 + Gq.chstep - 1) / Gq.chstep : 0;
         total += nch_g * ((Gq.K + kKS - 1) / kKS);
     }
     if (total == 0) return;
     // first group with a chunk of its own (a copy may own none for small kp)
     int gs = g0;
-    while (r.groups[lst[gs]].ch0 >= nchunk) ++gs;
+    while (GS[gs].ch0 >= nchunk) ++gs;
     auto advance = [&](ResCursor& c) {
         if (++c.sl * kKS < c.G.K) return;
         c.sl = 0;
         c.ch += c.G.chstep;
         if (c.ch < nchunk) return;
         while (++c.g < g1) {
-            c.G = r.groups[lst[c.g]];
+            c.G = GS[c.g];
             c.ch = c.G.ch0;
             if (c.ch < nchunk) return;
         }
@@ -1026,7 +1026,7 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
         const int j0 = c.sl * kKS;
         res_stage<T>(S + c.G.s_off, j0, min(kKS, c.G.K - j0), xc, kp, c.ch * 16, dst);
     };
-    ResCursor cur{gs, r.groups[lst[gs]].ch0, 0, r.groups[lst[gs]]};
+    ResCursor cur{gs, GS[gs].ch0, 0, GS[gs]};
     ResCursor nxt = cur;
 #pragma unroll
     for (int p = 0; p < kRS - 1; ++p) {                // prologue: kRS - 1 slices in flight
@@ -1132,7 +1132,7 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
             if (rr < G.nrows && G.role != 1) {
                 const int64_t orow = __ldg(r.outrow + G.out_off + rr);
                 if (PHASE == 1) {
-                    xc[(a.N + orow) * kp + col] = static_cast<const T*>(a.p1_scale)[orow] * q;
+                    xc[(a.N + orow) * kp + col] = q;                                    // S_t is in the weights
                 } else if (MODE == M_MATVEC) {
                     static_cast<T*>(a.Y)[orow * kp + col] = q;
                 } else {
@@ -1173,6 +1173,12 @@ __global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) 
     double* red = tile + 256;                          // [kRW warps][4 tiles][32 lanes][2] DMMA partials
     double* xch = red + kRW * 4 * 32 * 2;              // [2][256] partner tiles (DSMEM, cluster pairs)
     int xpar = 0;
+    RGroup* gs1 = reinterpret_cast<RGroup*>(xch + 2 * 256);   // this CTA's descriptors (phase 1, then 2)
+    const int ng1 = r.p1_ptr[blockIdx.x + 1] - r.p1_ptr[blockIdx.x];
+    const int ng2 = r.p2_ptr[blockIdx.x + 1] - r.p2_ptr[blockIdx.x];
+    RGroup* gs2 = gs1 + ng1;
+    for (int q = threadIdx.x; q < ng1; q += blockDim.x) gs1[q] = r.groups[r.p1_list[r.p1_ptr[blockIdx.x] + q]];
+    for (int q = threadIdx.x; q < ng2; q += blockDim.x) gs2[q] = r.groups[r.p2_list[r.p2_ptr[blockIdx.x] + q]];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const unsigned nblk = gridDim.x;
     {   // this CTA's F-hat values and source-row lists -> smem, once per launch
@@ -1199,12 +1205,12 @@ __global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) 
         T* xc = static_cast<T*>(cur ? a.xt1 : a.xt0);
         T* xn = static_cast<T*>(cur ? a.xt0 : a.xt1);
         trace_ev(a, it, 0);
-        if (have_p1) res_phase<T, 1, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red, xch, xpar);
+        if (have_p1) res_phase<T, 1, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red, xch, xpar, gs1, ng1, gs2, ng2);
         trace_ev(a, it, 1);
         if (MODE == M_MATVEC) {
             if (have_p1 && !a.tready) grid_sync(a.ctl, nblk);   // nrhs = 1: per-block T flags instead
             trace_ev(a, it, 2);
-            res_phase<T, 2, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red, xch, xpar);
+            res_phase<T, 2, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red, xch, xpar, gs1, ng1, gs2, ng2);
             trace_ev(a, it, 3);
             return;
         }
@@ -1219,7 +1225,7 @@ __global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) 
         }
         for (int c = threadIdx.x; c < a.kp; c += blockDim.x) sred[c] = 0.0;
         __syncthreads();
-        res_phase<T, 2, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red, xch, xpar);
+        res_phase<T, 2, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red, xch, xpar, gs1, ng1, gs2, ng2);
         __syncthreads();
         double* part = a.partial + (MODE == M_STEP ? 0 : (int64_t)(it & 1) * nblk * a.kp);   // [kp][nblk]
         for (int c = threadIdx.x; c < a.kp; c += blockDim.x) part[(int64_t)c * nblk + blockIdx.x] = sred[c];
@@ -1666,6 +1672,7 @@ struct DeviceHMat {
     bool res_ok = false;
     int res_grid = 0, res_wcap = 0, res_scap = 0;
     bool res_split = false;
+    int res_gmax = 0;                            // max groups (phase 1 + 2) of one CTA
     RGroup* r_groups = nullptr;
     int32_t *r_outrow = nullptr, *r_sblob = nullptr;
     void* r_wblob = nullptr;
@@ -2087,7 +2094,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             hg.swap(out);
         }
         const int64_t fixed = (int64_t)kRS * kKS * 16 * (int64_t)sizeof(T) + 256 * 8 + (int64_t)kMaxKp * 8 + 256 +
-                              (int64_t)kRW * 4 * 32 * 2 * 8 + 2 * 256 * 8;
+                              (int64_t)kRW * 4 * 32 * 2 * 8 + 2 * 256 * 8 + 64 * (int64_t)sizeof(RGroup);
         const int64_t budget = smem_optin - fixed;                 // bytes for values + source rows
         auto need = [&](const HG& x) { return (x.K * kGroup + EPL) * (int64_t)sizeof(T) + (x.K + 4) * 4; };
         bool ok = budget > 0 && !hg.empty();
@@ -2168,9 +2175,10 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                                 const int64_t j = j0 + e;
                                 if (j < kb || j >= ke) continue;
                                 sblob.push_back((int32_t)(sg.kind ? idx[sg.src + e] : sg.src + e));
-                                for (int r = 0; r < G.nrows; ++r)
+                                for (int r = 0; r < G.nrows; ++r)   // phase 1: S_t folded into V's column t
                                     Wg[(j - kb) * kGroup + (r ^ (4 * ((j - kb) & 3)))] =
-                                        vals[gvov[(G.seg_off + sgi) * kGroup + r] + e];
+                                        vals[gvov[(G.seg_off + sgi) * kGroup + r] + e] *
+                                        (ph == 1 ? p1_scale[grow1v[g * kGroup + r]] : T(1));
                             }
                             j0 += sg.len;
                         }
@@ -2218,6 +2226,8 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                 return rc;
             D->res_ok = !getenv("VF_NO_RESIDENT");
             D->res_split = split;
+            for (int c = 0; c < nsm; ++c)
+                D->res_gmax = std::max(D->res_gmax, (p1_ptr[c + 1] - p1_ptr[c]) + (p2_ptr[c + 1] - p2_ptr[c]));
             D->res_grid = nsm;
             D->res_wcap = (int)std::max<int64_t>(wmax, EPL);
             D->res_scap = (int)std::max<int64_t>(smax, 4);
@@ -2494,7 +2504,8 @@ int launch_res(Handle* h, HotArgs& a, cudaStream_t st) {
     DeviceHMat* D = h->dev;
     auto fn = res_kernel<T, MODE>;
     const size_t smem = (size_t)D->res_wcap * sizeof(T) + (size_t)D->res_scap * 4 + (size_t)kRS * kKS * 16 * sizeof(T) +
-                        (size_t)a.kp * 8 + 256 * 8 + (size_t)kRW * 4 * 32 * 2 * 8 + 2 * 256 * 8;
+                        (size_t)a.kp * 8 + 256 * 8 + (size_t)kRW * 4 * 32 * 2 * 8 + 2 * 256 * 8 +
+                        (size_t)D->res_gmax * sizeof(RGroup);
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kRW * 32, smem));
@@ -2563,7 +2574,8 @@ int launch_hot(Handle* h, HotArgs& a, cudaStream_t st) {
     const int kp = a.kp;
     if (kp >= 16 && kp % 16 == 0 && h->dev->res_ok &&
         (size_t)h->dev->res_wcap * sizeof(T) + (size_t)h->dev->res_scap * 4 + (size_t)kRS * kKS * 16 * sizeof(T) +
-                (size_t)kp * 8 + 2048 + (size_t)kRW * 4 * 32 * 2 * 8 + 4096 <= (size_t)232448)
+                (size_t)kp * 8 + 2048 + (size_t)kRW * 4 * 32 * 2 * 8 + 4096 +
+                (size_t)h->dev->res_gmax * sizeof(RGroup) <= (size_t)232448)
     {
         const int rc = launch_res<T, MODE>(h, a, st);
         if (rc != 1) return rc;                       // 1: resident layout unusable here, fall through
