@@ -313,6 +313,9 @@ template <> struct V4<float> {
 #ifndef VF_K1_CH
 #define VF_K1_CH 1
 #endif
+#ifndef VF_K1_CH_F32
+#define VF_K1_CH_F32 2
+#endif
 #ifndef VF_XVEC
 #define VF_XVEC 1
 #endif
@@ -350,7 +353,9 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
                                                const T* __restrict__ vals, const int32_t* __restrict__ idx,
                                                const T* xt, int lane, int64_t nx,
                                                const int32_t* tready = nullptr, const int32_t* seg_blk = nullptr) {
-    constexpr int CH = VF_K1_CH;                 // chunks of 4 terms in flight per lane
+    // chunks of 4 terms in flight per lane: FP32 chunks carry 2/3 of the bytes
+    // of FP64 ones, so two are in flight there (VF_K1_CH_F32)
+    constexpr int CH = sizeof(T) == 4 ? VF_K1_CH_F32 : VF_K1_CH;
     constexpr unsigned FULL = 0xffffffffu;
     T acc0 = T(0), acc1 = T(0);
     for (int64_t sb = s0; sb < s1; sb += 32) {
