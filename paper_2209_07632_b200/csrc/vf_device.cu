@@ -2772,6 +2772,13 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     // optional (VF_MV_FLAGS=1): phase 1 -> phase 2 by per-block flags and a dynamic
     // row queue instead of the grid barrier.  Measured slower on cfg3-shaped
     // F-hat (flag spinning + queue atomics > barrier wait), so off by default.
+    // nrhs = 1 matvec: phase-2 rows from a global LPT-ordered queue (dynamic
+    // balance: the static schedule left a ~10 % tail on cfg3); VF_MV_STATIC=1
+    // restores the static schedule.  Each row is summed identically either way.
+    if (kp == 1 && !getenv("VF_MV_STATIC") && !getenv("VF_MV_FLAGS")) {
+        CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
+        a.qctr = D->tready + D->n_svd; a.p2_order = D->p2_order;
+    }
     if (kp == 1 && getenv("VF_MV_FLAGS") && !getenv("VF_MV_BARRIER")) {
         CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
         a.tready = D->tready; a.seg_blk = D->seg_blk; a.g1_blk = D->g1_blk;

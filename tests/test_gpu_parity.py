@@ -354,15 +354,17 @@ def test_k1_matvec_flags_equal_barrier_bitwise(rough, tmp_path_factory, monkeypa
     hm.write_hvfm(H, p)
     X = sg.random_rhs(S.N, 1, seed=9)
     out = []
-    for barrier in (False, True):
-        if barrier:
-            monkeypatch.delenv("VF_MV_FLAGS", raising=False)
-        else:
+    for mode in ("flags", "queue", "static"):     # flags+queue / queue+barrier (default) / static+barrier
+        monkeypatch.delenv("VF_MV_FLAGS", raising=False)
+        monkeypatch.delenv("VF_MV_STATIC", raising=False)
+        if mode == "flags":
             monkeypatch.setenv("VF_MV_FLAGS", "1")
+        elif mode == "static":
+            monkeypatch.setenv("VF_MV_STATIC", "1")
         M = vf.ViewFactorMatrix.load(p, device=0)
         Y = empty(S.N, 1)
         for _ in range(3):                       # repeated launches reset the flags and the queue
             M.matvec(dev(X), Y)
         out.append(host(Y))
-    assert np.array_equal(out[0], out[1])
+    assert np.array_equal(out[0], out[1]) and np.array_equal(out[1], out[2])
     assert rel(out[0], hm.hmatvec(H, X)) <= 1e-12
