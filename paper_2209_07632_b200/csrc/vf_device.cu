@@ -316,6 +316,7 @@ template <> struct V4<float> {
 #ifndef VF_K1_CH_F32
 #define VF_K1_CH_F32 2
 #endif
+
 #ifndef VF_XVEC
 #define VF_XVEC 1
 #endif
@@ -579,6 +580,10 @@ __device__ __forceinline__ void solve_epilogue(const HotArgs& a, const T* xc, T*
 // multiplied into the group's kGroup accumulators, whose V values are
 // contiguous per t (coalesced across lanes); kGroup + 1 independent loads per
 // lane and step keep HBM busy.  Fixed-order xor reductions, one store per t.
+#ifndef VF_P1_UNROLL
+#define VF_P1_UNROLL 1
+#endif
+constexpr int kP1Unroll = VF_P1_UNROLL;
 template <typename T>
 __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_t gwarp, int lane) {
     const T* vals = static_cast<const T*>(a.vals);
@@ -598,6 +603,7 @@ __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_
             T acc[H];
 #pragma unroll
             for (int r = 0; r < H; ++r) acc[r] = T(0);
+#pragma unroll kP1Unroll
             for (int j = j0 + lane; j < jn; j += 32) {
                 const int64_t row = sg.kind ? (int64_t)__ldg(a.idx + sg.src + j) : sg.src + j;
                 const T x = __ldcg(xc + row);
