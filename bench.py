@@ -74,17 +74,57 @@ def fp32_peak_tflops(sm_mhz):
 
 
 class Clocks:
-    """Samples nvidia-smi during the timed region (the recipe's clocks line)."""
+    """Samples SM clocks and clock-event (throttle) reasons DURING the timed
+    region (the recipe's clocks line). NVML is polled every ~5 ms from a
+    thread, with one synchronous sample at start() and one at stop(), so even a
+    timed region of a few tens of ms carries several samples; nvidia-smi -lms
+    100 is the fallback when NVML is unavailable."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    BITS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
     def __init__(self, index):
         self.index = index
         self.p = None
+        self.nv = None
         self.lines = []
+        self.samples = []
+        self.stop_ev = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = None
+            try:
+                import torch
+                uuid = str(torch.cuda.get_device_properties(index).uuid)
+                h = pynvml.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.nv, self.h = pynvml, h
+            self.smax = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+        except Exception:
+            self.nv = None
+
+    def _sample(self):
+        nv = self.nv
+        self.samples.append((float(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)),
+                             int(nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))))
+
+    def _poll(self):
+        while not self.stop_ev.wait(0.005):
+            try:
+                self._sample()
+            except Exception:
+                return
 
     def start(self):
+        if self.nv:
+            self._sample()
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            return
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
                                        "-i", str(self.index), "-lms", "100"], stdout=subprocess.PIPE,
@@ -99,6 +139,14 @@ class Clocks:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nv:
+            self.stop_ev.set()
+            self.t.join()
+            self._sample()
+            sm = [c for c, _ in self.samples]
+            reasons = {nm for nm, bit in self.BITS.items() for _, r in self.samples if r & bit}
+            return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.smax, "reasons": sorted(reasons),
+                    "samples": len(sm), "source": "NVML, ~5 ms poll over the timed region"}
         if not self.p:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.p.terminate()
@@ -107,7 +155,6 @@ class Clocks:
         except Exception:
             self.p.kill()
         sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9:
@@ -117,11 +164,11 @@ class Clocks:
                 smax.append(float(f[2]))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[5:9]):
+            for nm, v in zip(self.NAMES, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi -lms 100"}
 
 
 def workload(rank, world):
