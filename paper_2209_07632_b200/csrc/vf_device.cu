@@ -1965,10 +1965,11 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         return c + mx;
     };
     // nrhs = 1 phase-1 parts: V rows of a group in pieces of <= kPart (the
-    // warp streams nrows x part values); costs for the LPT schedule
+    // warp streams nrows x part values); costs for the LPT schedule.
+    // VF_P1_PART overrides the piece length (experiments)
     std::vector<int32_t> pp_group, pp_begin, pp_len, pp_idx, pp_n;
     {
-        constexpr int kPart = 2048;
+        static const int kPart = getenv("VF_P1_PART") ? std::max(64, atoi(getenv("VF_P1_PART"))) : 2048;
         for (int64_t g = 0; g < (int64_t)g1v.size(); ++g) {
             const int len = gsegv[g1v[g].seg_off].len;
             const int np = std::max(1, (len + kPart - 1) / kPart);
