@@ -32,6 +32,7 @@
 #include <cstring>
 #include <numeric>
 #include <type_traits>
+#include <memory>
 #include <vector>
 
 #include "vf_internal.h"
@@ -1774,12 +1775,14 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     D->p1_bytes = alg_bytes;
     D->p1_flops = alg_flops;
     {
-        std::vector<char> used(N, 0);
+        std::unique_ptr<uint8_t[]> used(new uint8_t[(size_t)N + 1]());
         for (int b : svd_ids) {
             const Leaf& L = h->leaves[b];
             for (int32_t j : L.idx_b) used[L.col0 + j] = 1;
         }
-        D->p1_src = std::count(used.begin(), used.end(), 1);
+        int64_t n_used = 0;
+        for (int64_t j = 0; j < N; ++j) n_used += used[j];
+        D->p1_src = n_used;
     }
 
     // ---- phase 2 rows: per tree row, its segments.  Values are packed ROW BY
