@@ -608,16 +608,22 @@ def run_terrain(args, rank, world, local_rank):
         n_app = applies / max(args.steps, 1)
         avg = ms_hot / max(l_hot, 1)
         kp = k if k <= 2 else (k + 15) // 16 * 16 if k > 8 else (4 if k <= 4 else 8)
+        # 2..8 columns on an F-hat above 256 MB run column by column through the
+        # nrhs = 1 kernel (libvf's rule in matvec_impl): one launch = one column
+        colsplit = not rows_mode and 2 <= k <= 8 and info["device_bytes"] > (256 << 20)
+        kl = 1 if colsplit else k
+        if colsplit:
+            kp = 1
         solve_rows = 4 if rows_mode else 1
         bytes_app = (info["p1_bytes"] + info["p2_bytes"] + (info["p1_src_rows"] + info["p2_src_rows"]) * kp * w
                      + info["t_rows"] * kp * w + info["active_rows"] * kp * w * solve_rows)
-        flops_app = info["alg_flops_per_col"] * k
+        flops_app = info["alg_flops_per_col"] * kl
         apps_launch = (n_app / max(l_hot / args.steps, 1)) if rows_mode else 1
         ach_gbs = bytes_app * apps_launch / (avg * 1e-3) / 1e9 if avg > 0 else 0.0
         hbm = pk.get("hbm_gbs", 6559.0)
         traffic, traffic_src = ncu_traffic(f"{args.workload}_k{k}_{dt}")
         ach_tf = flops_app * apps_launch / (avg * 1e-3) / 1e12 if avg > 0 else 0.0
-        if k > 2:
+        if kl > 2:
             # batched: arithmetic intensity above the ridge -> FP64/FP32 FMA bound
             # (the wide per-row kernel runs SIMT FMAs)
             smax = pk.get("sm_max_mhz", 1965.0)
@@ -631,7 +637,7 @@ def run_terrain(args, rank, world, local_rank):
                 "traffic": traffic, "traffic_source": traffic_src,
                 "kernel": ("hot_kernel<double,1,1,M_STEP> (ROWS mode: one Jacobi iteration per launch)" if rows_mode
                            else "hot_kernel<double,1,1,M_MATVEC> (phase 1 V^T X, grid barrier, phase 2 row-owner "
-                           "accumulate)" if k <= 2 else
+                           "accumulate)" + (" once per column" if colsplit else "") if kl <= 2 else
                            "hot_kernel<double,32,VEC,M_MATVEC> (wide per-row: warp across 32 VEC columns)"),
                 "achieved_gbs": ach_gbs, "hbm_frac": ach_gbs / hbm,
                 "avg_launch_ms": avg, "launches": l_hot, "alg_bytes_per_apply": bytes_app,

@@ -135,7 +135,10 @@ int vf_free(vf_handle h);
  * torch.cuda.current_stream().cuda_stream).  NULL = legacy default stream. */
 int vf_set_stream(vf_handle h, void* stream);
 
-/* Y = F-hat X (Alg. 5), overwrite, no clamping (reading A12).  X, Y: N x nrhs. */
+/* Y = F-hat X (Alg. 5), overwrite, no clamping (reading A12).  X, Y: N x nrhs.
+ * 2..8 columns on an F-hat whose device layout exceeds 256 MB are applied
+ * column by column with the nrhs = 1 kernel (each column's result is bitwise
+ * that of a separate nrhs = 1 call); env VF_MV_COLSPLIT=0/1 overrides. */
 int vf_matvec(vf_handle h, const void* X, void* Y, int nrhs);
 
 /* Jacobi solve of B = E + diag(rho) F-hat B (eq. radiosity-system):

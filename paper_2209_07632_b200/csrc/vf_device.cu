@@ -2776,29 +2776,48 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     void* Yd;
     if ((rc = stage_in(h, 0, X, vb, st, &Xd))) return rc;
     if ((rc = stage_out_buf(h, 1, Y, vb, &Yd))) return rc;
-    launch_permute_in<T>(h, Xd, nrhs, kp, nullptr, D->xt[0], nullptr, nullptr, nullptr, st);
-    HotArgs a = hot_args(D, kp, nrhs);
-    a.Y = D->Yp;
-    // optional (VF_MV_FLAGS=1): phase 1 -> phase 2 by per-block flags and a dynamic
-    // row queue instead of the grid barrier.  Measured slower on cfg3-shaped
-    // F-hat (flag spinning + queue atomics > barrier wait), so off by default.
-    // nrhs = 1 matvec: phase-2 rows from a global LPT-ordered queue (dynamic
-    // balance: the static schedule left a ~10 % tail on cfg3); VF_MV_STATIC=1
-    // restores the static schedule.  Each row is summed identically either way.
-    if (kp == 1 && !getenv("VF_MV_STATIC") && !getenv("VF_MV_FLAGS")) {
-        CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
-        a.qctr = D->tready + D->n_svd; a.p2_order = D->p2_order;
+    auto apply = [&](const void* Xc, void* Yc, int n, int kpn) -> int {
+        int rc;
+        launch_permute_in<T>(h, Xc, n, kpn, nullptr, D->xt[0], nullptr, nullptr, nullptr, st);
+        HotArgs a = hot_args(D, kpn, n);
+        a.Y = D->Yp;
+        // optional (VF_MV_FLAGS=1): phase 1 -> phase 2 by per-block flags and a dynamic
+        // row queue instead of the grid barrier.  Measured slower on cfg3-shaped
+        // F-hat (flag spinning + queue atomics > barrier wait), so off by default.
+        // nrhs = 1 matvec: phase-2 rows from a global LPT-ordered queue (dynamic
+        // balance: the static schedule left a ~10 % tail on cfg3); VF_MV_STATIC=1
+        // restores the static schedule.  Each row is summed identically either way.
+        if (kpn == 1 && !getenv("VF_MV_STATIC") && !getenv("VF_MV_FLAGS")) {
+            CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
+            a.qctr = D->tready + D->n_svd; a.p2_order = D->p2_order;
+        }
+        if (kpn == 1 && getenv("VF_MV_FLAGS") && !getenv("VF_MV_BARRIER")) {
+            CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
+            a.tready = D->tready; a.seg_blk = D->seg_blk; a.g1_blk = D->g1_blk;
+            a.qctr = D->tready + D->n_svd; a.p2_order = D->p2_order;
+        }
+        const bool rows = D->world > 1 || h->comm;
+        if (rows) CK(cudaMemsetAsync(D->Yp, 0, (size_t)D->N * kpn * sizeof(T), st));   // rows of other ranks: 0 ...
+        if ((rc = launch_hot<T, M_MATVEC>(h, a, st))) return rc;
+        if (rows && h->comm && (rc = rows_allgather_buf<T>(h, D->Yp, kpn, st))) return rc;   // ... or gathered
+        launch_permute_out<T>(h, D->Yp, n, kpn, true, Yc, st);
+        return VF_OK;
+    };
+    // 2..8 columns on a large (HBM-resident, > 256 MB) F-hat: the batched
+    // kernels for kp = 2..8 stream F-hat at a small fraction of the nrhs = 1
+    // kernel's bandwidth (cfg3: nrhs 4 took 20 ms vs 4 x 0.94 ms), so each
+    // column goes through the nrhs = 1 path (one F-hat stream per column).
+    // VF_MV_COLSPLIT=1/0 forces it on/off (tests).
+    const char* cs = getenv("VF_MV_COLSPLIT");
+    const bool rows_mode = D->world > 1 || h->comm;
+    const bool split = !rows_mode && nrhs >= 2 && nrhs <= 8 &&
+                       (cs ? atoi(cs) != 0 : D->bytes > ((int64_t)256 << 20));
+    if (split) {
+        for (int c = 0; c < nrhs; ++c)
+            if ((rc = apply((const T*)Xd + (size_t)c * D->N, (T*)Yd + (size_t)c * D->N, 1, 1))) return rc;
+    } else if ((rc = apply(Xd, Yd, nrhs, kp))) {
+        return rc;
     }
-    if (kp == 1 && getenv("VF_MV_FLAGS") && !getenv("VF_MV_BARRIER")) {
-        CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
-        a.tready = D->tready; a.seg_blk = D->seg_blk; a.g1_blk = D->g1_blk;
-        a.qctr = D->tready + D->n_svd; a.p2_order = D->p2_order;
-    }
-    const bool rows = D->world > 1 || h->comm;
-    if (rows) CK(cudaMemsetAsync(D->Yp, 0, (size_t)D->N * kp * sizeof(T), st));   // rows of other ranks: 0 ...
-    if ((rc = launch_hot<T, M_MATVEC>(h, a, st))) return rc;
-    if (rows && h->comm && (rc = rows_allgather_buf<T>(h, D->Yp, kp, st))) return rc;   // ... or gathered
-    launch_permute_out<T>(h, D->Yp, nrhs, kp, true, Yd, st);
     CK(cudaGetLastError());
     if ((rc = stage_out_copy(Y, Yd, vb, st))) return rc;
     if (Yd != Y || h->timing) CK(cudaStreamSynchronize(st));
