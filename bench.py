@@ -607,22 +607,49 @@ def run_terrain(args, rank, world, local_rank):
         pk, pk_kind = peaks()
         n_app = applies / max(args.steps, 1)
         avg = ms_hot / max(l_hot, 1)
-        kp = k if k <= 2 else (k + 15) // 16 * 16 if k > 8 else (4 if k <= 4 else 8)
-        # 2..8 columns on an F-hat above 256 MB run column by column through the
-        # nrhs = 1 kernel (libvf's rule in matvec_impl): one launch = one column
-        colsplit = not rows_mode and 2 <= k <= 8 and info["device_bytes"] > (256 << 20)
-        kl = 1 if colsplit else k
-        if colsplit:
-            kp = 1
+        def pad(n):
+            return n if n <= 2 else (n + 15) // 16 * 16 if n > 8 else (4 if n <= 4 else 8)
+        # libvf's column rules for an F-hat above 256 MB (matvec_impl): 2..8
+        # columns go one by one through the nrhs = 1 kernel, more than 64 in
+        # 64-column chunks; one launch = one column / one chunk
+        big = not rows_mode and info["device_bytes"] > (256 << 20)
+        colsplit = big and 2 <= k <= 8
+        chunks = [1] * k if colsplit else [k]
+        if big and k > 64:                       # 64-column chunks; tail in 32/16 pieces, <= 8 one by one
+            chunks, c0, piece = [], 0, 64
+            while c0 < k:
+                n = k - c0
+                if n >= piece:
+                    n = piece
+                elif piece // 2 >= 16:
+                    piece //= 2
+                    continue
+                if n <= 8:
+                    chunks += [1] * (k - c0)
+                    break
+                chunks.append(n)
+                c0 += n
+        kl = max(chunks)
         solve_rows = 4 if rows_mode else 1
-        bytes_app = (info["p1_bytes"] + info["p2_bytes"] + (info["p1_src_rows"] + info["p2_src_rows"]) * kp * w
-                     + info["t_rows"] * kp * w + info["active_rows"] * kp * w * solve_rows)
-        flops_app = info["alg_flops_per_col"] * kl
-        apps_launch = (n_app / max(l_hot / args.steps, 1)) if rows_mode else 1
-        ach_gbs = bytes_app * apps_launch / (avg * 1e-3) / 1e9 if avg > 0 else 0.0
+
+        def alg_bytes(kp):
+            return (info["p1_bytes"] + info["p2_bytes"] + (info["p1_src_rows"] + info["p2_src_rows"]) * kp * w
+                    + info["t_rows"] * kp * w + info["active_rows"] * kp * w * solve_rows)
+        kp = pad(k)
+        bytes_app = alg_bytes(kp)
+        flops_app = info["alg_flops_per_col"] * k
+        if rows_mode:
+            apps_launch = n_app / max(l_hot / args.steps, 1)
+            ach_gbs = bytes_app * apps_launch / (avg * 1e-3) / 1e9 if avg > 0 else 0.0
+            ach_tf = flops_app * apps_launch / (avg * 1e-3) / 1e12 if avg > 0 else 0.0
+        else:
+            # per step: the launches' algorithmic bytes / flops over their summed device time
+            t_hot = ms_hot / max(args.steps, 1) * 1e-3
+            bytes_step = sum(alg_bytes(pad(n)) for n in chunks)
+            ach_gbs = bytes_step / t_hot / 1e9 if t_hot > 0 else 0.0
+            ach_tf = flops_app / t_hot / 1e12 if t_hot > 0 else 0.0
         hbm = pk.get("hbm_gbs", 6559.0)
         traffic, traffic_src = ncu_traffic(f"{args.workload}_k{k}_{dt}")
-        ach_tf = flops_app * apps_launch / (avg * 1e-3) / 1e12 if avg > 0 else 0.0
         if kl > 2:
             # batched: arithmetic intensity above the ridge -> FP64/FP32 FMA bound
             # (the wide per-row kernel runs SIMT FMAs)
@@ -640,9 +667,11 @@ def run_terrain(args, rank, world, local_rank):
                            "accumulate)" + (" once per column" if colsplit else "") if kl <= 2 else
                            "hot_kernel<double,32,VEC,M_MATVEC> (wide per-row: warp across 32 VEC columns)"),
                 "achieved_gbs": ach_gbs, "hbm_frac": ach_gbs / hbm,
-                "avg_launch_ms": avg, "launches": l_hot, "alg_bytes_per_apply": bytes_app,
-                "alg_flops_per_apply": flops_app, "achieved_tflops": flops_app * apps_launch / (avg * 1e-3) / 1e12
-                if avg > 0 else 0.0, "share_of_step": ms_hot / t_ms if t_ms > 0 else None}
+                "avg_launch_ms": avg, "launches": l_hot,
+                "alg_bytes_per_apply": bytes_app if rows_mode else bytes_step,
+                "alg_flops_per_apply": flops_app, "achieved_tflops": ach_tf,
+                "column_chunks": chunks[:4] + (["..."] if len(chunks) > 4 else []),
+                "share_of_step": ms_hot / t_ms if t_ms > 0 else None}
         cfgname = "configs[4]" if rows_mode else "configs[2]"
         wl = (f"BASELINE {cfgname}: {args.cells}^2-cell fBm terrain (H 0.8, RMS slope 15 deg, 10 m) + "
               f"{1000.0 * args.cells / 256:.0f} m cap crater, {N} facets, F-hat tol {args.tol:g}, {dt.upper()}, "

@@ -138,7 +138,10 @@ int vf_set_stream(vf_handle h, void* stream);
 /* Y = F-hat X (Alg. 5), overwrite, no clamping (reading A12).  X, Y: N x nrhs.
  * 2..8 columns on an F-hat whose device layout exceeds 256 MB are applied
  * column by column with the nrhs = 1 kernel (each column's result is bitwise
- * that of a separate nrhs = 1 call); env VF_MV_COLSPLIT=0/1 overrides. */
+ * that of a separate nrhs = 1 call); env VF_MV_COLSPLIT=0/1 overrides.
+ * More than 64 columns there run in 64-column chunks, the tail in 32/16-column
+ * pieces, a 9..15-column rest batched, <= 8 columns one by one (env
+ * VF_MV_CHUNK=c sets the chunk, 0 = one batch).  Not in ROWS mode. */
 int vf_matvec(vf_handle h, const void* X, void* Y, int nrhs);
 
 /* Jacobi solve of B = E + diag(rho) F-hat B (eq. radiosity-system):

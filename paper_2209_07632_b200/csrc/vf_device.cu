@@ -2812,9 +2812,32 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     const bool rows_mode = D->world > 1 || h->comm;
     const bool split = !rows_mode && nrhs >= 2 && nrhs <= 8 &&
                        (cs ? atoi(cs) != 0 : D->bytes > ((int64_t)256 << 20));
+    // More than 64 columns on a large F-hat: 64-column chunks (cfg3: 64 columns
+    // 17.0 ms, 128 columns 44.8 ms in one batch -- the wide per-row kernel
+    // loses more to register pressure at VEC = 4 than it saves in F-hat
+    // reads).  VF_MV_CHUNK=c forces chunks of c columns (tests), 0 = off.
+    const char* ch = getenv("VF_MV_CHUNK");
+    const int chunk = ch ? atoi(ch) : (D->bytes > ((int64_t)256 << 20) ? 64 : 0);
     if (split) {
         for (int c = 0; c < nrhs; ++c)
             if ((rc = apply((const T*)Xd + (size_t)c * D->N, (T*)Yd + (size_t)c * D->N, 1, 1))) return rc;
+    } else if (!rows_mode && chunk > 8 && nrhs > chunk) {
+        // chunks of `chunk`, then the tail in pieces of chunk/2, chunk/4 (>= 16)
+        // columns, a last 9..15-column piece batched and <= 8 columns one by
+        // one (cfg3: a padded 36-column tail cost 26 ms, 32 + 4 cost 19)
+        int c0 = 0;
+        for (int piece = chunk; c0 < nrhs;) {
+            int n = nrhs - c0;
+            if (n >= piece) n = piece;
+            else if (piece / 2 >= 16) { piece /= 2; continue; }
+            if (n <= 8) {
+                for (; c0 < nrhs; ++c0)
+                    if ((rc = apply((const T*)Xd + (size_t)c0 * D->N, (T*)Yd + (size_t)c0 * D->N, 1, 1))) return rc;
+                break;
+            }
+            if ((rc = apply((const T*)Xd + (size_t)c0 * D->N, (T*)Yd + (size_t)c0 * D->N, n, pad_k(n)))) return rc;
+            c0 += n;
+        }
     } else if ((rc = apply(Xd, Yd, nrhs, kp))) {
         return rc;
     }

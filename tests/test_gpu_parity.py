@@ -400,3 +400,44 @@ def test_small_batch_column_split_equals_k1_applies(rough, tmp_path_factory, mon
     Yref = hm.hmatvec(H, X)
     assert rel(host(Y), Yref) <= 1e-12
     assert rel(host(Yb), Yref) <= 1e-12
+
+
+def test_wide_batch_chunks_equal_separate_applies(rough, tmp_path_factory, monkeypatch):
+    """More than 64 columns on a large F-hat are applied in 64-column chunks,
+    the tail in 32/16-column pieces and single columns (VF_MV_CHUNK forces
+    the rule here): each piece equals a separate apply of those columns bit
+    for bit, and the whole result matches the oracle's Alg. 5 apply."""
+    V, F, S, Fd = rough
+    H = hm.compress(S.x, Fd, 1e-6, min_size=2048)
+    p = str(tmp_path_factory.mktemp("ch") / "r.hvfm")
+    hm.write_hvfm(H, p)
+    k, c = 150, 64
+    X = sg.random_rhs(S.N, k, seed=12)
+    M = vf.ViewFactorMatrix.load(p, device=0)
+    monkeypatch.setenv("VF_MV_CHUNK", str(c))
+    Y = empty(S.N, k)
+    M.matvec(dev(X), Y)
+    monkeypatch.setenv("VF_MV_CHUNK", "0")
+    monkeypatch.setenv("VF_MV_COLSPLIT", "0")
+    pieces, c0, piece = [], 0, c                 # libvf's piece rule: 64, 64, 16, then 6 single columns
+    while c0 < k:
+        n = k - c0
+        if n >= piece:
+            n = piece
+        elif piece // 2 >= 16:
+            piece //= 2
+            continue
+        if n <= 8:
+            pieces += [1] * (k - c0)
+            break
+        pieces.append(n)
+        c0 += n
+    assert pieces == [64, 64, 16] + [1] * 6
+    parts, c0 = [], 0
+    for n in pieces:
+        y = empty(S.N, n)
+        M.matvec(dev(np.asfortranarray(X[:, c0:c0 + n])), y)
+        parts.append(host(y))
+        c0 += n
+    assert np.array_equal(host(Y), np.concatenate(parts, axis=1))
+    assert rel(host(Y), hm.hmatvec(H, X)) <= 1e-12
