@@ -1,19 +1,24 @@
 #!/usr/bin/env python
 """Benchmark of the compressed view-factor hot path on B200.
 
-Workload (BASELINE.json configs[1], the config the metric is quoted on):
-the spherical-cap crater (d/D = 0.2) inset in a square plain of side 4D,
-~19,200 facets, F-hat built at tol 1e-5 (FP64, or FP32 with --dtype f32),
-64 sun directions at 5 deg elevation as one batched right-hand side.
-One STEP = one vf_solve_thermal call on the 64-column batch: every §8(a)
-row of the hot path (permute-in, low-rank phase 1, row-owner accumulate
-with the fused Jacobi epilogue, convergence, radiosity -> IR chaining and
-the temperature epilogue), i.e. (iters1 + iters2) F-hat applies.
+Default workload (BASELINE.json configs[2], the largest single-GPU config:
+BASELINE.json's `metric` names no config, so the largest one that fits one
+GPU applies): the 256^2-cell fBm terrain (Hurst 0.8, RMS slope 15 deg, 10 m
+spacing) with a 1 km spherical-cap crater, 131,072 facets, F-hat built at
+tol 1e-5 in FP64 (untimed).  One STEP = one vf_matvec with nrhs = 1 (the
+HBM-bound compressed apply, Alg. 5): permute-in, low-rank
+phase 1 (T = S V^T X), row-owner accumulate, permute-out.  The same line
+carries `batched`: nrhs = 128 (configs[2]'s batched case) timed the same way.
 
 metric value = RHS-column applies per second = sum over ranks of
-64 * (iters1 + iters2) per step / step time (max over ranks).
-Multi-GPU (torchrun): every rank solves its own batch of 64 suns (azimuths
-offset per rank), no data-path collective: weak scaling.
+nrhs * steps / time (max over ranks).  Multi-GPU (torchrun): every rank
+applies the replicated F-hat to its own right-hand sides (COLS), no
+data-path collective: weak scaling.
+
+--workload cfg2 : configs[1], the 64-sun batched thermal solve (cap crater in
+                  a plain, F-hat resident in shared memory).
+--workload cfg5 : configs[4], the cfg3 mesh with one sun, radiosity + IR to
+                  1e-8, block-row sharded (ROWS) with a per-iteration allgather.
 
 --impl reference runs the FP64 CPU oracle (oracle/, the reference arm for
 this tier) on a bounded sample of the same workload on the host cores.
@@ -42,6 +47,7 @@ TOL_SOLVE = {"f64": 1e-10, "f32": 1e-6}
 ALBEDO, EMISS = 0.12, 0.95
 S_SUN = 1365.0
 ELEV = 5.0
+REF_ROWS = 2000          # oracle rows of the exact F sampled on the terrain configs
 
 
 def peaks():
@@ -218,22 +224,24 @@ def oracle_sample(V, F, suns, ncols, budget_s):
 
 
 def run_reference(args, rank, world):
+    """The reference arm of this tier: the FP64 CPU oracle as it stands, on a
+    bounded sample of the SAME workload as the GPU arm (rank 0 only)."""
     if rank != 0:
         return
-    V, F, suns = workload(0, 1)
     import oracle
     oracle.build()
+    if args.workload in ("cfg3", "cfg5"):
+        return run_reference_terrain(args)
+    V, F, suns = workload(0, 1)
     ncols = 8
-    S = None
     times, applies = [], 0
-    import oracle as O
-    S = O.Scene(V, F)
+    S = oracle.Scene(V, F)
     csr = S.F_csr_rows()
     Q = S.insolation(suns[:ncols], S_SUN)
     alb, emi = np.full(S.N, ALBEDO), np.full(S.N, EMISS)
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        out = O.thermal(lambda X: O.apply_csr(csr, X), Q, alb, emi, TOL_SOLVE["f64"], 100)
+        out = oracle.thermal(lambda X: oracle.apply_csr(csr, X), Q, alb, emi, TOL_SOLVE["f64"], 100)
         dt = time.perf_counter() - t0
         if i >= args.warmup:
             times.append(dt)
@@ -249,6 +257,51 @@ def run_reference(args, rank, world):
                              "sample": sample, "cpu": cpu_model()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def run_reference_terrain(args):
+    """configs[2] (cfg3) reference: the oracle's exact F (eq. FF-def with its
+    own visibility) on REF_ROWS seeded rows, applied to the same nrhs columns
+    as the GPU arm each step; value scaled to whole-matrix applies."""
+    import oracle
+    import scenegen as sg
+    V, F = sg.cfg3_mesh(n=args.cells, crater_D=1000.0 * args.cells / 256)
+    S = oracle.Scene(V, F)
+    N = S.N
+    k = args.nrhs
+    rows = np.sort(np.random.default_rng(8).choice(N, size=min(N, REF_ROWS), replace=False))
+    t0 = time.perf_counter()
+    csr = S.F_csr_rows(rows)
+    t_rows = time.perf_counter() - t0
+    X = sg.random_rhs(N, k, seed=3)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.apply_csr(csr, X)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    tot = sum(times)
+    v = args.steps * k * rows.size / N / tot
+    sample = (f"oracle exact-CSR apply (eq. FF-def rows, FP64, OpenMP) of {rows.size} seeded rows of F x {k} "
+              f"column(s) per step, scaled to whole-matrix applies (rows computed once, {t_rows:.1f} s, untimed)")
+    wl = terrain_workload_name(args, N, "f64", k)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": wl, "N": N, "nrhs": k, "rows_sampled": int(rows.size)},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+                             "sample": sample, "cpu": cpu_model()},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def terrain_workload_name(args, N, dt, k, rows_mode=False):
+    cfgname = "configs[4]" if rows_mode else "configs[2]"
+    return (f"BASELINE {cfgname}: {args.cells}^2-cell fBm terrain (H 0.8, RMS slope 15 deg, 10 m) + "
+            f"{1000.0 * args.cells / 256:.0f} m cap crater, {N} facets, F-hat tol {args.tol:g}, {dt.upper()}, "
+            + ("one sun (e 5 deg), radiosity + IR Jacobi to 1e-8, block-row sharded (ROWS) with a per-iteration "
+               "ncclAllGather" if rows_mode else f"vf_matvec with nrhs = {k} (U[0,1) columns, seed 3)"))
 
 
 def config_block(N, dtype, extra=None):
@@ -476,6 +529,132 @@ def oracle_rows(V, F, rows):
     return S, S.F_csr_rows(rows)
 
 
+def _pad(n):
+    return n if n <= 2 else (n + 15) // 16 * 16 if n > 8 else (4 if n <= 4 else 8)
+
+
+def matvec_chunks(info, k, rows_mode):
+    """The launches libvf's vf_matvec issues for k columns (matvec_impl's
+    column rules): one entry per launch, its column count."""
+    big = not rows_mode and info["device_bytes"] > (256 << 20) and not info.get("stream_batched")
+    if big and 2 <= k <= 8:
+        return [1] * k
+    if big and k > 64:
+        chunks, c0, piece = [], 0, 64
+        while c0 < k:
+            n = k - c0
+            if n >= piece:
+                n = piece
+            elif piece // 2 >= 16:
+                piece //= 2
+                continue
+            if n <= 8:
+                chunks += [1] * (k - c0)
+                break
+            chunks.append(n)
+            c0 += n
+        return chunks
+    return [k]
+
+
+def time_steps(M, vf, step, steps, warmup, stream, dist, local_rank, per_step_sync):
+    """W untimed steps, then K steps bracketed by barrier + synchronize; CUDA
+    events on the library's stream around each step; libvf's own per-launch
+    event pairs give the hot kernel's device time.  Returns a dict."""
+    import torch
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    vf.vf_enable_kernel_timing(M.h, True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    clocks = Clocks(local_rank)
+    ms_hot, l_hot, launches, extra = 0.0, 0, 0, 0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for i in range(steps):
+        ev[i][0].record(stream)
+        e = step()
+        ev[i][1].record(stream)
+        if per_step_sync:
+            torch.cuda.synchronize()
+        kt = vf.vf_kernel_timing(M.h)
+        ms_hot += kt["ms_phase2"]
+        l_hot += kt["launches_phase2"]
+        launches += kt["launches_total"]
+        extra += e or 0
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clk = clocks.stop()
+    vf.vf_enable_kernel_timing(M.h, False)
+    t_ms = sum(x.elapsed_time(y) for x, y in ev)
+    return {"t_ms": t_ms, "ms_hot": ms_hot, "l_hot": l_hot, "launches": launches, "clocks": clk, "extra": extra}
+
+
+def reduce_time_work(t_ms, work, dist, dev, sum_work=True):
+    import torch
+    tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
+    wk = torch.tensor([float(work)], dtype=torch.float64, device=dev)
+    if dist:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        if sum_work:
+            dist.all_reduce(wk, op=dist.ReduceOp.SUM)
+    return tt.item(), wk.item()
+
+
+def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
+    """Roofline object of the dominant kernel for a terrain line:
+    nrhs <= 2 -> HBM bound, algorithmic bytes = F-hat payload + X/T rows read
+    + T rows written + Y rows written; batched -> FP64/FP32 FMA bound,
+    algorithmic flops = nrhs x alg_flops_per_col."""
+    w = 8 if dt == "f64" else 4
+    chunks = matvec_chunks(info, k, rows_mode)
+    solve_rows = 4 if rows_mode else 1
+    hbm = pk.get("hbm_gbs", 6559.0)
+
+    def alg_bytes(kp):
+        return (info["p1_bytes"] + info["p2_bytes"] + (info["p1_src_rows"] + info["p2_src_rows"]) * kp * w
+                + info["t_rows"] * kp * w + info["active_rows"] * kp * w * solve_rows)
+    avg = tm["ms_hot"] / max(tm["l_hot"], 1)
+    flops_app = info["alg_flops_per_col"] * k
+    if rows_mode:
+        n_app = tm["extra"] / max(steps, 1)
+        apps_launch = n_app / max(tm["l_hot"] / steps, 1)
+        bytes_app = alg_bytes(1)
+        ach_gbs = bytes_app * apps_launch / (avg * 1e-3) / 1e9 if avg > 0 else 0.0
+        ach_tf = flops_app * apps_launch / (avg * 1e-3) / 1e12 if avg > 0 else 0.0
+    else:
+        t_hot = tm["ms_hot"] / max(steps, 1) * 1e-3
+        bytes_app = sum(alg_bytes(_pad(n)) for n in chunks)
+        ach_gbs = bytes_app / t_hot / 1e9 if t_hot > 0 else 0.0
+        ach_tf = flops_app / t_hot / 1e12 if t_hot > 0 else 0.0
+    traffic, traffic_src = ncu_traffic(f"{workload}_k{k}_{dt}")
+    if max(chunks) > 2:
+        smax = pk.get("sm_max_mhz", 1965.0)
+        peak_tf = fp64_peak_tflops(smax) if dt == "f64" else fp32_peak_tflops(smax)
+        dmma = bool(info.get("stream_batched")) and dt == "f64"
+        bound = {"bound": "tensor" if dmma else "alu", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                 "frac": ach_tf / peak_tf,
+                 "peak_basis": (("derived FP64 DMMA peak (= the DFMA rate on B200): " if dmma else "derived: ")
+                                + f"148 SM x {64 if dt == 'f64' else 128} FMA/clk x 2 x {smax:.0f} MHz "
+                                  f"(sm_max of {pk_kind} MEASURED_PEAKS.json)")}
+    else:
+        bound = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm,
+                 "peak_basis": f"{pk_kind} MEASURED_PEAKS.json hbm_gbs (copy bandwidth, 'burst' figure for a kernel "
+                               "timed alone)"}
+    kern = info.get("kernel_name_k1" if max(chunks) <= 2 else "kernel_name_batched") or (
+        "hot_kernel<T,1,1,M_MATVEC>" if max(chunks) <= 2 else "hot_kernel<T,32,VEC,M_MATVEC>")
+    return {**bound, "traffic": traffic, "traffic_source": traffic_src,
+            "kernel": ("(ROWS mode, one Jacobi iteration per launch) " if rows_mode else "") + kern,
+            "achieved_gbs": ach_gbs, "hbm_frac": ach_gbs / hbm, "hbm_frac_vs_8TBs_spec": ach_gbs / 8000.0,
+            "avg_launch_ms": avg, "launches": tm["l_hot"], "alg_bytes_per_apply": bytes_app,
+            "alg_flops_per_apply": flops_app, "achieved_tflops": ach_tf,
+            "column_chunks": chunks[:4] + (["..."] if len(chunks) > 4 else []),
+            "share_of_step": tm["ms_hot"] / tm["t_ms"] if tm["t_ms"] > 0 else None}
+
+
 def run_terrain(args, rank, world, local_rank):
     import torch
     import paper_2209_07632_b200 as vf
@@ -488,6 +667,7 @@ def run_terrain(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     dt = args.dtype
     tdt = torch.float64 if dt == "f64" else torch.float32
+    ndt = np.float64 if dt == "f64" else np.float32
     w = 8 if dt == "f64" else 4
     M, V, F, binfo = terrain_fhat(args, local_rank)
     rows_mode = args.workload == "cfg5"
@@ -504,7 +684,7 @@ def run_terrain(args, rank, world, local_rank):
     k = 1 if rows_mode else args.nrhs
 
     def colmajor(a):
-        return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64 if dt == "f64" else np.float32).T)).to(dev).T
+        return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=ndt).T)).to(dev).T
 
     if rows_mode:
         sun = sg.sun_dirs(5.0, 1)
@@ -517,64 +697,32 @@ def run_terrain(args, rank, world, local_rank):
 
         def step():
             M.solve_thermal(Qd, alb, emi, T, Qv, Qi, iters=500, tol=1e-8)
+            st = M.stats()
+            return st["iters1"] + st["iters2"]
     else:
         X = colmajor(sg.random_rhs(N, k, seed=3 + rank))
         Y = torch.empty((k, N), dtype=tdt, device=dev).T
 
         def step():
             M.matvec(X, Y)
+            return k
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    vf.vf_enable_kernel_timing(M.h, True)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    clocks = Clocks(local_rank)
-    ms_hot, l_hot, launches, applies = 0.0, 0, 0, 0
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    for i in range(args.steps):
-        ev[i][0].record(stream)
-        step()
-        ev[i][1].record(stream)
-        kt = vf.vf_kernel_timing(M.h)
-        if not rows_mode:
-            torch.cuda.synchronize()
-            kt = vf.vf_kernel_timing(M.h)
-        ms_hot += kt["ms_phase2"]; l_hot += kt["launches_phase2"]
-        launches += kt["launches_total"]
-        if rows_mode:
-            st = M.stats()
-            applies += st["iters1"] + st["iters2"]
-        else:
-            applies += k
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
-    clk = clocks.stop()
-    vf.vf_enable_kernel_timing(M.h, False)
-    t_ms = sum(a.elapsed_time(b) for a, b in ev)
-    tt = torch.tensor([t_ms], dtype=torch.float64, device=dev)
-    wk = torch.tensor([float(applies)], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        if not rows_mode:                      # COLS replicas: work adds up; ROWS: one shared solve
-            dist.all_reduce(wk, op=dist.ReduceOp.SUM)
-    t_max = tt.item()
-    value = wk.item() / (t_max / 1e3)
+    tm = time_steps(M, vf, step, args.steps, args.warmup, stream, dist, local_rank, per_step_sync=not rows_mode)
+    t_max, work = reduce_time_work(tm["t_ms"], tm["extra"], dist, dev, sum_work=not rows_mode)
+    value = work / (t_max / 1e3)
 
-    # e2e through the same call with pinned HOST buffers
+    # e2e through the same call with pinned HOST buffers (H2D of the inputs and
+    # D2H of the result inside the timed region)
     e_ms, e_app = 0.0, 0
     if rows_mode:
-        Qp = torch.from_numpy(np.ascontiguousarray(Qh.T.astype(np.float64 if dt == "f64" else np.float32))).pin_memory().T
+        Qp = torch.from_numpy(np.ascontiguousarray(Qh.T.astype(ndt))).pin_memory().T
         ap_ = torch.full((N,), ALBEDO, dtype=tdt).pin_memory()
         ep_ = torch.full((N,), EMISS, dtype=tdt).pin_memory()
         Tp = torch.empty((1, N), dtype=tdt).pin_memory().T
 
         def estep():
             M.solve_thermal(Qp, ap_, ep_, Tp, None, None, iters=500, tol=1e-8)
+            return M.stats()["iters1"] + M.stats()["iters2"]
         h2d, d2h = N * w + 2 * N * w, N * w
     else:
         Xp = X.cpu().T.contiguous().pin_memory().T
@@ -582,6 +730,7 @@ def run_terrain(args, rank, world, local_rank):
 
         def estep():
             M.matvec(Xp, Yp)
+            return k
         h2d, d2h = N * k * w, N * k * w
     estep()
     ke = max(3, min(args.steps, 10))
@@ -589,113 +738,57 @@ def run_terrain(args, rank, world, local_rank):
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        estep()
+        n = estep()
         e1.record(stream)
         e1.synchronize()
         e_ms += e0.elapsed_time(e1)
-        e_app += (M.stats()["iters1"] + M.stats()["iters2"]) if rows_mode else k
-    et = torch.tensor([e_ms], dtype=torch.float64, device=dev)
-    ew = torch.tensor([float(e_app)], dtype=torch.float64, device=dev)
-    if dist:
-        dist.all_reduce(et, op=dist.ReduceOp.MAX)
-        if not rows_mode:
-            dist.all_reduce(ew, op=dist.ReduceOp.SUM)
-    e2e_value = ew.item() / (et.item() / 1e3)
+        e_app += n
+    et, ew = reduce_time_work(e_ms, e_app, dist, dev, sum_work=not rows_mode)
+    e2e_value = ew / (et / 1e3)
 
-    parity = None
+    # the batched case of configs[2] (nrhs = 128) on the same F-hat, same protocol
+    batched = None
+    kb = args.batched if (not rows_mode and k == 1) else 0
+    if kb:
+        Xb = colmajor(sg.random_rhs(N, kb, seed=3 + rank))
+        Yb = torch.empty((kb, N), dtype=tdt, device=dev).T
+
+        def bstep():
+            M.matvec(Xb, Yb)
+            return kb
+        sb = max(3, min(args.steps, 20))
+        tb = time_steps(M, vf, bstep, sb, 3, stream, dist, local_rank, per_step_sync=True)
+        tbm, wb = reduce_time_work(tb["t_ms"], tb["extra"], dist, dev)
+        if rank == 0:
+            pk, pk_kind = peaks()
+            batched = {"nrhs": kb, "value": wb / (tbm / 1e3), "unit": UNIT, "steps": sb,
+                       "ms_per_step": tbm / sb, "gpu_launches": tb["launches"], "clocks": tb["clocks"],
+                       "roofline": terrain_roofline(info, kb, dt, tb, sb, False, pk, pk_kind, args.workload)}
+
     if rank == 0:
         pk, pk_kind = peaks()
-        n_app = applies / max(args.steps, 1)
-        avg = ms_hot / max(l_hot, 1)
-        def pad(n):
-            return n if n <= 2 else (n + 15) // 16 * 16 if n > 8 else (4 if n <= 4 else 8)
-        # libvf's column rules for an F-hat above 256 MB (matvec_impl): 2..8
-        # columns go one by one through the nrhs = 1 kernel, more than 64 in
-        # 64-column chunks; one launch = one column / one chunk
-        big = not rows_mode and info["device_bytes"] > (256 << 20)
-        colsplit = big and 2 <= k <= 8
-        chunks = [1] * k if colsplit else [k]
-        if big and k > 64:                       # 64-column chunks; tail in 32/16 pieces, <= 8 one by one
-            chunks, c0, piece = [], 0, 64
-            while c0 < k:
-                n = k - c0
-                if n >= piece:
-                    n = piece
-                elif piece // 2 >= 16:
-                    piece //= 2
-                    continue
-                if n <= 8:
-                    chunks += [1] * (k - c0)
-                    break
-                chunks.append(n)
-                c0 += n
-        kl = max(chunks)
-        solve_rows = 4 if rows_mode else 1
-
-        def alg_bytes(kp):
-            return (info["p1_bytes"] + info["p2_bytes"] + (info["p1_src_rows"] + info["p2_src_rows"]) * kp * w
-                    + info["t_rows"] * kp * w + info["active_rows"] * kp * w * solve_rows)
-        kp = pad(k)
-        bytes_app = alg_bytes(kp)
-        flops_app = info["alg_flops_per_col"] * k
-        if rows_mode:
-            apps_launch = n_app / max(l_hot / args.steps, 1)
-            ach_gbs = bytes_app * apps_launch / (avg * 1e-3) / 1e9 if avg > 0 else 0.0
-            ach_tf = flops_app * apps_launch / (avg * 1e-3) / 1e12 if avg > 0 else 0.0
-        else:
-            # per step: the launches' algorithmic bytes / flops over their summed device time
-            t_hot = ms_hot / max(args.steps, 1) * 1e-3
-            bytes_step = sum(alg_bytes(pad(n)) for n in chunks)
-            ach_gbs = bytes_step / t_hot / 1e9 if t_hot > 0 else 0.0
-            ach_tf = flops_app / t_hot / 1e12 if t_hot > 0 else 0.0
-        hbm = pk.get("hbm_gbs", 6559.0)
-        traffic, traffic_src = ncu_traffic(f"{args.workload}_k{k}_{dt}")
-        if kl > 2:
-            # batched: arithmetic intensity above the ridge -> FP64/FP32 FMA bound
-            # (the wide per-row kernel runs SIMT FMAs)
-            smax = pk.get("sm_max_mhz", 1965.0)
-            peak_tf = fp64_peak_tflops(smax) if dt == "f64" else fp32_peak_tflops(smax)
-            bound = {"bound": "alu", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach_tf / peak_tf,
-                     "peak_basis": f"derived: 148 SM x {64 if dt == 'f64' else 128} FMA/clk x 2 x {smax:.0f} MHz"}
-        else:
-            bound = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm,
-                     "peak_basis": f"{pk_kind} MEASURED_PEAKS.json hbm_gbs (copy bandwidth)"}
-        roof = {**bound,
-                "traffic": traffic, "traffic_source": traffic_src,
-                "kernel": ("hot_kernel<double,1,1,M_STEP> (ROWS mode: one Jacobi iteration per launch)" if rows_mode
-                           else "hot_kernel<double,1,1,M_MATVEC> (phase 1 V^T X, grid barrier, phase 2 row-owner "
-                           "accumulate)" + (" once per column" if colsplit else "") if kl <= 2 else
-                           "hot_kernel<double,32,VEC,M_MATVEC> (wide per-row: warp across 32 VEC columns)"),
-                "achieved_gbs": ach_gbs, "hbm_frac": ach_gbs / hbm,
-                "avg_launch_ms": avg, "launches": l_hot,
-                "alg_bytes_per_apply": bytes_app if rows_mode else bytes_step,
-                "alg_flops_per_apply": flops_app, "achieved_tflops": ach_tf,
-                "column_chunks": chunks[:4] + (["..."] if len(chunks) > 4 else []),
-                "share_of_step": ms_hot / t_ms if t_ms > 0 else None}
-        cfgname = "configs[4]" if rows_mode else "configs[2]"
-        wl = (f"BASELINE {cfgname}: {args.cells}^2-cell fBm terrain (H 0.8, RMS slope 15 deg, 10 m) + "
-              f"{1000.0 * args.cells / 256:.0f} m cap crater, {N} facets, F-hat tol {args.tol:g}, {dt.upper()}, "
-              + ("one sun (e 5 deg), radiosity + IR Jacobi to 1e-8, block-row sharded (ROWS) with a per-iteration "
-                 "ncclAllGather" if rows_mode else f"vf_matvec with nrhs = {k} (U[0,1) columns, seed 3)"))
+        roof = terrain_roofline(info, k, dt, tm, args.steps, rows_mode, pk, pk_kind, args.workload)
+        wl = terrain_workload_name(args, N, dt, k, rows_mode)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
                 "scaling": "strong" if rows_mode else "weak", "vs_baseline": None, "dtype": dt, "data": "synthetic",
                 "config": {"workload": wl, "N": N, "nrhs": k, "tol_build": args.tol,
-                           "l2": "inputs larger than L2: F-hat %.2f GB vs 126 MB L2" % (info["alg_bytes"] / 1e9),
+                           "l2": "inputs larger than L2: F-hat %.2f GB vs 126 MB L2 (no flush needed)"
+                                 % (info["alg_bytes"] / 1e9),
                            "fhat_alg_bytes": info["alg_bytes"], "fhat_device_bytes": info["device_bytes"],
                            "blocks": {"dense": info["n_dense"], "csr": info["n_csr"], "svd": info["n_svd"]},
                            "nnz_csr": info["nnz_csr"], "sum_rank": info["sum_rank"],
                            "active_rows": info["active_rows"], "visible_pairs": info["visible_pairs"],
-                           "applies_per_step": n_app, **binfo,
+                           "applies_per_step": tm["extra"] / max(args.steps, 1), **binfo,
                            "parallelism": (f"rows{world}" if rows_mode else f"cols{world}")},
-                "roofline": roof, "cpu_baseline": None, "parity": parity,
+                "roofline": roof, "cpu_baseline": None, "parity": None, "batched": batched,
                 "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
-                "gpu_launches": launches, "clocks": clk}
+                "gpu_launches": tm["launches"], "clocks": tm["clocks"]}
         if not args.no_cpu_baseline and world == 1 and not rows_mode:
             import oracle
             oracle.build()
             rng = np.random.default_rng(8)
-            rows = np.sort(rng.choice(N, size=min(N, 2000), replace=False))
+            rows = np.sort(rng.choice(N, size=min(N, REF_ROWS), replace=False))
             _, csr = oracle_rows(V, F, rows)
             Xh = X.cpu().numpy().astype(np.float64)
             reps, tc = 0, 0.0
@@ -705,13 +798,19 @@ def run_terrain(args, rank, world, local_rank):
                 tc += time.perf_counter() - t0
                 reps += 1
             v_cpu = reps * k * rows.size / N / tc
-            # the same oracle rows check the GPU result of this launch configuration
+            # the same oracle rows check the GPU results of the timed launch configurations
             step()
             torch.cuda.synchronize()
             Yg = Y.cpu().numpy().astype(np.float64)[rows]
             parity = {"rows": int(rows.size), "rel_l2_vs_exact_F": float(np.linalg.norm(Yg - Yref) /
                                                                          np.linalg.norm(Yref)),
-                      "bound": 10 * args.tol, "source": "the cpu_baseline leg's oracle rows"}
+                      "bound": 10 * args.tol, "source": "the cpu_baseline leg's oracle rows (eq. FF-def)"}
+            if kb:
+                bstep()
+                torch.cuda.synchronize()
+                Yrb = oracle.apply_csr(csr, Xb.cpu().numpy().astype(np.float64))
+                Ygb = Yb.cpu().numpy().astype(np.float64)[rows]
+                parity["batched_rel_l2_vs_exact_F"] = float(np.linalg.norm(Ygb - Yrb) / np.linalg.norm(Yrb))
             line["parity"] = parity
             line["cpu_baseline"] = {"value": v_cpu, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
                                     "sample": f"oracle exact-CSR apply (eq. FF-def rows, FP64, OpenMP) of {rows.size} "
@@ -726,16 +825,18 @@ def run_terrain(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="cfg2", choices=["cfg2", "cfg3", "cfg5"],
-                    help="cfg2: BASELINE configs[1] batched thermal solve (default); cfg3: configs[2] matvec; "
+    ap.add_argument("--workload", default="cfg3", choices=["cfg2", "cfg3", "cfg5"],
+                    help="cfg3: BASELINE configs[2] matvec (default); cfg2: configs[1] batched thermal solve; "
                          "cfg5: configs[4] ROWS-sharded single-sun solve on the cfg3 mesh")
     ap.add_argument("--nrhs", type=int, default=1)
+    ap.add_argument("--batched", type=int, default=128,
+                    help="cfg3 with nrhs = 1: also time this many columns (configs[2]'s batched case; 0 = off)")
     ap.add_argument("--tol", type=float, default=1e-5)
     ap.add_argument("--cells", type=int, default=256)
     ap.add_argument("--fhat", default=None, help="HVFM cache path (may use {n}, {tol}, {dtype})")

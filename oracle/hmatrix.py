@@ -91,9 +91,10 @@ def estimate_rank(block: np.ndarray, eps: float, w: int, k0: int = 8):
     Reading A8: U and V inherit the zero rows/columns of F_IJ (P:229, P:235);
     the SVD is taken of the block restricted to its nonzero rows/columns and
     only those rows of U/V are stored.  Reading A6: eps relative to the
-    block's own sigma_1.  Reading A5: the doubling stops once k >= min(m',n')/2
-    or once w k (m'+n') >= nbytes(F_IJ), with m', n' the nonzero rows/columns
-    that U and V store (A8): then no q >= k can pass eq. nbytes-comparison."""
+    block's own sigma_1.  Reading A5: the doubling ("increase k ... jump back",
+    P:230) stops only once w k (m'+n') >= nbytes(F_IJ), with m', n' the
+    nonzero rows/columns that U and V store (A8) -- then no q > k can pass
+    eq. nbytes-comparison -- or once the whole spectrum is in hand (k >= r)."""
     m, n = block.shape
     nnz = int(np.count_nonzero(block))
     target = nbytes_csr(m, nnz, w)                       # nbytes(F_IJ) as CSR (step 1)
@@ -118,7 +119,7 @@ def estimate_rank(block: np.ndarray, eps: float, w: int, k0: int = 8):
             if nbytes_svd(q, urows.size, vrows.size, w) < target:   # eq. nbytes-comparison
                 return q, urows, vrows, U[:, :q].copy(), s[:q].copy(), Vt[:q, :].T.copy()
             return None
-        if k >= min(urows.size, vrows.size) / 2 or w * k * (urows.size + vrows.size) >= target or kk == r:
+        if w * k * (urows.size + vrows.size) >= target or kk == r:
             return None
         k *= 2
 

@@ -532,7 +532,7 @@ struct HotArgs {
     const int32_t* pp_len;
     const int32_t* pp_idx;
     const int32_t* pp_n;
-    int32_t* pp_cnt;              // per group: parts finished (cumulative over launches)
+    int32_t* pp_cnt;              // per group: parts finished (reset to 0 by the part that completes the group)
     double* pp_scratch;           // [part][kGroup] partial sums (part-major, group parts contiguous)
     int32_t* tready;
     const int32_t* seg_blk;
@@ -598,9 +598,9 @@ __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_
         constexpr int H = kGroup / 2;                 // rows per pass (register budget)
         double mine = 0.0;
         for (int h0 = 0; h0 < G.nrows; h0 += H) {
-            int32_t vo[H];                            // value offsets (< 2^31 elements)
+            int64_t vo[H];                            // value offsets (64-bit: F-hat may exceed 2^31 values)
 #pragma unroll
-            for (int r = 0; r < H; ++r) vo[r] = h0 + r < G.nrows ? (int32_t)a.gvo[G.seg_off * kGroup + h0 + r] : -1;
+            for (int r = 0; r < H; ++r) vo[r] = h0 + r < G.nrows ? a.gvo[G.seg_off * kGroup + h0 + r] : -1;
             T acc[H];
 #pragma unroll
             for (int r = 0; r < H; ++r) acc[r] = T(0);
@@ -628,7 +628,10 @@ __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_
             __threadfence();
             __syncwarp();
             int last = 0;
-            if (lane == 0) last = (atomicAdd(a.pp_cnt + gi, 1) + 1) % np == 0;
+            if (lane == 0) {
+                last = atomicAdd(a.pp_cnt + gi, 1) + 1 == np;
+                if (last) atomicExch(a.pp_cnt + gi, 0);   // every part has arrived: reset for the next launch
+            }
             finish = __shfl_sync(0xffffffffu, last, 0);
             if (finish) {
                 __threadfence();
@@ -2306,7 +2309,9 @@ void reset_counters(Handle* h) {
     h->dev->evused = 0;
 }
 
-int ensure_scratch(DeviceHMat* D, int kp) {
+int ensure_scratch(DeviceHMat* D, int kp, cudaStream_t st) {
+    // zeroing is ordered on the handle's stream (the legacy-stream cudaMemset
+    // would not be ordered against non-blocking caller streams)
     if (kp <= D->kp_cap) return VF_OK;
     void** bufs[] = {&D->xt[0], &D->xt[1], &D->Ep, &D->Qp, &D->Qdp, &D->Qvp, &D->Yp, &D->Qip};
     for (void** b : bufs) if (*b) { cudaFree(*b); *b = nullptr; }
@@ -2314,12 +2319,12 @@ int ensure_scratch(DeviceHMat* D, int kp) {
     const size_t rows_x = (size_t)(D->N + D->NT), rows = (size_t)D->N;
     for (int i = 0; i < 2; ++i) {
         CK(cudaMalloc(&D->xt[i], std::max<size_t>(16, rows_x * kp * D->w)));
-        CK(cudaMemset(D->xt[i], 0, std::max<size_t>(16, rows_x * kp * D->w)));
+        CK(cudaMemsetAsync(D->xt[i], 0, std::max<size_t>(16, rows_x * kp * D->w), st));
     }
     void** vbufs[] = {&D->Ep, &D->Qp, &D->Qdp, &D->Qvp, &D->Yp, &D->Qip};
     for (void** b : vbufs) {
         CK(cudaMalloc(b, std::max<size_t>(16, rows * kp * D->w)));
-        CK(cudaMemset(*b, 0, std::max<size_t>(16, rows * kp * D->w)));
+        CK(cudaMemsetAsync(*b, 0, std::max<size_t>(16, rows * kp * D->w), st));
     }
     for (void*& b : D->pv) CK(cudaMalloc(&b, std::max<size_t>(16, rows * D->w)));
     int nsm = 148;
@@ -2327,12 +2332,12 @@ int ensure_scratch(DeviceHMat* D, int kp) {
     const int64_t nblk = (int64_t)nsm * std::max(kMaxCtasPerSm, kMaxCtasRow);
     if (D->partial) cudaFree(D->partial);
     CK(cudaMalloc((void**)&D->partial, (size_t)2 * nblk * kp * 8));
-    CK(cudaMemset(D->partial, 0, (size_t)2 * nblk * kp * 8));
+    CK(cudaMemsetAsync(D->partial, 0, (size_t)2 * nblk * kp * 8, st));
     if (D->enorm2) cudaFree(D->enorm2);
     if (D->resid) cudaFree(D->resid);
     CK(cudaMalloc((void**)&D->enorm2, (size_t)kp * 8));
     CK(cudaMalloc((void**)&D->resid, (size_t)kp * 8));
-    CK(cudaMemset(D->resid, 0, (size_t)kp * 8));
+    CK(cudaMemsetAsync(D->resid, 0, (size_t)kp * 8, st));
     if (D->resid_host) cudaFreeHost(D->resid_host);
     CK(cudaMallocHost((void**)&D->resid_host, (size_t)2 * kp * 8));
     D->kp_cap = kp;
@@ -2550,11 +2555,13 @@ int launch_res(Handle* h, HotArgs& a, cudaStream_t st) {
             cfg.blockDim = dim3(kRW * 32);
             cfg.dynamicSmemBytes = smem;
             cfg.stream = st;
-            cudaLaunchAttribute at[1];
+            cudaLaunchAttribute at[2];
             at[0].id = cudaLaunchAttributeClusterDimension;
             at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+            at[1].id = cudaLaunchAttributeCooperative;      // co-residency for the software grid barrier
+            at[1].val.cooperative = 1;
             cfg.attrs = at;
-            cfg.numAttrs = 1;
+            cfg.numAttrs = 2;
             int nclusters = 0;
             CK(cudaOccupancyMaxActiveClusters(&nclusters, (const void*)fn, &cfg));
             if (nclusters * 2 < grid) {                // not all pairs co-resident: use the streaming path
@@ -2660,7 +2667,7 @@ void stage_stats(DeviceHMat* D, int slot, int k, int* iters_done, double* max_re
 size_t rows_tail_off(const DeviceHMat* D, int kp) { return ((size_t)D->rows_max * kp * D->w + 15) & ~(size_t)15; }
 size_t rows_slot(const DeviceHMat* D, int kp) { return (rows_tail_off(D, kp) + (size_t)kp * 8 + 15) & ~(size_t)15; }
 
-int ensure_rows_bufs(DeviceHMat* D, int kp) {
+int ensure_rows_bufs(DeviceHMat* D, int kp, cudaStream_t st) {
     const size_t slot = rows_slot(D, kp);
     if (slot <= D->slot_cap) return VF_OK;
     if (D->send) cudaFree(D->send);
@@ -2668,7 +2675,7 @@ int ensure_rows_bufs(DeviceHMat* D, int kp) {
     D->send = D->recv = nullptr;
     CK(cudaMalloc((void**)&D->send, slot));
     CK(cudaMalloc((void**)&D->recv, slot * D->world));
-    CK(cudaMemset(D->send, 0, slot));
+    CK(cudaMemsetAsync(D->send, 0, slot, st));
     D->slot_cap = slot;
     return VF_OK;
 }
@@ -2680,7 +2687,7 @@ template <typename T>
 int rows_allgather_buf(Handle* h, void* buf, int kp, cudaStream_t st) {
     DeviceHMat* D = h->dev;
     int rc;
-    if ((rc = ensure_rows_bufs(D, kp))) return rc;
+    if ((rc = ensure_rows_bufs(D, kp, st))) return rc;
     const size_t slot = rows_slot(D, kp);
     const int64_t own = D->row_hi - D->row_lo;
     rows_pack_kernel<T><<<rows_grid(own * kp), 256, 0, st>>>(nullptr, nullptr, nullptr, (const T*)buf, D->row_lo, own,
@@ -2706,7 +2713,7 @@ int iterate_rows(Handle* h, int k, int kp, const void* rho, int clamp, int iters
     if (iters <= 0) return VF_OK;
     if (!h->comm) return set_error(VF_EINVAL, "solve on a row-sharded handle needs vf_comm_init");
     int rc;
-    if ((rc = ensure_rows_bufs(D, kp))) return rc;
+    if ((rc = ensure_rows_bufs(D, kp, st))) return rc;
     const size_t slot = rows_slot(D, kp), toff = rows_tail_off(D, kp);
     const int64_t own = D->row_hi - D->row_lo;
     CK(cudaMemsetAsync(D->ctl, 0, sizeof(Ctl), st));
@@ -2769,7 +2776,7 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     int rc;
     if ((rc = check_k(nrhs)) || (rc = stream_of(h, &st))) return rc;
     const int kp = pad_k(nrhs);
-    if ((rc = ensure_scratch(D, kp))) return rc;
+    if ((rc = ensure_scratch(D, kp, st))) return rc;
     reset_counters(h);
     const size_t vb = (size_t)D->N * nrhs * sizeof(T);
     const void* Xd;
@@ -2843,7 +2850,10 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     }
     CK(cudaGetLastError());
     if ((rc = stage_out_copy(Y, Yd, vb, st))) return rc;
-    if (Yd != Y || h->timing) CK(cudaStreamSynchronize(st));
+    // a host input is copied asynchronously from the caller's buffer: the call
+    // must not return while that copy may still read it (vf.h: no reference
+    // is kept after return)
+    if (Yd != Y || Xd != X || h->timing) CK(cudaStreamSynchronize(st));
     if (h->timing) collect_timing(h);
     return VF_OK;
 }
@@ -2855,7 +2865,7 @@ int radiosity_impl(Handle* h, const void* E, const void* rho, void* B, int nrhs,
     int rc;
     if ((rc = check_k(nrhs)) || (rc = stream_of(h, &st))) return rc;
     const int kp = pad_k(nrhs);
-    if ((rc = ensure_scratch(D, kp))) return rc;
+    if ((rc = ensure_scratch(D, kp, st))) return rc;
     reset_counters(h);
     const size_t vb = (size_t)D->N * nrhs * sizeof(T);
     const void *Ed, *rd;
@@ -2893,7 +2903,7 @@ int thermal_impl(Handle* h, const void* Qdir, const void* alb, const void* emi, 
     int rc;
     if ((rc = check_k(nrhs)) || (rc = stream_of(h, &st))) return rc;
     const int kp = pad_k(nrhs);
-    if ((rc = ensure_scratch(D, kp))) return rc;
+    if ((rc = ensure_scratch(D, kp, st))) return rc;
     reset_counters(h);
     const size_t vb = (size_t)D->N * nrhs * sizeof(T), pb = (size_t)D->N * sizeof(T);
     const void *Qd, *ad, *ed;

@@ -478,8 +478,9 @@ SvdResult estimate_rank(int64_t mu, int64_t nv, const double* dense, const int64
                 for (int64_t p = 0; p < q; ++p) R.V[j * q + p] = T.V[j * T.l + p];
             return R;
         }
-        // reading A5: stop once k >= min(m,n)/2 or w k (m+n) >= nbytes(F_IJ)
-        if (2 * k >= r || (int64_t)w * k * (mu + nv) >= target_bytes || complete) return R;
+        // reading A5: the doubling stops once w k (m'+n') >= nbytes(F_IJ) (then every
+        // q > k fails eq. nbytes-comparison) or the spectrum is complete (k >= rank)
+        if ((int64_t)w * k * (mu + nv) >= target_bytes || complete) return R;
     }
 }
 

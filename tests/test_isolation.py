@@ -50,7 +50,7 @@ def test_bench_uses_the_oracle_only_in_its_cpu_legs():
     for node in ast.walk(tree):
         for ch in ast.iter_child_nodes(node):
             parents[ch] = node
-    helpers = {"oracle_sample", "oracle_rows", "run_reference"}
+    helpers = {"oracle_sample", "oracle_rows", "run_reference", "run_reference_terrain"}
     gated = {"run_gpu", "run_terrain"}
     for node in ast.walk(tree):
         uses = (isinstance(node, ast.Import) and any(a.name.split(".")[0] == "oracle" for a in node.names)) or \

@@ -283,7 +283,7 @@ def test_P6_cfg1_values():
 def test_P6_shadow_temperature_approached_under_refinement():
     g = json.load(open(os.path.join(GOLD, "cap_cfg1_survey.json")))
     Tex = oracle.cap_T_global(g["S"], g["e_sun_deg"], oracle.cap_f(5.0), g["albedo"], g["emiss"], "shadow")
-    errs = []
+    errs, errs_lit = [], []
     for nfib in (180, 770, 3000):
         S = oracle.Scene(*sg.cap_mesh(nfib, int(round(90 * math.sqrt(nfib / 770)))))
         F = S.F_dense()
@@ -293,8 +293,14 @@ def test_P6_shadow_temperature_approached_under_refinement():
         sh = Q[:, 0] == 0
         T = out["T"][sh, 0]
         errs.append(np.linalg.norm(T - Tex) / (math.sqrt(T.size) * Tex))
+        # sunlit crater facets: P:370-377 'lit' branch, sin e_local = n_i.s = Q_i / S
+        lit = ~sh
+        Tl = np.array([oracle.cap_T_global(g["S"], g["e_sun_deg"], oracle.cap_f(5.0), g["albedo"], g["emiss"],
+                                           "lit", q / g["S"]) for q in Q[lit, 0]])
+        errs_lit.append(np.linalg.norm(out["T"][lit, 0] - Tl) / np.linalg.norm(Tl))
     assert errs[0] > errs[1] > errs[2]
     assert errs[2] < 0.02
+    assert errs_lit[0] > errs_lit[1] > errs_lit[2] and errs_lit[2] < 5e-4
 
 
 # --------------------------------------------------------- hierarchical (Alg. 2-5)
@@ -377,3 +383,98 @@ def test_hmatvec_zero_cases():
     H = hm.compress(S.x, F, 1e-5, min_size=256)
     assert H.leaves() == [] and H.nbytes == 0
     assert np.all(hm.hmatvec(H, np.ones((S.N, 2))) == 0)
+
+
+# ------------------------------------------------------------ round-2 pins
+
+def test_alg3_accepts_rank_above_half_min():
+    """Alg. 3 ("Increase k ... jump back") has no k >= min(m,n)/2
+    stop: a 100 x 100 block whose 50 x 50 nonzero core has exactly 33 unit
+    singular values (rank 33 > 50/2) is accepted at q = 33, because its SVD
+    (w q (m'+n') + w q + 4 (m'+n') = 26400 + 264 + 400 = 27,064 B, reading A7/A8)
+    is smaller than its CSR (8 (100+1) + 12 x 2500 = 30,808 B)."""
+    rng = np.random.default_rng(11)
+    Qa, _ = np.linalg.qr(rng.standard_normal((50, 50)))
+    Qb, _ = np.linalg.qr(rng.standard_normal((50, 50)))
+    core = Qa[:, :33] @ Qb[:, :33].T                       # singular values: 33 x 1.0, 17 x 0
+    B = np.zeros((100, 100))
+    rows, cols = rng.choice(100, 50, replace=False), rng.choice(100, 50, replace=False)
+    B[np.ix_(np.sort(rows), np.sort(cols))] = core
+    assert np.count_nonzero(B) == 2500
+    assert hm.nbytes_csr(100, 2500, 8) == 30808
+    assert hm.nbytes_svd(33, 50, 50, 8) == 27064
+    out = hm.estimate_rank(B, 1e-5, 8)
+    assert out is not None
+    q, ur, vr, U, S, V = out
+    assert q == 33
+    assert np.array_equal(ur, np.sort(rows)) and np.array_equal(vr, np.sort(cols))
+    R = np.zeros_like(B)
+    R[np.ix_(ur, vr)] = (U * S) @ V.T
+    assert np.abs(R - B).max() < 1e-12
+
+
+def test_alg3_rejects_when_factor_bytes_reach_csr_bytes():
+    """The one stop rule left (A5): w k (m'+n') >= nbytes(F_IJ) -> no q > k can
+    pass eq. nbytes-comparison.  A full-rank 40 x 40 random block never passes."""
+    rng = np.random.default_rng(12)
+    assert hm.estimate_rank(rng.random((40, 40)), 1e-5, 8) is None
+
+
+def test_F_csr_rows_and_apply_csr_match_dense():
+    """or_viewfactor_csr_rows / or_apply_csr (the exact-F reference of the
+    full-size GPU parity and of bench.py's parity) on a rows subset that is
+    neither 0..n nor sorted: every stored row equals the dense row (pinned by
+    P1/P3/P7) and holds every nonzero of it; the apply equals numpy's product."""
+    S = oracle.Scene(*sg.rough_small_mesh(14, amp=0.3))        # 392 facets, occluded
+    Fd = S.F_dense()
+    rng = np.random.default_rng(5)
+    rows = rng.choice(S.N, 97, replace=False)                  # unsorted, gaps
+    rows[3] = rows[0]                                          # a repeated row
+    rowptr, cols, vals = S.F_csr_rows(rows)
+    assert rowptr[0] == 0 and rowptr.size == rows.size + 1
+    for i, r in enumerate(rows):
+        c, v = cols[rowptr[i]:rowptr[i + 1]], vals[rowptr[i]:rowptr[i + 1]]
+        dense_row = np.zeros(S.N)
+        dense_row[c] = v
+        assert np.array_equal(dense_row, Fd[r]), r             # bitwise, incl. the zero pattern
+        assert np.all(v != 0) and np.all(np.diff(c) > 0)
+    assert rowptr[-1] == np.count_nonzero(Fd[rows])
+    # the grid accelerator and brute force give the same rows
+    rp2, c2, v2 = S.F_csr_rows(rows, grid=0)
+    assert np.array_equal(rp2, rowptr) and np.array_equal(c2, cols) and np.array_equal(v2, vals)
+    X = sg.random_rhs(S.N, 3)
+    Y = oracle.apply_csr((rowptr, cols, vals), X)
+    Yn = Fd[rows] @ X
+    assert np.abs(Y - Yn).max() <= 1e-14 * np.abs(Yn).max()
+    assert np.array_equal(Y, oracle.apply_dense(Fd, X)[rows])  # same per-row order -> bitwise
+
+
+def test_quadtree_splits_at_midpoint_not_median():
+    """Reading A1: split at x_mid = (x_min + x_max)/2,
+    y_mid likewise, a coordinate equal to mid goes to the upper half.  On this
+    asymmetric set the median split would put 2 points on each side of x."""
+    xy = np.array([[0.0, 0.0], [0.1, 0.3], [0.2, 0.1], [0.3, 0.2], [10.0, 10.0]])
+    root, perm = hm.quadtree(xy, 8, 1)
+    # x_mid = y_mid = 5: four points lower-left (I1), one upper-right (I4)
+    assert [c.size for c in root.children] == [4, 1]
+    assert sorted(perm[root.children[0].start:root.children[0].stop].tolist()) == [0, 1, 2, 3]
+    assert perm[root.children[1].start] == 4
+    # ties: x = x_mid and y = y_mid go to the upper halves
+    xy = np.array([[0.0, 0.0], [4.0, 4.0], [8.0, 8.0], [4.0, 0.0], [0.0, 4.0]])
+    root, perm = hm.quadtree(xy, 8, 1)
+    sets = [sorted(perm[c.start:c.stop].tolist()) for c in root.children]
+    # I1 = {x<4,y<4}: 0; I2 = {x<4,y>=4}: 4; I3 = {x>=4,y<4}: 3; I4 = {x>=4,y>=4}: 1, 2
+    assert sets == [[0], [4], [3], [1, 2]]
+
+
+def test_cap_T_global_outside_is_flat_plane_equilibrium():
+    """P:370-377 'outside' branch: eps sigma T^4 = (1 - alpha) S sin e for a
+    facet that sees no other facet -- the oracle's thermal chain on a flat
+    plane (F = 0, P9) must give exactly this temperature."""
+    S = oracle.Scene(*sg.flat_plane_mesh(6))
+    F = S.F_dense()
+    e = 23.0
+    Q = S.insolation(sg.sun_dirs(e, 1), S=1365.0)
+    out = oracle.thermal(lambda X: oracle.apply_dense(F, X), Q, np.full(S.N, 0.12), np.full(S.N, 0.95), 1e-12, 20)
+    Tout = oracle.cap_T_global(1365.0, e, 0.1, 0.12, 0.95, "outside")
+    assert np.allclose(out["T"][:, 0], Tout, rtol=1e-13)
