@@ -614,8 +614,13 @@ def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
     solve_rows = 4 if rows_mode else 1
     hbm = pk.get("hbm_gbs", 6559.0)
 
+    stream = info.get("stream_chunks", 0) > 0 and not rows_mode
+
     def alg_bytes(kp):
-        return (info["p1_bytes"] + info["p2_bytes"] + (info["p1_src_rows"] + info["p2_src_rows"]) * kp * w
+        # F-hat payload: the chunk stream's values + 16-bit CSR offsets + phase-1 row lists
+        # for nrhs = 1 (stream_k1_kernel), else values + 32-bit indices of the row layout
+        fh = info["stream_payload_bytes"] if (stream and kp == 1) else info["p1_bytes"] + info["p2_bytes"]
+        return (fh + (info["p1_src_rows"] + info["p2_src_rows"]) * kp * w
                 + info["t_rows"] * kp * w + info["active_rows"] * kp * w * solve_rows)
     avg = tm["ms_hot"] / max(tm["l_hot"], 1)
     flops_app = info["alg_flops_per_col"] * k
@@ -644,13 +649,19 @@ def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
         bound = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm,
                  "peak_basis": f"{pk_kind} MEASURED_PEAKS.json hbm_gbs (copy bandwidth, 'burst' figure for a kernel "
                                "timed alone)"}
-    kern = info.get("kernel_name_k1" if max(chunks) <= 2 else "kernel_name_batched") or (
-        "hot_kernel<T,1,1,M_MATVEC>" if max(chunks) <= 2 else "hot_kernel<T,32,VEC,M_MATVEC>")
+    tn = "double" if dt == "f64" else "float"
+    if max(chunks) <= 2:
+        kern = (f"stream_k1_kernel<{tn}> (bulk-copy chunk stream: phase 1 T = S V^T x, warp-granular grid barrier, "
+                "phase 2 row-owner accumulate)" if stream and max(chunks) == 1 else f"hot_kernel<{tn},1,VEC,M_MATVEC>")
+    else:
+        kern = f"hot_kernel<{tn},32,VEC,M_MATVEC> (wide per-row: warp across 32 VEC columns)"
     return {**bound, "traffic": traffic, "traffic_source": traffic_src,
             "kernel": ("(ROWS mode, one Jacobi iteration per launch) " if rows_mode else "") + kern,
             "achieved_gbs": ach_gbs, "hbm_frac": ach_gbs / hbm, "hbm_frac_vs_8TBs_spec": ach_gbs / 8000.0,
             "avg_launch_ms": avg, "launches": tm["l_hot"], "alg_bytes_per_apply": bytes_app,
             "alg_flops_per_apply": flops_app, "achieved_tflops": ach_tf,
+            "stream_bytes_per_apply": (info["stream_payload_bytes"] + info["stream_meta_bytes"]) if stream else None,
+            "stream_meta_bytes": info["stream_meta_bytes"] if stream else None,
             "column_chunks": chunks[:4] + (["..."] if len(chunks) > 4 else []),
             "share_of_step": tm["ms_hot"] / tm["t_ms"] if tm["t_ms"] > 0 else None}
 

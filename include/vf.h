@@ -204,6 +204,12 @@ typedef struct {
     int64_t groups1, groups2;  /* row groups of the batched layout (phase 1 / 2)      */
     int64_t resident;      /* 1: batched applies (nrhs >= 9) keep F-hat in shared
                               memory across iterations (res_kernel); 0: streamed    */
+    /* chunk-stream layout of the nrhs = 1 apply (0 if absent): the F-hat bytes one
+       apply streams = payload (values, 16-bit CSR column offsets, phase-1 row
+       lists) + meta (chunk headers, piece descriptors, 16-B padding)            */
+    int64_t stream_payload_bytes;
+    int64_t stream_meta_bytes;
+    int64_t stream_chunks;
 } vf_info_t;
 
 int vf_info(vf_handle h, vf_info_t* out);

@@ -36,6 +36,9 @@
 #include <vector>
 
 #include "vf_internal.h"
+#include "vf_stream.h"
+
+#include <omp.h>
 
 namespace vf {
 
@@ -1700,12 +1703,234 @@ struct DeviceHMat {
     unsigned char* send = nullptr;
     unsigned char* recv = nullptr;
     size_t slot_cap = 0;
+    // chunk-stream layout of the nrhs = 1 apply (vf_stream.cu)
+    stream::DevLayout sl;
     // staging for host pointers
     void* stage[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     size_t stage_cap[6] = {0, 0, 0, 0, 0, 0};
 };
 
 namespace {
+
+// ---- chunk-stream layout of the nrhs = 1 apply (vf_stream.h / vf_stream.cu).
+// Phase-1 items: (row group g of <= 16 consecutive T rows of one SVD block,
+// part of its V rows); chunk = header, [int32 X rows if J_b is not a
+// contiguous run], then t-major values S_t V[j, t] (S folded in) for nj V rows
+// (a multiple of 32: one per lane).  Phase-2 items: one active tree row;
+// chunk = header, <= 32 piece descriptors, the pieces' values back to back,
+// then the u16 column offsets of its CSR pieces.  A row's merged CSR columns
+// are cut into runs whose span fits 16 bits (column = run base + offset).
+// Items are laid out longest first (the queue order of the kernel).
+template <typename T>
+void build_stream(int64_t N, const std::vector<T>& vals, const std::vector<int32_t>& idx,
+                  const std::vector<Seg>& segs, const std::vector<int64_t>& p2_segptr,
+                  const std::vector<int32_t>& p2_rows, const std::vector<Group>& g1v,
+                  const std::vector<GSeg>& gsegv, const std::vector<int64_t>& gvov,
+                  const std::vector<int32_t>& grow1v, const std::vector<T>& p1_scale, stream::HostLayout& L) {
+    using namespace stream;
+    constexpr int w = (int)sizeof(T);
+    auto p16 = [](int64_t b) { return (b + 15) & ~(int64_t)15; };
+    // ---------------- phase 1
+    struct P1Plan { int64_t g; int jb, je; int64_t bytes; int nch; };
+    std::vector<P1Plan> plan1;
+    std::vector<int32_t> g_np(g1v.size(), 1);
+    auto nj_max = [&](int G, bool gather) {
+        const int64_t per32 = 32 * ((int64_t)w * G + (gather ? 4 : 0));
+        return (int)std::max<int64_t>(1, (kSlot - 16) / per32) * 32;
+    };
+    // V rows per phase-1 item and the span of a 16-bit CSR run; VF_P1_PART /
+    // VF_U16_SPAN override them (tests force multi-part groups and many runs)
+    const int p1part = getenv("VF_P1_PART") ? std::max(32, atoi(getenv("VF_P1_PART"))) : kP1Part;
+    const int64_t span = getenv("VF_U16_SPAN") ? std::min(65536, std::max(2, atoi(getenv("VF_U16_SPAN")))) : 65536;
+    for (int64_t g = 0; g < (int64_t)g1v.size(); ++g) {
+        const GSeg& sg = gsegv[g1v[g].seg_off];
+        const int len = sg.len, G = g1v[g].nrows;
+        const int np = std::max(1, (len + p1part - 1) / p1part);
+        g_np[g] = np;
+        const int njm = nj_max(G, sg.kind != 0);
+        for (int p = 0; p < np; ++p) {
+            const int jb = (int)((int64_t)len * p / np), je = (int)((int64_t)len * (p + 1) / np);
+            int64_t by = 0; int nch = 0;
+            for (int j0 = jb; j0 < je || (j0 == jb && je == jb); j0 += njm) {
+                const int nj = std::min(njm, je - j0);
+                by += 16 + (sg.kind ? p16(4 * (int64_t)nj) : 0) + p16((int64_t)w * G * nj);
+                ++nch;
+                if (je == jb) break;
+            }
+            plan1.push_back({g, jb, je, by, nch});
+        }
+    }
+    // ---------------- phase 2 pieces per row
+    struct PPiece { int kind; int32_t src; int64_t voff; int64_t len; int64_t coff; };   // coff: CSR column offset in idx
+    auto row_pieces = [&](int64_t r, std::vector<PPiece>& out) {
+        out.clear();
+        for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1]; ++q) {
+            const Seg& sg = segs[q];
+            if (sg.kind == 0) {
+                if (sg.src >= N) out.push_back({1, (int32_t)(sg.src - N), sg.val_off, sg.len, 0});
+                else out.push_back({0, (int32_t)sg.src, sg.val_off, sg.len, 0});
+            } else {
+                for (int64_t e = 0; e < sg.len;) {         // runs of columns within a 16-bit span
+                    const int32_t base = idx[sg.src + e];
+                    int64_t f = e + 1;
+                    while (f < sg.len && idx[sg.src + f] - base < span) ++f;
+                    out.push_back({2, base, sg.val_off + e, f - e, sg.src + e});
+                    e = f;
+                }
+            }
+        }
+    };
+    // greedy packing of a row's pieces into chunks; emit when dst != nullptr
+    auto pack_row = [&](int32_t orow, const std::vector<PPiece>& pcs, unsigned char* dst, int64_t* coff_out,
+                        int64_t base_off, int64_t* nbytes, int* nchunks, int64_t* payload) {
+        struct Cur { int np = 0; int64_t nt = 0, nc = 0; } c;
+        std::vector<std::array<int64_t, 5>> cp;   // (piece, first term, count) of the open chunk
+        int64_t off = 0; int nch = 0; int64_t pay = 0;
+        auto cbytes = [&](int np, int64_t nt, int64_t nc) { return 16 + p16(8 * np) + p16(w * nt) + p16(2 * nc); };
+        auto flush = [&](bool last) {
+            const int64_t by = cbytes(c.np, c.nt, c.nc);
+            if (dst) {
+                unsigned char* ch = dst + off;
+                std::memset(ch, 0, (size_t)by);
+                Hdr hd{orow, (int16_t)c.np, (int16_t)(last ? 1 : 0), (int32_t)c.nt, 0};
+                std::memcpy(ch, &hd, 16);
+                Piece* pd = reinterpret_cast<Piece*>(ch + 16);
+                T* vv = reinterpret_cast<T*>(ch + 16 + p16(8 * c.np));
+                uint16_t* ii = reinterpret_cast<uint16_t*>(reinterpret_cast<unsigned char*>(vv) + p16(w * c.nt));
+                int64_t t = 0, ci = 0;
+                for (int k = 0; k < c.np; ++k) {
+                    const PPiece& P = pcs[cp[k][0]];
+                    const int64_t e0 = cp[k][1], n = cp[k][2];
+                    pd[k].src = P.kind == 2 ? P.src : (int32_t)(P.src + e0);
+                    pd[k].len = (uint16_t)n;
+                    pd[k].kind = (uint8_t)P.kind;
+                    pd[k].pad = 0;
+                    for (int64_t e = 0; e < n; ++e) vv[t++] = vals[P.voff + e0 + e];
+                    if (P.kind == 2)
+                        for (int64_t e = 0; e < n; ++e) ii[ci++] = (uint16_t)(idx[P.coff + e0 + e] - P.src);
+                }
+                if (coff_out) coff_out[nch] = base_off + off;
+            }
+            pay += (int64_t)w * c.nt + 2 * c.nc;
+            off += by;
+            ++nch;
+            c = Cur{};
+            cp.clear();
+        };
+        for (size_t k = 0; k < pcs.size(); ++k) {
+            const PPiece& P = pcs[k];
+            const int per = w + (P.kind == 2 ? 2 : 0);
+            for (int64_t e = 0; e < P.len;) {
+                if (c.np == kMaxPieces) flush(false);
+                const int64_t avail = kSlot - 16 - p16(8 * (c.np + 1)) - w * c.nt - 2 * c.nc - 32;
+                int64_t a = std::min<int64_t>({P.len - e, avail / per, 65535});
+                if (a <= 0) { flush(false); continue; }
+                cp.push_back({(int64_t)k, e, a, 0, 0});
+                c.np++; c.nt += a; if (P.kind == 2) c.nc += a;
+                e += a;
+            }
+        }
+        if (c.np > 0 || nch == 0) flush(true);
+        *nbytes = off; *nchunks = nch; *payload = pay;
+    };
+    const int64_t n2 = (int64_t)p2_rows.size();
+    std::vector<int64_t> rbytes(n2), rpay(n2);
+    std::vector<int> rnch(n2);
+#pragma omp parallel
+    {
+        std::vector<PPiece> pcs;
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t r = 0; r < n2; ++r) {
+            row_pieces(r, pcs);
+            pack_row(p2_rows[r], pcs, nullptr, nullptr, 0, &rbytes[r], &rnch[r], &rpay[r]);
+        }
+    }
+    // ---------------- order (longest first), offsets
+    std::vector<int64_t> o1(plan1.size()), o2(n2);
+    std::iota(o1.begin(), o1.end(), 0);
+    std::iota(o2.begin(), o2.end(), 0);
+    std::stable_sort(o1.begin(), o1.end(), [&](int64_t x, int64_t y) { return plan1[x].bytes > plan1[y].bytes; });
+    std::stable_sort(o2.begin(), o2.end(), [&](int64_t x, int64_t y) { return rbytes[x] > rbytes[y]; });
+    const int64_t n1 = (int64_t)plan1.size();
+    L.n1 = n1; L.n2 = n2; L.ngroups = (int64_t)g1v.size();
+    L.ic0.assign(n1 + n2 + 1, 0);
+    std::vector<int64_t> boff(n1 + n2 + 1, 0);
+    for (int64_t i = 0; i < n1; ++i) {
+        L.ic0[i + 1] = L.ic0[i] + plan1[o1[i]].nch;
+        boff[i + 1] = boff[i] + plan1[o1[i]].bytes;
+    }
+    for (int64_t i = 0; i < n2; ++i) {
+        L.ic0[n1 + i + 1] = L.ic0[n1 + i] + rnch[o2[i]];
+        boff[n1 + i + 1] = boff[n1 + i] + rbytes[o2[i]];
+    }
+    const int64_t total = boff[n1 + n2], nchunks = L.ic0[n1 + n2];
+    if (nchunks >= INT32_MAX) { L = HostLayout{}; return; }
+    L.bytes.assign((size_t)total, 0);
+    L.coff.assign((size_t)nchunks + 1, 0);
+    L.coff[nchunks] = total;
+    // phase-1 item table (scratch bases of multi-part groups)
+    std::vector<int32_t> sbase(g1v.size(), 0);
+    int64_t nscr = 0;
+    for (int64_t g = 0; g < (int64_t)g1v.size(); ++g)
+        if (g_np[g] > 1) { sbase[g] = (int32_t)nscr; nscr += g_np[g]; }
+    L.nscratch = nscr;
+    L.p1.resize(n1);
+    int64_t pay1 = 0;
+    for (int64_t i = 0; i < n1; ++i) {
+        const P1Plan& P = plan1[o1[i]];
+        const Group& Gr = g1v[P.g];
+        const int G = Gr.nrows;
+        const GSeg& sg = gsegv[Gr.seg_off];
+        const int32_t t0 = grow1v[P.g * kGroup];
+        for (int r = 1; r < G; ++r)
+            if (grow1v[P.g * kGroup + r] != t0 + r) { L = HostLayout{}; return; }   // T rows must be consecutive
+        int pidx = 0;
+        for (int64_t q = o1[i]; q > 0 && plan1[q - 1].g == P.g; --q) ++pidx;
+        L.p1[i] = P1Item{t0, (int16_t)G, (int16_t)g_np[P.g], pidx, (int32_t)P.g, sbase[P.g], 0};
+        const int njm = nj_max(G, sg.kind != 0);
+        int64_t off = boff[i];
+        int c = L.ic0[i];
+        for (int j0 = P.jb; j0 < P.je || (j0 == P.jb && P.je == P.jb); j0 += njm) {
+            const int nj = std::min(njm, P.je - j0);
+            unsigned char* ch = L.bytes.data() + off;
+            Hdr hd{(int32_t)i, (int16_t)G, (int16_t)(2 | (j0 + nj >= P.je ? 1 : 0)), nj,
+                   sg.kind ? -1 : (int32_t)(sg.src + j0)};
+            std::memcpy(ch, &hd, 16);
+            unsigned char* pp = ch + 16;
+            if (sg.kind) {
+                for (int jj = 0; jj < nj; ++jj) reinterpret_cast<int32_t*>(pp)[jj] = idx[sg.src + j0 + jj];
+                pp += p16(4 * (int64_t)nj);
+                pay1 += 4 * (int64_t)nj;
+            }
+            T* V = reinterpret_cast<T*>(pp);
+            for (int t = 0; t < G; ++t) {
+                const T sc = p1_scale[t0 + t];
+                const int64_t vo = gvov[Gr.seg_off * kGroup + t];
+                for (int jj = 0; jj < nj; ++jj) V[(int64_t)t * nj + jj] = vals[vo + j0 + jj] * sc;
+            }
+            pay1 += (int64_t)w * G * nj;
+            L.coff[c++] = off;
+            off += 16 + (sg.kind ? p16(4 * (int64_t)nj) : 0) + p16((int64_t)w * G * nj);
+            if (P.je == P.jb) break;
+        }
+    }
+    int64_t pay2 = 0;
+#pragma omp parallel reduction(+ : pay2)
+    {
+        std::vector<PPiece> pcs;
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t i = 0; i < n2; ++i) {
+            const int64_t r = o2[i];
+            row_pieces(r, pcs);
+            int64_t by, pay; int nch;
+            pack_row(p2_rows[r], pcs, L.bytes.data() + boff[n1 + i], L.coff.data() + L.ic0[n1 + i], boff[n1 + i], &by,
+                     &nch, &pay);
+            pay2 += pay;
+        }
+    }
+    L.payload_bytes = pay1 + pay2;
+    L.meta_bytes = total - L.payload_bytes;
+}
 
 template <typename T>
 int upload_impl(Handle* h, DeviceHMat* D) {
@@ -1853,6 +2078,38 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     if (segs.empty()) segs.push_back(Seg{0, 0, 0, 0});
     D->n_p1 = (int64_t)p1_rows.size();
     D->n_p2 = (int64_t)p2_rows.size();
+    if (getenv("VF_LAYOUT_STATS")) {          // structure of the phase-2 rows (layout design)
+        int64_t hseg[8] = {0}, hlen[3][8] = {{0}}, hrow[10] = {0}, tot[3] = {0, 0, 0}, nsg[3] = {0, 0, 0};
+        auto bin = [](int64_t v, int nb) { int b = 0; while (v > 1 && b < nb - 1) { v >>= 2; ++b; } return b; };
+        for (int64_t r = 0; r < (int64_t)p2_rows.size(); ++r) {
+            const int64_t ns = p2_segptr[r + 1] - p2_segptr[r];
+            hseg[bin(ns, 8)]++;
+            int64_t rb = 0;
+            for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1]; ++q) {
+                const Seg& sg = segs[q];
+                const int k = sg.kind ? 2 : (sg.src >= N ? 1 : 0);
+                hlen[k][bin(sg.len, 8)]++;
+                tot[k] += sg.len;
+                nsg[k]++;
+                rb += sg.len * (int64_t)sizeof(T) + (sg.kind ? 4 * sg.len : 0);
+            }
+            hrow[bin(rb / 256, 10)]++;
+        }
+        fprintf(stderr, "[vf layout] rows %lld; terms dense %lld (%lld segs) U %lld (%lld segs) csr %lld (%lld segs)\n",
+                (long long)p2_rows.size(), (long long)tot[0], (long long)nsg[0], (long long)tot[1], (long long)nsg[1],
+                (long long)tot[2], (long long)nsg[2]);
+        fprintf(stderr, "[vf layout] segs/row hist (bins 1,4,16,..):");
+        for (int b = 0; b < 8; ++b) fprintf(stderr, " %lld", (long long)hseg[b]);
+        for (int k = 0; k < 3; ++k) {
+            fprintf(stderr, "\n[vf layout] len hist kind %d:", k);
+            for (int b = 0; b < 8; ++b) fprintf(stderr, " %lld", (long long)hlen[k][b]);
+        }
+        fprintf(stderr, "\n[vf layout] row bytes hist (256 B x 1,4,16,..):");
+        for (int b = 0; b < 10; ++b) fprintf(stderr, " %lld", (long long)hrow[b]);
+        int64_t g1n = 0, g1t = 0;
+        for (int64_t r = 0; r < (int64_t)p1_rows.size(); ++r) { g1n++; g1t += segs[p1_segptr[r]].len; }
+        fprintf(stderr, "\n[vf layout] phase-1 T rows %lld, V terms %lld\n", (long long)g1n, (long long)g1t);
+    }
     D->alg_bytes = alg_bytes;
     D->alg_flops_per_col = alg_flops;
     D->p2_bytes = alg_bytes - D->p1_bytes;
@@ -2249,6 +2506,15 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             D->res_grid = nsm;
             D->res_wcap = (int)std::max<int64_t>(wmax, EPL);
             D->res_scap = (int)std::max<int64_t>(smax, 4);
+        }
+    }
+    if (!h->sharded && !getenv("VF_NO_STREAM")) {
+        // the nrhs = 1 chunk stream (an F-hat copy in the layout of vf_stream.cu)
+        stream::HostLayout SL;
+        build_stream<T>(N, vals, idx, segs, p2_segptr, p2_rows, g1v, gsegv, gvov, grow1v, p1_scale, SL);
+        if (!SL.coff.empty()) {
+            if ((rc = stream::upload(SL, (int)sizeof(T), NT, &D->sl))) return rc;
+            D->bytes += D->sl.device_bytes;
         }
     }
     CK(cudaMalloc((void**)&D->ctl, sizeof(Ctl)));
@@ -2805,7 +3071,17 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
         }
         const bool rows = D->world > 1 || h->comm;
         if (rows) CK(cudaMemsetAsync(D->Yp, 0, (size_t)D->N * kpn * sizeof(T), st));   // rows of other ranks: 0 ...
-        if ((rc = launch_hot<T, M_MATVEC>(h, a, st))) return rc;
+        if (kpn == 1 && D->sl.ok && !rows) {
+            int grid = 0;
+            {
+                Timer tm(h, st, 2);
+                if ((rc = stream::matvec_k1(D->sl, D->dtype, D->xt[0], D->Yp, st, &grid))) return rc;
+            }
+            h->launches_total++;
+            D->last_grid = grid;
+        } else if ((rc = launch_hot<T, M_MATVEC>(h, a, st))) {
+            return rc;
+        }
         if (rows && h->comm && (rc = rows_allgather_buf<T>(h, D->Yp, kpn, st))) return rc;   // ... or gathered
         launch_permute_out<T>(h, D->Yp, n, kpn, true, Yc, st);
         return VF_OK;
@@ -2994,6 +3270,7 @@ void device_free(Handle* h) {
     if (D->resid_host) cudaFreeHost(D->resid_host);
     for (auto& e : D->evpool) if (e) cudaEventDestroy(e);
     for (auto& kv : D->sched) { cudaFree(kv.second.ptr); cudaFree(kv.second.items); }
+    stream::free_dev(&D->sl);
     delete D;
     h->dev = nullptr;
 }
@@ -3020,8 +3297,11 @@ int64_t device_alg_flops(const Handle* h) { return h->dev ? h->dev->alg_flops_pe
 int64_t device_active_rows(const Handle* h) { return h->dev ? h->dev->n_p2 : -1; }
 void device_phase_info(const Handle* h, int64_t* out9) {
     const DeviceHMat* D = h->dev;
-    if (!D) { for (int i = 0; i < 10; ++i) out9[i] = 0; return; }
+    if (!D) { for (int i = 0; i < 13; ++i) out9[i] = 0; return; }
     out9[9] = D->res_ok ? 1 : 0;
+    out9[10] = D->sl.ok ? D->sl.payload_bytes : 0;
+    out9[11] = D->sl.ok ? D->sl.meta_bytes : 0;
+    out9[12] = D->sl.ok ? D->sl.nchunks : 0;
     out9[0] = D->NT; out9[1] = D->p1_bytes; out9[2] = D->p2_bytes; out9[3] = D->p1_src; out9[4] = D->p2_src;
     out9[5] = D->p1_flops; out9[6] = D->p2_flops; out9[7] = D->n_g1; out9[8] = D->n_g2;
 }
