@@ -171,6 +171,14 @@ int vf_last_solve_stats(vf_handle h, int* iters1, double* resid1, int* iters2, d
  * Qdir: N x k column-major HOST double output.  Needs a mesh-built handle. */
 int vf_insolation(vf_handle h, const double* suns, int k, double S, double* Qdir);
 
+/* Finite solar disk as a sum over point sources: for each of the k
+ * suns, Q_ic = sum_p w_p S max(0, n_i.d_{c,p}) V_sun(x_i, d_{c,p}) -- the
+ * point-sun insolation above per source, weighted.  dirs: (k*P) x 3 unit
+ * vectors, sun c's sources at rows c*P .. c*P+P-1 (HOST); w: P weights
+ * (HOST); Qdir: N x k column-major HOST double output.  Sources are summed in
+ * the order p = 0 .. P-1.  Needs a mesh-built handle. */
+int vf_insolation_sum(vf_handle h, const double* dirs, const double* w, int k, int P, double S, double* Qdir);
+
 /* Attach the mesh a loaded handle was built from (HOST arrays, copied) so
  * that vf_insolation works on it: facet f of the mesh is facet f of the
  * handle (nf must equal N); orient_up as in vf_build_opts. */

@@ -156,6 +156,21 @@ class Scene:
         return Q
 
 
+def insolation_disk(scene, dirs, w, S: float = 1365.0):
+    """Finite solar disk as a sum over point sources: each source
+    contributes eq. insolation-for-point-sun (P:76-80) with weight w_p;
+    Q[:, c] = sum_p w_p Q_point(dirs[c P + p]) summed in p order."""
+    w = np.asarray(w, dtype=np.float64).reshape(-1)
+    P = w.size
+    Qp = scene.insolation(dirs, S)                 # N x (k P)
+    k = Qp.shape[1] // P
+    Q = np.zeros((scene.N, k), order="F")
+    for c in range(k):
+        for p in range(P):
+            Q[:, c] += w[p] * Qp[:, c * P + p]
+    return Q
+
+
 def F_dense_facets(x, n, A, cull_only=True):
     """Dense F from facet data alone (no occluding mesh): used with
     sphere-exact facet data (pin P1/P4) where V_ij is the culling test."""

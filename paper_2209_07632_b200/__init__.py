@@ -23,7 +23,7 @@ from . import build as _build
 
 __all__ = [
     "VFError", "lib", "ViewFactorMatrix", "vf_build", "vf_build_facets", "vf_load", "vf_save", "vf_free",
-    "vf_upload", "vf_set_stream", "vf_matvec", "vf_solve_radiosity", "vf_solve_thermal", "vf_insolation",
+    "vf_upload", "vf_set_stream", "vf_matvec", "vf_solve_radiosity", "vf_solve_thermal", "vf_insolation", "vf_insolation_sum",
     "vf_info", "vf_last_solve_stats", "vf_enable_kernel_timing", "vf_kernel_timing", "VF_F64", "VF_F32",
     "VF_VIS_RAYCAST", "VF_VIS_CULL_ONLY", "HEADER", "vf_row_partition", "vf_shard_rows", "vf_row_range",
     "vf_get_nccl_id", "vf_comm_init", "vf_set_mesh", "VF_EVAL_AUTO", "VF_EVAL_HOST", "VF_EVAL_DEVICE",
@@ -101,6 +101,7 @@ def lib():
             "vf_last_solve_stats": ([H, ctypes.POINTER(i), ctypes.POINTER(d), ctypes.POINTER(i),
                                      ctypes.POINTER(d)], i),
             "vf_insolation": ([H, P, i, d, P], i),
+            "vf_insolation_sum": ([H, P, P, i, i, d, P], i),
             "vf_info": ([H, ctypes.POINTER(vf_info_t)], i),
             "vf_enable_kernel_timing": ([H, i], i),
             "vf_kernel_timing": ([H, ctypes.POINTER(d), ctypes.POINTER(i), ctypes.POINTER(d),
@@ -302,6 +303,21 @@ def vf_insolation(h, suns, S: float = 1365.0) -> np.ndarray:
     return Q
 
 
+def vf_insolation_sum(h, dirs, w, S: float = 1365.0) -> np.ndarray:
+    """Finite solar disk: Q[:, c] = sum_p w[p] Q_point(dirs[c*P + p]).
+    dirs (k*P, 3), w (P,) -> N x k column-major float64."""
+    dirs = np.ascontiguousarray(np.atleast_2d(dirs), dtype=np.float64)
+    w = np.ascontiguousarray(w, dtype=np.float64).reshape(-1)
+    P = w.size
+    if dirs.shape[0] % P:
+        raise ValueError("dirs rows must be a multiple of len(w)")
+    k = dirs.shape[0] // P
+    N = _dims(h)[0]
+    Q = np.empty((N, k), order="F")
+    _check(lib().vf_insolation_sum(h, dirs.ctypes.data, w.ctypes.data, k, P, float(S), Q.ctypes.data))
+    return Q
+
+
 def vf_enable_kernel_timing(h, on: bool = True):
     _check(lib().vf_enable_kernel_timing(h, int(bool(on))))
 
@@ -387,6 +403,9 @@ class ViewFactorMatrix:
 
     def insolation(self, suns, S=1365.0):
         return vf_insolation(self.h, suns, S)
+
+    def insolation_sum(self, dirs, w, S=1365.0):
+        return vf_insolation_sum(self.h, dirs, w, S)
 
     def set_stream(self, stream):
         vf_set_stream(self.h, stream)

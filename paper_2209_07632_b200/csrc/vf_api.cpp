@@ -231,6 +231,24 @@ int vf_insolation(vf_handle hh, const double* suns, int k, double S, double* Q) 
     })
 }
 
+int vf_insolation_sum(vf_handle hh, const double* dirs, const double* w, int k, int P, double S, double* Q) {
+    GUARD({
+        if (!hh || !dirs || !w || !Q || k <= 0 || P <= 0) return set_error(VF_EINVAL, "vf_insolation_sum: bad arguments");
+        Handle* h = reinterpret_cast<Handle*>(hh);
+        const int64_t N = h->N;
+        std::vector<double> Qp((size_t)N * P);
+        std::fill(Q, Q + (size_t)N * k, 0.0);
+        for (int c = 0; c < k; ++c) {
+            const int rc = insolation(h, dirs + (size_t)3 * c * P, P, S, Qp.data());   // N x P
+            if (rc) return rc;
+            double* q = Q + (size_t)c * N;
+            for (int p = 0; p < P; ++p)
+                for (int64_t i = 0; i < N; ++i) q[i] += w[p] * Qp[(size_t)p * N + i];
+        }
+        return VF_OK;
+    })
+}
+
 int vf_info(vf_handle hh, vf_info_t* out) {
     if (!hh || !out) return set_error(VF_EINVAL, "vf_info: null argument");
     Handle* h = reinterpret_cast<Handle*>(hh);

@@ -222,10 +222,16 @@ struct Builder {
         // steps 3 and 4 are independent: the rank estimate of this block and
         // the recursion on its children pairs (slicing the CSR, never
         // re-ray-tracing) run as concurrent OpenMP tasks.
+        // Alg. 3's byte test is against nbytes(F_IJ) as CSR (eq. nbytes-comparison);
+        // the doubling is cut at min(CSR, dense) bytes instead: step 5 takes the
+        // SVD only below both, and the smallest passing q is reached either way,
+        // so the chosen leaves are identical while dense, not-low-rank blocks
+        // stop doubling at k ~ min(m', n')/2 instead of running to a full SVD.
         SvdResult svd;
+        const int64_t b_svd_cap = std::min(b_csr, b_den);
 #pragma omp task shared(svd, dense, crp, ccol, cval) if (m * n >= 16 * min_block)
         svd = estimate_rank(mu, nv, dense.empty() ? nullptr : dense.data(), crp.data(), ccol.data(), cval.data(), tol,
-                            w, k0, b_csr, m, n, bseed);
+                            w, k0, b_svd_cap, m, n, bseed);
         std::vector<TreeBlock> kids(I.kids.size() * J.kids.size());
         for (size_t a = 0; a < I.kids.size(); ++a)
             for (size_t b = 0; b < J.kids.size(); ++b) {

@@ -2078,38 +2078,6 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     if (segs.empty()) segs.push_back(Seg{0, 0, 0, 0});
     D->n_p1 = (int64_t)p1_rows.size();
     D->n_p2 = (int64_t)p2_rows.size();
-    if (getenv("VF_LAYOUT_STATS")) {          // structure of the phase-2 rows (layout design)
-        int64_t hseg[8] = {0}, hlen[3][8] = {{0}}, hrow[10] = {0}, tot[3] = {0, 0, 0}, nsg[3] = {0, 0, 0};
-        auto bin = [](int64_t v, int nb) { int b = 0; while (v > 1 && b < nb - 1) { v >>= 2; ++b; } return b; };
-        for (int64_t r = 0; r < (int64_t)p2_rows.size(); ++r) {
-            const int64_t ns = p2_segptr[r + 1] - p2_segptr[r];
-            hseg[bin(ns, 8)]++;
-            int64_t rb = 0;
-            for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1]; ++q) {
-                const Seg& sg = segs[q];
-                const int k = sg.kind ? 2 : (sg.src >= N ? 1 : 0);
-                hlen[k][bin(sg.len, 8)]++;
-                tot[k] += sg.len;
-                nsg[k]++;
-                rb += sg.len * (int64_t)sizeof(T) + (sg.kind ? 4 * sg.len : 0);
-            }
-            hrow[bin(rb / 256, 10)]++;
-        }
-        fprintf(stderr, "[vf layout] rows %lld; terms dense %lld (%lld segs) U %lld (%lld segs) csr %lld (%lld segs)\n",
-                (long long)p2_rows.size(), (long long)tot[0], (long long)nsg[0], (long long)tot[1], (long long)nsg[1],
-                (long long)tot[2], (long long)nsg[2]);
-        fprintf(stderr, "[vf layout] segs/row hist (bins 1,4,16,..):");
-        for (int b = 0; b < 8; ++b) fprintf(stderr, " %lld", (long long)hseg[b]);
-        for (int k = 0; k < 3; ++k) {
-            fprintf(stderr, "\n[vf layout] len hist kind %d:", k);
-            for (int b = 0; b < 8; ++b) fprintf(stderr, " %lld", (long long)hlen[k][b]);
-        }
-        fprintf(stderr, "\n[vf layout] row bytes hist (256 B x 1,4,16,..):");
-        for (int b = 0; b < 10; ++b) fprintf(stderr, " %lld", (long long)hrow[b]);
-        int64_t g1n = 0, g1t = 0;
-        for (int64_t r = 0; r < (int64_t)p1_rows.size(); ++r) { g1n++; g1t += segs[p1_segptr[r]].len; }
-        fprintf(stderr, "\n[vf layout] phase-1 T rows %lld, V terms %lld\n", (long long)g1n, (long long)g1t);
-    }
     D->alg_bytes = alg_bytes;
     D->alg_flops_per_col = alg_flops;
     D->p2_bytes = alg_bytes - D->p1_bytes;
@@ -2201,6 +2169,71 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     }
     D->n_g1 = (int64_t)g1v.size();
     D->n_g2 = (int64_t)g2v.size();
+    if (getenv("VF_LAYOUT_STATS")) {          // structure of the phase-2 rows (layout design)
+        int64_t hseg[8] = {0}, hlen[3][8] = {{0}}, hrow[10] = {0}, tot[3] = {0, 0, 0}, nsg[3] = {0, 0, 0};
+        auto bin = [](int64_t v, int nb) { int b = 0; while (v > 1 && b < nb - 1) { v >>= 2; ++b; } return b; };
+        for (int64_t r = 0; r < (int64_t)p2_rows.size(); ++r) {
+            const int64_t ns = p2_segptr[r + 1] - p2_segptr[r];
+            hseg[bin(ns, 8)]++;
+            int64_t rb = 0;
+            for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1]; ++q) {
+                const Seg& sg = segs[q];
+                const int k = sg.kind ? 2 : (sg.src >= N ? 1 : 0);
+                hlen[k][bin(sg.len, 8)]++;
+                tot[k] += sg.len;
+                nsg[k]++;
+                rb += sg.len * (int64_t)sizeof(T) + (sg.kind ? 4 * sg.len : 0);
+            }
+            hrow[bin(rb / 256, 10)]++;
+        }
+        fprintf(stderr, "[vf layout] rows %lld; terms dense %lld (%lld segs) U %lld (%lld segs) csr %lld (%lld segs)\n",
+                (long long)p2_rows.size(), (long long)tot[0], (long long)nsg[0], (long long)tot[1], (long long)nsg[1],
+                (long long)tot[2], (long long)nsg[2]);
+        fprintf(stderr, "[vf layout] segs/row hist (bins 1,4,16,..):");
+        for (int b = 0; b < 8; ++b) fprintf(stderr, " %lld", (long long)hseg[b]);
+        for (int k = 0; k < 3; ++k) {
+            fprintf(stderr, "\n[vf layout] len hist kind %d:", k);
+            for (int b = 0; b < 8; ++b) fprintf(stderr, " %lld", (long long)hlen[k][b]);
+        }
+        fprintf(stderr, "\n[vf layout] row bytes hist (256 B x 1,4,16,..):");
+        for (int b = 0; b < 10; ++b) fprintf(stderr, " %lld", (long long)hrow[b]);
+        int64_t g1n = 0, g1t = 0;
+        for (int64_t r = 0; r < (int64_t)p1_rows.size(); ++r) { g1n++; g1t += segs[p1_segptr[r]].len; }
+        fprintf(stderr, "\n[vf layout] phase-1 T rows %lld, V terms %lld\n", (long long)g1n, (long long)g1t);
+        // reuse available to a batched row-tile kernel: terms / distinct staged source rows
+        for (int R : {16, 32, 64, 128}) {
+            int64_t t_run = 0, st_run = 0, t_csr = 0, st_csr = 0, cells = 0;
+            std::vector<int32_t> cols;
+            std::vector<std::pair<int64_t, int32_t>> runs;
+            for (int64_t r0 = 0; r0 < (int64_t)p2_rows.size(); r0 += R) {
+                const int64_t r1 = std::min<int64_t>(r0 + R, (int64_t)p2_rows.size());
+                cols.clear(); runs.clear();
+                for (int64_t r = r0; r < r1; ++r)
+                    for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1]; ++q) {
+                        const Seg& sg = segs[q];
+                        if (sg.kind) { t_csr += sg.len; for (int32_t e = 0; e < sg.len; ++e) cols.push_back(idx[sg.src + e]); }
+                        else { t_run += sg.len; runs.push_back({sg.src, sg.len}); }
+                    }
+                std::sort(cols.begin(), cols.end());
+                const int64_t u = std::unique(cols.begin(), cols.end()) - cols.begin();
+                st_csr += u; cells += u * (r1 - r0);
+                std::sort(runs.begin(), runs.end());
+                runs.erase(std::unique(runs.begin(), runs.end()), runs.end());
+                for (auto& x : runs) st_run += x.second;
+            }
+            fprintf(stderr, "[vf layout] tile R=%d: runs reuse %.2f (terms %lld), csr reuse %.2f fill %.3f\n", R,
+                    (double)t_run / std::max<int64_t>(st_run, 1), (long long)t_run,
+                    (double)t_csr / std::max<int64_t>(st_csr, 1), (double)t_csr / std::max<int64_t>(cells, 1));
+        }
+        {   // phase 1: V terms vs distinct X rows per SVD block (reuse = q)
+            int64_t vt = 0, vrows = 0;
+            for (size_t g = 0; g < g1v.size(); ++g) { vt += (int64_t)g1v[g].nrows * gsegv[g1v[g].seg_off].len; }
+            for (int64_t r = 0; r < (int64_t)p1_rows.size(); ++r) if (r == 0 || p1_rows[r] != p1_rows[r - 1] + 1) {}
+            (void)vrows;
+            fprintf(stderr, "[vf layout] phase-1 groups %lld, V terms %lld, avg group rows %.2f\n", (long long)g1v.size(),
+                    (long long)vt, (double)p1_rows.size() / std::max<size_t>(g1v.size(), 1));
+        }
+    }
     // static-schedule costs: number of terms a work item sums (+ fixed overhead)
     auto row_cost = [&](const std::vector<int64_t>& ptr, int64_t r) {
         int64_t c = 8;

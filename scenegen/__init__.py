@@ -26,7 +26,7 @@ __all__ = [
     "fbm_heightfield", "grid_mesh", "sun_dirs", "random_rhs",
     "flat_plane_mesh", "closed_sphere_mesh", "sphere_exact_facets",
     "facing_plates_mesh", "rough_small_mesh", "blocked_plates_mesh",
-    "cap_mesh",
+    "cap_mesh", "sun_disk_points", "SUN_ANGULAR_RADIUS",
 ]
 
 SEED_MESH = 1   # mesh jitter seed
@@ -217,6 +217,33 @@ def sun_dirs(elev_deg: float, n: int, phase0: float = 0.0) -> np.ndarray:
     return np.ascontiguousarray(np.stack([math.cos(e) * np.cos(phi),
                                           math.cos(e) * np.sin(phi),
                                           np.full(n, math.sin(e))], 1))
+
+
+SUN_ANGULAR_RADIUS = math.radians(0.2666)   # solar disk seen from 1 AU (~16 arcmin)
+
+
+def sun_disk_points(suns, radius: float = SUN_ANGULAR_RADIUS, P: int = 16):
+    """Point sources sampling the solar disk around each sun direction
+    ("a disk of finite extent ... a sum over point sources"):
+    a sunflower pattern in the disk's tangent plane, offset angle
+    r_p = radius sqrt((p + 1/2)/P), position angle p * golden angle, equal
+    weights 1/P (uniform disk).  Input shaping only: returns (k*P, 3) unit
+    directions (sun c's points at rows c*P .. c*P+P-1) and the (P,) weights."""
+    suns = np.atleast_2d(np.asarray(suns, dtype=np.float64))
+    ga = math.pi * (3.0 - math.sqrt(5.0))
+    p = np.arange(P, dtype=np.float64)
+    rp = radius * np.sqrt((p + 0.5) / P)
+    th = p * ga
+    out = np.empty((suns.shape[0] * P, 3))
+    for c, s in enumerate(suns):
+        s = s / np.linalg.norm(s)
+        a = np.array([0.0, 0.0, 1.0]) if abs(s[2]) < 0.9 else np.array([1.0, 0.0, 0.0])
+        u = np.cross(s, a); u /= np.linalg.norm(u)
+        v = np.cross(s, u)
+        d = (np.cos(rp)[:, None] * s[None, :] + np.sin(rp)[:, None] *
+             (np.cos(th)[:, None] * u[None, :] + np.sin(th)[:, None] * v[None, :]))
+        out[c * P:(c + 1) * P] = d / np.linalg.norm(d, axis=1)[:, None]
+    return np.ascontiguousarray(out), np.full(P, 1.0 / P)
 
 
 def random_rhs(N: int, k: int, seed: int = SEED_X) -> np.ndarray:

@@ -189,3 +189,20 @@ def test_device_evaluator_needs_a_device():
     with pytest.raises(vf.VFError) as e:
         vf.vf_build(V, F, 1e-5, device=-1, evaluator=vf.VF_EVAL_DEVICE)
     assert e.value.code == vf.VF_EINVAL
+
+
+def test_insolation_sum_finite_disk_equals_oracle():
+    """vf_insolation_sum (finite solar disk as a sum over point sources)
+    equals the oracle's insolation_disk on the same sources (cap crater, where
+    the disk straddles the rim shadow for some facets)."""
+    V, F = sg.cfg1_mesh()
+    M = vf.ViewFactorMatrix.build(V, F, 1e-5, device=-1)
+    S = oracle.Scene(V, F)
+    suns = sg.sun_dirs(10.0, 2)
+    dirs, w = sg.sun_disk_points(suns, radius=0.02, P=12)
+    Qp = M.insolation_sum(dirs, w)
+    Qo = oracle.insolation_disk(S, dirs, w)
+    np.testing.assert_allclose(Qp, Qo, rtol=0, atol=1e-12)
+    frac = Qp / np.maximum(M.insolation(suns), 1e-300)
+    pen = (Qp > 0) & (Qp < M.insolation(suns) * 0.95)
+    assert pen.sum() > 0                         # penumbra facets exist at this disk size

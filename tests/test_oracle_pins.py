@@ -478,3 +478,43 @@ def test_cap_T_global_outside_is_flat_plane_equilibrium():
     out = oracle.thermal(lambda X: oracle.apply_dense(F, X), Q, np.full(S.N, 0.12), np.full(S.N, 0.95), 1e-12, 20)
     Tout = oracle.cap_T_global(1365.0, e, 0.1, 0.12, 0.95, "outside")
     assert np.allclose(out["T"][:, 0], Tout, rtol=1e-13)
+
+
+def test_insolation_disk_point_limit_and_flat_plane():
+    """Finite solar disk: P = 1 at radius 0 is the point sun; on an
+    unoccluded flat plane the sum over the sunflower sources equals
+    S sum_p w_p sin(e_p) with sin(e_p) = d_p.z, whose mean over a disk uniform
+    in the tangent plane (r^2 uniform) is sin(e) 2 (cos rho + rho sin rho - 1)/rho^2
+    to the quadrature error; the azimuthal terms cancel."""
+    S = oracle.Scene(*sg.flat_plane_mesh(5))
+    suns = sg.sun_dirs(30.0, 3)
+    d1, w1 = sg.sun_disk_points(suns, radius=0.0, P=1)
+    np.testing.assert_array_equal(oracle.insolation_disk(S, d1, w1, 1000.0), S.insolation(suns, 1000.0))
+    rho = math.radians(5.0)
+    mean_cos = 2.0 * (math.cos(rho) + rho * math.sin(rho) - 1.0) / rho ** 2
+    exact = 1000.0 * math.sin(math.radians(30.0)) * mean_cos
+    errs = []
+    for P in (100, 400, 1600):                       # quadrature error ~ 1/P
+        d, w = sg.sun_disk_points(suns, radius=rho, P=P)
+        errs.append(np.abs(oracle.insolation_disk(S, d, w, 1000.0) / exact - 1.0).max())
+    assert errs[0] > errs[1] > errs[2] and errs[2] < 1e-4
+    assert abs(mean_cos - 1.0) > 1e-3                # the disk effect is resolved, not rounding
+
+
+def test_insolation_disk_penumbra_between_zero_and_point_flux():
+    """Facets near the cap's shadow edge see part of the disk: 0 <= Q_disk <= S n.s_max,
+    and far from the edge the disk and point fluxes agree closely."""
+    S = oracle.Scene(*sg.cfg1_mesh())
+    suns = sg.sun_dirs(10.0, 1)
+    d, w = sg.sun_disk_points(suns, radius=0.03, P=24)
+    Qd = oracle.insolation_disk(S, d, w)[:, 0]
+    Qp = S.insolation(suns)[:, 0]
+    mu_max = np.max(S.n @ d.T, axis=1).clip(0) * 1365.0
+    assert np.all(Qd >= 0) and np.all(Qd <= mu_max + 1e-9)
+    part = (Qd > 0) & (Qd < 0.9 * (S.n @ suns[0]).clip(0) * 1365.0)
+    assert part.sum() > 0
+    # facets that see every source: Qd = S sum_p w_p n.d_p, within S rho of the point flux
+    unocc = np.abs(Qd - 1365.0 * (np.clip(S.n @ d.T, 0, None) @ w)) < 1e-9
+    full = unocc & (Qp > 0) & (Qd > 0)
+    assert full.sum() > 0.15 * S.N
+    assert np.all(np.abs(Qd[full] - Qp[full]) <= 1365.0 * 0.03)
