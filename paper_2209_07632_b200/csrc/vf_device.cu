@@ -1767,14 +1767,13 @@ void build_stream(int64_t N, const std::vector<T>& vals, const std::vector<int32
         for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1]; ++q) {
             const Seg& sg = segs[q];
             if (sg.kind == 0) {
-                if (sg.src >= N) out.push_back({1, (int32_t)(sg.src - N), sg.val_off, sg.len, 0});
-                else out.push_back({0, (int32_t)sg.src, sg.val_off, sg.len, 0});
+                out.push_back({0, (int32_t)sg.src, sg.val_off, sg.len, 0});     // X rows or (src >= N) T rows
             } else {
                 for (int64_t e = 0; e < sg.len;) {         // runs of columns within a 16-bit span
                     const int32_t base = idx[sg.src + e];
                     int64_t f = e + 1;
                     while (f < sg.len && idx[sg.src + f] - base < span) ++f;
-                    out.push_back({2, base, sg.val_off + e, f - e, sg.src + e});
+                    out.push_back({1, base, sg.val_off + e, f - e, sg.src + e});
                     e = f;
                 }
             }
@@ -1801,12 +1800,12 @@ void build_stream(int64_t N, const std::vector<T>& vals, const std::vector<int32
                 for (int k = 0; k < c.np; ++k) {
                     const PPiece& P = pcs[cp[k][0]];
                     const int64_t e0 = cp[k][1], n = cp[k][2];
-                    pd[k].src = P.kind == 2 ? P.src : (int32_t)(P.src + e0);
+                    pd[k].src = P.kind == 1 ? P.src : (int32_t)(P.src + e0);
                     pd[k].len = (uint16_t)n;
                     pd[k].kind = (uint8_t)P.kind;
                     pd[k].pad = 0;
                     for (int64_t e = 0; e < n; ++e) vv[t++] = vals[P.voff + e0 + e];
-                    if (P.kind == 2)
+                    if (P.kind == 1)
                         for (int64_t e = 0; e < n; ++e) ii[ci++] = (uint16_t)(idx[P.coff + e0 + e] - P.src);
                 }
                 if (coff_out) coff_out[nch] = base_off + off;
@@ -1819,14 +1818,14 @@ void build_stream(int64_t N, const std::vector<T>& vals, const std::vector<int32
         };
         for (size_t k = 0; k < pcs.size(); ++k) {
             const PPiece& P = pcs[k];
-            const int per = w + (P.kind == 2 ? 2 : 0);
+            const int per = w + (P.kind == 1 ? 2 : 0);
             for (int64_t e = 0; e < P.len;) {
-                if (c.np == kMaxPieces) flush(false);
+                if (c.np == kMaxPieces || c.nt == kMaxTerms) flush(false);
                 const int64_t avail = kSlot - 16 - p16(8 * (c.np + 1)) - w * c.nt - 2 * c.nc - 32;
-                int64_t a = std::min<int64_t>({P.len - e, avail / per, 65535});
+                int64_t a = std::min<int64_t>({P.len - e, avail / per, 65535, kMaxTerms - c.nt});
                 if (a <= 0) { flush(false); continue; }
                 cp.push_back({(int64_t)k, e, a, 0, 0});
-                c.np++; c.nt += a; if (P.kind == 2) c.nc += a;
+                c.np++; c.nt += a; if (P.kind == 1) c.nc += a;
                 e += a;
             }
         }
@@ -1886,7 +1885,7 @@ void build_stream(int64_t N, const std::vector<T>& vals, const std::vector<int32
             if (grow1v[P.g * kGroup + r] != t0 + r) { L = HostLayout{}; return; }   // T rows must be consecutive
         int pidx = 0;
         for (int64_t q = o1[i]; q > 0 && plan1[q - 1].g == P.g; --q) ++pidx;
-        L.p1[i] = P1Item{t0, (int16_t)G, (int16_t)g_np[P.g], pidx, (int32_t)P.g, sbase[P.g], 0};
+        L.p1[i] = P1Item{(int32_t)(N + t0), (int16_t)G, (int16_t)g_np[P.g], pidx, (int32_t)P.g, sbase[P.g], 0};
         const int njm = nj_max(G, sg.kind != 0);
         int64_t off = boff[i];
         int c = L.ic0[i];
@@ -3108,7 +3107,7 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
             int grid = 0;
             {
                 Timer tm(h, st, 2);
-                if ((rc = stream::matvec_k1(D->sl, D->dtype, D->xt[0], D->Yp, st, &grid))) return rc;
+                if ((rc = stream::matvec_k1(D->sl, D->dtype, D->xt[0], D->Yp, st, &grid))) return rc;   // XT = [Xp ; T]
             }
             h->launches_total++;
             D->last_grid = grid;

@@ -26,6 +26,10 @@
 #include "vf_internal.h"
 #include "vf_stream.h"
 
+#ifndef VF_SK1_U
+#define VF_SK1_U 8       // phase-2 terms in flight per lane
+#endif
+
 namespace vf {
 namespace stream {
 
@@ -86,8 +90,7 @@ struct SArgs {
     const int32_t* ic0;
     const P1Item* p1;
     int32_t n1, n2;
-    const T* X;          // tree-order x (N)
-    T* Tb;               // T rows (sum of ranks)
+    T* XT;               // [x (N rows, read-only) | T rows (N + t, written in phase 1)]
     T* Y;                // tree-order y
     double* pscr;        // [scratch rows][16] part sums of multi-part phase-1 groups
     int32_t* pcnt;       // [group] parts finished (reset by the finisher)
@@ -101,12 +104,14 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_k1_kernel(SArgs<T> a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr unsigned FULL = 0xffffffffu;
     unsigned char* ring = sm + (size_t)warp * NS * kSlot;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + (size_t)NW * NS * kSlot) + warp * NS;
+    int32_t* xi = reinterpret_cast<int32_t*>(sm + (size_t)NW * NS * kSlot) + warp * kMaxTerms;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + (size_t)NW * NS * kSlot + (size_t)NW * kMaxTerms * 4) + warp * NS;
     if (threadIdx.x == 0) cta_arrived = 0;
     if (lane == 0)
         for (int s = 0; s < NS; ++s) mbar_init(bar + s, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     __syncthreads();
+    const T* __restrict__ XT = a.XT;
 
     // ---- producer (lane 0): item cursor over the two queues
     const uint64_t pol = evict_first_policy();
@@ -171,7 +176,7 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_k1_kernel(SArgs<T> a) {
             }
             const T* V = reinterpret_cast<const T*>(p);
             for (int jj = lane; jj < nj; jj += 32) {
-                const T x = a.X[rows ? rows[jj] : h.src + jj];
+                const T x = XT[rows ? rows[jj] : h.src + jj];
 #pragma unroll
                 for (int t = 0; t < 16; ++t)
                     if (t < G) acc1[t] = fma(V[t * nj + jj], x, acc1[t]);
@@ -206,7 +211,7 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_k1_kernel(SArgs<T> a) {
                             for (int q = 0; q < it.np; ++q) mine += __ldcg(a.pscr + ((int64_t)it.sbase + q) * 16 + lane);
                     }
                 }
-                if (finish && lane < G) a.Tb[it.t0 + lane] = (T)mine;      // S_t is folded into V
+                if (finish && lane < G) a.XT[it.t0 + lane] = (T)mine;      // S_t is folded into V
             }
         } else {
             // ---- phase 2
@@ -229,7 +234,7 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_k1_kernel(SArgs<T> a) {
                 reinterpret_cast<const uint16_t*>(reinterpret_cast<const unsigned char*>(vals) + pad16((int)sizeof(T) * nt));
             Piece my{0, 0, 0, 0};
             if (lane < np) my = pcs[lane];
-            const int len = my.len, clen = my.kind == 2 ? len : 0;
+            const int len = my.len, clen = my.kind ? len : 0;
             int incl = len, cincl = clen;
 #pragma unroll
             for (int off = 1; off < 32; off <<= 1) {
@@ -237,30 +242,27 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_k1_kernel(SArgs<T> a) {
                 if (lane >= off) { incl += v; cincl += cv; }
             }
             const int excl = incl - len, cexcl = cincl - clen;
-            constexpr int U = 4;
-            for (int base = 0; base < nt; base += 32 * U) {
+            // pass A: the XT row of every term, piece by piece (lanes over the piece's terms)
+            for (int q = 0; q < np; ++q) {
+                const int q_src = __shfl_sync(FULL, my.src, q), q_len = __shfl_sync(FULL, len, q);
+                const int q_kind = __shfl_sync(FULL, (int)my.kind, q);
+                const int q_ex = __shfl_sync(FULL, excl, q), q_cex = __shfl_sync(FULL, cexcl, q);
+                for (int e = lane; e < q_len; e += 32)
+                    xi[q_ex + e] = q_src + (q_kind ? (int)ix[q_cex + e] : e);
+            }
+            __syncwarp();
+            // pass B: every term's gather in flight, U per lane
+            constexpr int U = VF_SK1_U;
+            for (int t0 = 0; t0 < nt; t0 += 32 * U) {
                 T v[U], x[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int t = base + u * 32 + lane;
-                    int g = 0;                                   // last piece with excl <= t
-#pragma unroll
-                    for (int step = 16; step > 0; step >>= 1) {
-                        const int cand = g + step;
-                        const int e = __shfl_sync(FULL, excl, cand & 31);
-                        if (cand < np && e <= t) g = cand;
-                    }
-                    const int g_src = __shfl_sync(FULL, my.src, g);
-                    const int g_kind = __shfl_sync(FULL, (int)my.kind, g);
-                    const int g_excl = __shfl_sync(FULL, excl, g);
-                    const int g_cexcl = __shfl_sync(FULL, cexcl, g);
+                    const int t = t0 + 32 * u + lane;
                     v[u] = T(0);
                     x[u] = T(0);
                     if (t < nt) {
                         v[u] = vals[t];
-                        const int e = t - g_excl;
-                        if (g_kind == 1) x[u] = __ldcg(a.Tb + g_src + e);
-                        else x[u] = a.X[g_src + (g_kind == 2 ? (int)ix[g_cexcl + e] : e)];
+                        x[u] = XT[xi[t]];
                     }
                 }
 #pragma unroll
@@ -289,7 +291,7 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_k1_kernel(SArgs<T> a) {
 }  // namespace
 
 #ifndef VF_SK1_WARPS
-#define VF_SK1_WARPS 16
+#define VF_SK1_WARPS 14
 #endif
 #ifndef VF_SK1_STAGES
 #define VF_SK1_STAGES 3
@@ -297,7 +299,7 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_k1_kernel(SArgs<T> a) {
 constexpr int kNW = VF_SK1_WARPS;    // warps per CTA (one CTA per SM)
 constexpr int kNS = VF_SK1_STAGES;   // ring slots per warp
 
-size_t smem_bytes() { return (size_t)kNW * kNS * kSlot + (size_t)kNW * kNS * 8; }
+size_t smem_bytes() { return (size_t)kNW * kNS * kSlot + (size_t)kNW * kMaxTerms * 4 + (size_t)kNW * kNS * 8; }
 
 #define SCK(call)                                                                        \
     do {                                                                                 \
@@ -325,9 +327,9 @@ int upload(const HostLayout& L, int w, int64_t NT, DevLayout* D) {
         (rc = up((void**)&D->p1, p1.data(), p1.size() * sizeof(P1Item))) ||
         (rc = up((void**)&D->pscr, nullptr, (size_t)std::max<int64_t>(L.nscratch, 1) * 16 * 8)) ||
         (rc = up((void**)&D->pcnt, pc.data(), pc.size() * 4)) ||
-        (rc = up((void**)&D->ctr, nullptr, 16)) ||
-        (rc = up(&D->Tb, nullptr, (size_t)std::max<int64_t>(NT, 1) * w)))
+        (rc = up((void**)&D->ctr, nullptr, 16)))
         return rc;
+    (void)NT;
     D->n1 = L.n1;
     D->n2 = L.n2;
     D->w = w;
@@ -340,13 +342,13 @@ int upload(const HostLayout& L, int w, int64_t NT, DevLayout* D) {
 }
 
 void free_dev(DevLayout* D) {
-    void* ps[] = {D->bytes, D->coff, D->ic0, D->p1, D->pscr, D->pcnt, D->ctr, D->Tb};
+    void* ps[] = {D->bytes, D->coff, D->ic0, D->p1, D->pscr, D->pcnt, D->ctr};
     for (void* p : ps) if (p) cudaFree(p);
     *D = DevLayout{};
 }
 
 template <typename T>
-static int launch_t(const DevLayout& D, const void* X, void* Y, cudaStream_t st, int* grid_out) {
+static int launch_t(const DevLayout& D, void* XT, void* Y, cudaStream_t st, int* grid_out) {
     auto fn = stream_k1_kernel<T, kNW, kNS>;
     const size_t smem = smem_bytes();
     SCK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -356,8 +358,8 @@ static int launch_t(const DevLayout& D, const void* X, void* Y, cudaStream_t st,
     int dev = 0, nsm = 148;
     SCK(cudaGetDevice(&dev));
     SCK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-    SArgs<T> a{D.bytes, D.coff, D.ic0, D.p1, (int32_t)D.n1, (int32_t)D.n2, static_cast<const T*>(X),
-               static_cast<T*>(D.Tb), static_cast<T*>(Y), D.pscr, D.pcnt, D.ctr};
+    SArgs<T> a{D.bytes, D.coff, D.ic0, D.p1, (int32_t)D.n1, (int32_t)D.n2, static_cast<T*>(XT),
+               static_cast<T*>(Y), D.pscr, D.pcnt, D.ctr};
     SCK(cudaMemsetAsync(D.ctr, 0, 16, st));
     void* args[] = {&a};
     SCK(cudaLaunchCooperativeKernel((const void*)fn, dim3(nsm), dim3(kNW * 32), args, smem, st));
@@ -365,9 +367,9 @@ static int launch_t(const DevLayout& D, const void* X, void* Y, cudaStream_t st,
     return VF_OK;
 }
 
-int matvec_k1(const DevLayout& D, int dtype, const void* X, void* Y, cudaStream_t st, int* grid_out) {
+int matvec_k1(const DevLayout& D, int dtype, void* XT, void* Y, cudaStream_t st, int* grid_out) {
     if (!D.ok) return set_error(VF_EUNSUPPORTED, "no stream layout");
-    return dtype == VF_F64 ? launch_t<double>(D, X, Y, st, grid_out) : launch_t<float>(D, X, Y, st, grid_out);
+    return dtype == VF_F64 ? launch_t<double>(D, XT, Y, st, grid_out) : launch_t<float>(D, XT, Y, st, grid_out);
 }
 
 }  // namespace stream

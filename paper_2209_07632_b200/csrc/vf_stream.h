@@ -22,6 +22,7 @@ namespace stream {
 
 constexpr int kSlot = 4608;      // max chunk bytes (= one ring slot)
 constexpr int kMaxPieces = 32;   // phase-2 pieces per chunk (one descriptor per lane)
+constexpr int kMaxTerms = 576;   // phase-2 terms per chunk (the consumer's per-warp XT-row buffer)
 constexpr int kP1J = 32;         // phase-1 chunks carry a multiple of 32 V rows (one per lane)
 constexpr int kP1Part = 2048;    // V rows per phase-1 item (long blocks split over warps)
 
@@ -35,12 +36,12 @@ struct Hdr {
 };
 // phase-2 piece descriptor, 8 B
 struct Piece {
-    int32_t src;       // kind 0/2: X row (base); kind 1: T row
+    int32_t src;       // first XT row (kind 0) or base XT row of the run (kind 1)
     uint16_t len;      // terms
-    uint8_t kind;      // 0: X rows src..src+len; 1: T rows src..; 2: X rows src + u16 offset
+    uint8_t kind;      // 0: XT rows src .. src+len (dense-leaf X rows or U_b's T rows); 1: src + u16 offset
     uint8_t pad;
 };
-// phase-1 item: T rows t0 .. t0+G of one SVD block, V rows [j0, j0+nj) of it
+// phase-1 item: T rows t0 .. t0+G (XT rows) of one SVD block, a part of its V rows
 struct P1Item {
     int32_t t0;
     int16_t G;
@@ -73,15 +74,15 @@ struct DevLayout {
     double* pscr = nullptr;
     int32_t* pcnt = nullptr;
     int32_t* ctr = nullptr;
-    void* Tb = nullptr;
     int64_t n1 = 0, n2 = 0, nchunks = 0;
     int w = 8;
     int64_t stream_bytes = 0, payload_bytes = 0, meta_bytes = 0, device_bytes = 0;
 };
 int upload(const HostLayout& L, int w, int64_t NT, DevLayout* D);
 void free_dev(DevLayout* D);
-// Y = F-hat X for one column; X, Y tree-order device vectors of length N
-int matvec_k1(const DevLayout& D, int dtype, const void* X, void* Y, cudaStream_t st, int* grid);
+// Y = F-hat X for one column.  XT: tree-order device vector [x (N) | T rows]
+// (the XT buffer of vf_device.cu; T rows are written), Y: tree-order (N)
+int matvec_k1(const DevLayout& D, int dtype, void* XT, void* Y, cudaStream_t st, int* grid);
 
 }  // namespace stream
 }  // namespace vf
