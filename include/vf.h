@@ -94,9 +94,14 @@ typedef struct {
                             VF_EVAL_AUTO (default): the device when device >= 0,
                             else the host; VF_EVAL_HOST; VF_EVAL_DEVICE.  Both take
                             bit-identical decisions and values (reading R-VIS)     */
+    int tree;            /* spatial tree of the permutation: VF_TREE_QUAD
+                            (default; centroids' x, y -- height fields) or
+                            VF_TREE_OCT (x, y, z: closed bodies, overhangs; 64
+                            first-level block pairs)                         */
 } vf_build_opts;
 
 enum { VF_EVAL_AUTO = 0, VF_EVAL_HOST = 1, VF_EVAL_DEVICE = 2 };
+enum { VF_TREE_QUAD = 0, VF_TREE_OCT = 1 };
 
 /* Fill *opts with the defaults above. */
 void vf_default_opts(vf_build_opts* opts);

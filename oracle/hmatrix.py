@@ -3,6 +3,7 @@
 TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  PAPER.md = P:<line>.
 
   * quadtree            Alg. 2 with readings A1-A3
+  * octree              its 3D analogue
   * estimate_rank       Alg. 3; numpy.linalg.svd supplies the
                         k-term truncated SVD (a library primitive); A5-A8
   * assemble            Alg. 4 dynamic programming over block
@@ -66,6 +67,37 @@ def quadtree(xy: np.ndarray, max_depth: int = 16, min_leaf: int = 16):
         return node
 
     root = build(np.arange(xy.shape[0]), 0)
+    return root, np.asarray(order, dtype=np.int64)
+
+
+def octree(xyz: np.ndarray, max_depth: int = 16, min_leaf: int = 16):
+    """The 3D analogue of Alg. 2 ("an octree ... each internal node
+    has at most 8 child nodes"; 64 first-level pairs).  Reading A1 in
+    3D: split at x_mid, y_mid, z_mid, a coordinate equal to mid goes to the
+    upper half; children ordered by (x, y, z) half, x slowest -- the quadtree's
+    I1..I4 order with z added.  A2/A3 as for the quadtree."""
+    order = []
+
+    def build(idx: np.ndarray, depth: int) -> Node:
+        start = len(order)
+        if depth >= max_depth or idx.size <= min_leaf:
+            order.extend(np.sort(idx).tolist())
+            return Node(start, len(order), depth)
+        x, y, z = xyz[idx, 0], xyz[idx, 1], xyz[idx, 2]
+        xm = 0.5 * (x.min() + x.max())
+        ym = 0.5 * (y.min() + y.max())
+        zm = 0.5 * (z.min() + z.max())
+        node = Node(start, start, depth)
+        for hx in (False, True):
+            for hy in (False, True):
+                for hz in (False, True):
+                    sel = idx[((x >= xm) == hx) & ((y >= ym) == hy) & ((z >= zm) == hz)]
+                    if sel.size:
+                        node.children.append(build(sel, depth + 1))
+        node.stop = len(order)
+        return node
+
+    root = build(np.arange(xyz.shape[0]), 0)
     return root, np.asarray(order, dtype=np.int64)
 
 
@@ -221,12 +253,13 @@ def _round(a, dtype):
 
 
 def compress(x: np.ndarray, F: np.ndarray, eps: float, dtype: str = "f64", max_depth: int = 16,
-             min_leaf: int = 16, min_size: int = 16384, k0: int = 8) -> HMatrix:
-    """Quadtree on centroids (Alg. 2), then Alg. 4 on every first-level block
-    pair (at most 16 pairs).  Values are rounded to the storage dtype
-    (f32 variant: the block values a GPU f32 path stores)."""
+             min_leaf: int = 16, min_size: int = 16384, k0: int = 8, tree: str = "quad") -> HMatrix:
+    """Quadtree (Alg. 2) or octree (tree="oct") on centroids, then
+    Alg. 4 on every first-level block pair (at most 16 / 64 pairs).
+    Values are rounded to the storage dtype (f32 variant: the block values a
+    GPU f32 path stores)."""
     w = 8 if dtype == "f64" else 4
-    root, perm = quadtree(x[:, :2], max_depth, min_leaf)
+    root, perm = (octree(x, max_depth, min_leaf) if tree == "oct" else quadtree(x[:, :2], max_depth, min_leaf))
     Fp = F[np.ix_(perm, perm)]
     level1 = root.children if root.children else [root]
     tops = [assemble(Fp, I, J, eps, w, min_size, k0, 1) for I in level1 for J in level1]

@@ -27,6 +27,7 @@ __all__ = [
     "vf_info", "vf_last_solve_stats", "vf_enable_kernel_timing", "vf_kernel_timing", "VF_F64", "VF_F32",
     "VF_VIS_RAYCAST", "VF_VIS_CULL_ONLY", "HEADER", "vf_row_partition", "vf_shard_rows", "vf_row_range",
     "vf_get_nccl_id", "vf_comm_init", "vf_set_mesh", "VF_EVAL_AUTO", "VF_EVAL_HOST", "VF_EVAL_DEVICE",
+    "VF_TREE_QUAD", "VF_TREE_OCT", "vf_insolation_sum",
 ]
 
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "vf.h")
@@ -36,6 +37,7 @@ VF_OK, VF_EINVAL, VF_ENOMEM, VF_ECUDA, VF_ENOCONV, VF_EIO, VF_ENCCL, VF_EUNSUPPO
 VF_F64, VF_F32 = 1, 2
 VF_VIS_RAYCAST, VF_VIS_CULL_ONLY = 0, 1
 VF_EVAL_AUTO, VF_EVAL_HOST, VF_EVAL_DEVICE = 0, 1, 2
+VF_TREE_QUAD, VF_TREE_OCT = 0, 1
 _STATUS = {0: "VF_OK", -1: "VF_EINVAL", -2: "VF_ENOMEM", -3: "VF_ECUDA", -4: "VF_ENOCONV", -5: "VF_EIO",
            -6: "VF_ENCCL", -7: "VF_EUNSUPPORTED", -8: "VF_ENODEV"}
 
@@ -55,7 +57,7 @@ class vf_build_opts(ctypes.Structure):
     _fields_ = [("dtype", ctypes.c_int), ("max_depth", ctypes.c_int), ("min_leaf", ctypes.c_int),
                 ("min_block", ctypes.c_int64), ("k0", ctypes.c_int), ("visibility", ctypes.c_int),
                 ("orient_up", ctypes.c_int), ("device", ctypes.c_int), ("threads", ctypes.c_int),
-                ("seed", ctypes.c_uint64), ("evaluator", ctypes.c_int)]
+                ("seed", ctypes.c_uint64), ("evaluator", ctypes.c_int), ("tree", ctypes.c_int)]
 
 
 class vf_info_t(ctypes.Structure):

@@ -33,6 +33,9 @@ struct QuadTree {
     std::vector<int32_t> perm;
     // Alg. 2, readings A1 (split at the midpoint, ties to the
     // upper half), A2 (one root), A3 (stop at max_depth or <= min_leaf).
+    // dims = 3: the octree, split also at z_mid; children ordered
+    // by (x, y, z) half with x slowest (reading A1 in 3D).
+    int dims = 2;
     int build(const double* x, std::vector<int32_t> idx, int depth, int max_depth, int min_leaf) {
         int id = (int)nodes.size();
         nodes.push_back(QNode{(int64_t)perm.size(), 0, depth, {}});
@@ -42,18 +45,20 @@ struct QuadTree {
             nodes[id].stop = (int64_t)perm.size();
             return id;
         }
-        double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY;
+        double xmin = INFINITY, xmax = -INFINITY, ymin = INFINITY, ymax = -INFINITY, zmin = INFINITY, zmax = -INFINITY;
         for (int32_t i : idx) {
             xmin = std::min(xmin, x[3 * i]); xmax = std::max(xmax, x[3 * i]);
             ymin = std::min(ymin, x[3 * i + 1]); ymax = std::max(ymax, x[3 * i + 1]);
+            zmin = std::min(zmin, x[3 * i + 2]); zmax = std::max(zmax, x[3 * i + 2]);
         }
-        double xmid = 0.5 * (xmin + xmax), ymid = 0.5 * (ymin + ymax);
-        std::vector<int32_t> part[4];
+        double xmid = 0.5 * (xmin + xmax), ymid = 0.5 * (ymin + ymax), zmid = 0.5 * (zmin + zmax);
+        std::vector<int32_t> part[8];
         for (int32_t i : idx) {
             bool hx = x[3 * i] >= xmid, hy = x[3 * i + 1] >= ymid;
-            part[(hx ? 2 : 0) + (hy ? 1 : 0)].push_back(i);     // I1..I4 of step 4
+            if (dims == 3) part[(hx ? 4 : 0) + (hy ? 2 : 0) + (x[3 * i + 2] >= zmid ? 1 : 0)].push_back(i);
+            else part[(hx ? 2 : 0) + (hy ? 1 : 0)].push_back(i);     // I1..I4 of step 4
         }
-        for (int c = 0; c < 4; ++c)
+        for (int c = 0; c < (dims == 3 ? 8 : 4); ++c)
             if (!part[c].empty()) {
                 int k = build(x, std::move(part[c]), depth + 1, max_depth, min_leaf);
                 nodes[id].kids.push_back(k);
@@ -335,6 +340,7 @@ int build_handle(Handle* h, int64_t N, const double* x, const double* n, const d
     std::vector<int32_t> all(N);
     std::iota(all.begin(), all.end(), 0);
     qt.nodes.reserve(4 * N / std::max(1, o.min_leaf) + 16);
+    qt.dims = o.tree == VF_TREE_OCT ? 3 : 2;
     qt.build(h->x.data(), std::move(all), 0, o.max_depth, o.min_leaf);
     h->perm = qt.perm;
 

@@ -26,7 +26,7 @@ __all__ = [
     "fbm_heightfield", "grid_mesh", "sun_dirs", "random_rhs",
     "flat_plane_mesh", "closed_sphere_mesh", "sphere_exact_facets",
     "facing_plates_mesh", "rough_small_mesh", "blocked_plates_mesh",
-    "cap_mesh", "sun_disk_points", "SUN_ANGULAR_RADIUS",
+    "cap_mesh", "sun_disk_points", "SUN_ANGULAR_RADIUS", "bilobed_body_mesh",
 ]
 
 SEED_MESH = 1   # mesh jitter seed
@@ -253,6 +253,32 @@ def random_rhs(N: int, k: int, seed: int = SEED_X) -> np.ndarray:
 
 
 # ---------------------------------------------------------------- test scenes
+
+def bilobed_body_mesh(n_pts: int = 800, neck: float = 0.45, elong: float = 1.6, seed: int = SEED_MESH):
+    """Closed bilobed body, a synthetic stand-in for the 67P shape model
+    (the Rosetta model is not in the container): Fibonacci
+    points on the unit sphere (seeded tangential jitter), convex hull
+    triangulation (outward, counter-clockwise seen from outside), then the
+    radial map p = r(u) (u_x, u_y, elong u_z) with r = 1 - neck exp(-(u_z/0.35)^2):
+    a concave neck between two lobes, so facets see each other across it and
+    shadow each other (a closed body needs the octree)."""
+    from scipy.spatial import ConvexHull
+    rng = np.random.default_rng(seed)
+    k = np.arange(n_pts) + 0.5
+    z = 1.0 - 2.0 * k / n_pts
+    phi = k * math.pi * (3.0 - math.sqrt(5.0)) + 0.2 * rng.standard_normal(n_pts) / math.sqrt(n_pts)
+    r = np.sqrt(1.0 - z * z)
+    U = np.stack([r * np.cos(phi), r * np.sin(phi), z], 1)
+    U /= np.linalg.norm(U, axis=1)[:, None]
+    hull = ConvexHull(U)
+    F = hull.simplices.astype(np.int32).copy()
+    a, b, c = U[F[:, 0]], U[F[:, 1]], U[F[:, 2]]
+    flip = np.einsum("ij,ij->i", np.cross(b - a, c - a), a + b + c) < 0
+    F[flip] = F[flip][:, [0, 2, 1]]
+    rad = 1.0 - neck * np.exp(-(U[:, 2] / 0.35) ** 2)
+    V = np.stack([rad * U[:, 0], rad * U[:, 1], rad * elong * U[:, 2]], 1)
+    return np.ascontiguousarray(V), np.ascontiguousarray(F)
+
 
 def flat_plane_mesh(n: int = 8, size: float = 1.0):
     return grid_mesh(np.zeros((n + 1, n + 1)), size / n)

@@ -206,3 +206,20 @@ def test_insolation_sum_finite_disk_equals_oracle():
     frac = Qp / np.maximum(M.insolation(suns), 1e-300)
     pen = (Qp > 0) & (Qp < M.insolation(suns) * 0.95)
     assert pen.sum() > 0                         # penumbra facets exist at this disk size
+
+
+def test_octree_permutation_and_blocks_match_oracle(tmp_path):
+    """Octree on a closed bilobed body: the product's permutation
+    equals the oracle's octree (reading A1 in 3D), and its densified F-hat
+    matches the oracle's exact F within 10 tol."""
+    V, F = sg.bilobed_body_mesh(600)
+    S = oracle.Scene(V, F, orient_up=False)
+    M = vf.ViewFactorMatrix.build(V, F, 1e-5, device=-1, orient_up=0, tree=vf.VF_TREE_OCT, min_block=2048)
+    p = str(tmp_path / "o.hvfm")
+    M.save(p)
+    H = read_hvfm(p)
+    _, perm = hm.octree(S.x, 16, 16)
+    assert np.array_equal(H["perm"], perm)
+    Fd = S.F_dense()
+    assert np.count_nonzero(Fd) > 0
+    assert np.linalg.norm(densify(H) - Fd) / np.linalg.norm(Fd) <= 1e-4

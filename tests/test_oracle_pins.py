@@ -518,3 +518,48 @@ def test_insolation_disk_penumbra_between_zero_and_point_flux():
     full = unocc & (Qp > 0) & (Qd > 0)
     assert full.sum() > 0.15 * S.N
     assert np.all(np.abs(Qd[full] - Qp[full]) <= 1365.0 * 0.03)
+
+
+def test_octree_partition_and_midpoint_rule():
+    """Octree: <= 8 children split at the x/y/z midpoints (reading
+    A1 in 3D, ties to the upper half), children in (x, y, z) order, x slowest;
+    nested, contiguous tree-order ranges."""
+    pts = np.array([[0, 0, 0], [0, 0, 4.0], [0, 4.0, 0], [0, 4, 4], [4, 0, 0], [4, 0, 4], [4, 4, 0], [8, 8, 8.0],
+                    [0.1, 0.2, 0.3]])
+    root, perm = hm.octree(pts, 8, 1)
+    sets = [sorted(perm[c.start:c.stop].tolist()) for c in root.children]
+    # mid = 4 on every axis: the 4's go up; (0.1,0.2,0.3) joins the origin's octant
+    assert sets == [[0, 8], [1], [2], [3], [4], [5], [6], [7]]
+    rng = np.random.default_rng(3)
+    xyz = rng.random((700, 3)) ** 2                          # skewed: midpoint != median
+    root, perm = hm.octree(xyz, 6, 8)
+    assert np.array_equal(np.sort(perm), np.arange(700))
+    assert len(root.children) == 8
+
+    def check(nd):
+        if nd.children:
+            assert len(nd.children) <= 8
+            assert nd.children[0].start == nd.start and nd.children[-1].stop == nd.stop
+            par = xyz[perm[nd.start:nd.stop]]
+            mid = 0.5 * (par.min(0) + par.max(0))
+            for c in nd.children:
+                pts_c = xyz[perm[c.start:c.stop]]
+                hi = pts_c >= mid
+                assert np.all(hi == hi[0])                     # one octant per child
+                check(c)
+    check(root)
+
+
+def test_octree_closed_body_reciprocity_and_compression():
+    """Closed bilobed body (67P stand-in): the exact F satisfies reciprocity
+    (P3), is nonzero only across the concave neck region, and the octree
+    compression reproduces it within 10 eps."""
+    V, F = sg.bilobed_body_mesh(800)
+    S = oracle.Scene(V, F, orient_up=False)
+    Fd = S.F_dense()
+    AF = S.A[:, None] * Fd
+    assert np.abs(AF - AF.T).max() <= 1e-14 * AF.max()
+    assert 0 < np.count_nonzero(Fd) < 0.1 * Fd.size
+    H = hm.compress(S.x, Fd, 1e-5, min_size=2048, tree="oct")
+    assert len(H.tops) <= 64
+    assert np.linalg.norm(hm.densify(H) - Fd) / np.linalg.norm(Fd) <= 1e-4
