@@ -189,6 +189,33 @@ int vf_insolation_sum(vf_handle h, const double* dirs, const double* w, int k, i
  * handle (nf must equal N); orient_up as in vf_build_opts. */
 int vf_set_mesh(vf_handle h, const vf_mesh* mesh, int orient_up);
 
+/*
+ * Time-dependent thermal model (Alg. 6; NEXT-1): per step one
+ * F-hat product of the 2 nscen columns [alpha (Q_dir^(n+1) + Q_refl^(n)) |
+ * Q_rad^(n) + (1 - eps) Q_IR^(n)] (clamped >= 0, reading A12), Q_abs^(n+1) =
+ * (1 - alpha)(Q_dir^(n+1) + Q_refl^(n+1)) + eps Q_IR^(n+1), then one
+ * Crank-Nicolson step of every facet's subsurface column (reading
+ * A27 in DESIGN.md: M layers, geometric thicknesses d_1 r^(j-1) to `depth`,
+ * conductivity k_th, volumetric heat capacity rho_c, a capacity-free surface
+ * node balanced at n+1 with eps sigma T^4 linearised about T_0^(n), bottom flux
+ * H) and Q_rad = eps sigma T_0^4.  nscen independent scenarios (sites,
+ * parameter sets) step together; steps are sequential.  The state lives on the
+ * device, owned by the vf_tstate; vectors as for the solves (column-major
+ * N x nscen, caller order, device or host, handle dtype).
+ */
+typedef struct vf_tstate_s* vf_tstate;
+/* Initialise: Q_abs^(0) = (1 - alpha) Qdir0 + H, Q_refl = Q_IR = 0,
+ * Q_rad^(0) = Q_abs^(0); every column starts uniform at T0 (N x nscen).
+ * 1 <= M <= 128, depth > 0, ratio > 0, k_th > 0, rho_c > 0. */
+int vf_ts_create(vf_handle h, int nscen, int M, double depth, double ratio, double k_th, double rho_c, double H,
+                 const void* albedo, const void* emiss, const void* Qdir0, const void* T0, vf_tstate* out);
+/* One step with the direct flux Q_dir^(n+1) (N x nscen) and time step dt (s);
+ * Tsurf (N x nscen, nullable) receives the new surface temperature. */
+int vf_ts_step(vf_tstate s, const void* Qdir, double dt, void* Tsurf);
+/* Current Q_refl, Q_IR, Q_abs and surface T (each N x nscen, nullable). */
+int vf_ts_get(vf_tstate s, void* Qrefl, void* Qir, void* Qabs, void* Tsurf);
+int vf_ts_free(vf_tstate s);
+
 typedef struct {
     int64_t N;             /* facets                                               */
     int dtype;             /* VF_F64 / VF_F32                                      */

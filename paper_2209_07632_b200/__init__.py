@@ -27,7 +27,7 @@ __all__ = [
     "vf_info", "vf_last_solve_stats", "vf_enable_kernel_timing", "vf_kernel_timing", "VF_F64", "VF_F32",
     "VF_VIS_RAYCAST", "VF_VIS_CULL_ONLY", "HEADER", "vf_row_partition", "vf_shard_rows", "vf_row_range",
     "vf_get_nccl_id", "vf_comm_init", "vf_set_mesh", "VF_EVAL_AUTO", "VF_EVAL_HOST", "VF_EVAL_DEVICE",
-    "VF_TREE_QUAD", "VF_TREE_OCT", "vf_insolation_sum",
+    "VF_TREE_QUAD", "VF_TREE_OCT", "vf_insolation_sum", "TimeStepper",
 ]
 
 HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include", "vf.h")
@@ -104,6 +104,10 @@ def lib():
                                      ctypes.POINTER(d)], i),
             "vf_insolation": ([H, P, i, d, P], i),
             "vf_insolation_sum": ([H, P, P, i, i, d, P], i),
+            "vf_ts_create": ([H, i, i, d, d, d, d, d, P, P, P, P, ctypes.POINTER(ctypes.c_void_p)], i),
+            "vf_ts_step": ([ctypes.c_void_p, P, d, P], i),
+            "vf_ts_get": ([ctypes.c_void_p, P, P, P, P], i),
+            "vf_ts_free": ([ctypes.c_void_p], i),
             "vf_info": ([H, ctypes.POINTER(vf_info_t)], i),
             "vf_enable_kernel_timing": ([H, i], i),
             "vf_kernel_timing": ([H, ctypes.POINTER(d), ctypes.POINTER(i), ctypes.POINTER(d),
@@ -287,6 +291,51 @@ def vf_solve_thermal(h, Qdir, albedo, emiss, T, Qvis=None, Qir=None, iters: int 
     if kt != k:
         raise ValueError("Qdir/T column counts differ")
     _check(lib().vf_solve_thermal(h, pq, pa, pe, pt, pv, pi, int(k), int(iters), float(tol)))
+
+
+class TimeStepper:
+    """Alg. 6 on the device: vf_ts_create / vf_ts_step / vf_ts_get
+    (argument marshalling only; include/vf.h documents the operation)."""
+
+    def __init__(self, M, albedo, emiss, Qdir0, T0, layers=30, depth=0.5, ratio=1.2, k_th=0.01, rho_c=1.0e6,
+                 H=0.0):
+        self.h = M.h if hasattr(M, "h") else M
+        N, dt = _dims(self.h)
+        self.N, self.dt = N, dt
+        pa, _ = _vec_ptr(albedo, N, dt, "albedo")
+        pe, _ = _vec_ptr(emiss, N, dt, "emiss")
+        pq, k = _vec_ptr(Qdir0, N, dt, "Qdir0")
+        pt, kt = _vec_ptr(T0, N, dt, "T0")
+        if kt != k:
+            raise ValueError("Qdir0 / T0 column counts differ")
+        self.nscen = k
+        s = ctypes.c_void_p()
+        _check(lib().vf_ts_create(self.h, int(k), int(layers), float(depth), float(ratio), float(k_th), float(rho_c),
+                                  float(H), pa, pe, pq, pt, ctypes.byref(s)))
+        self.s = s
+
+    def step(self, Qdir, dt, Tsurf=None):
+        pq, k = _vec_ptr(Qdir, self.N, self.dt, "Qdir")
+        pt, _ = _vec_ptr(Tsurf, self.N, self.dt, "Tsurf", writable=True)
+        if k != self.nscen:
+            raise ValueError("Qdir column count differs from the state's scenarios")
+        _check(lib().vf_ts_step(self.s, pq, float(dt), pt))
+
+    def get(self, Qrefl=None, Qir=None, Qabs=None, Tsurf=None):
+        ps = [_vec_ptr(a, self.N, self.dt, n, writable=True)[0] for a, n in
+              ((Qrefl, "Qrefl"), (Qir, "Qir"), (Qabs, "Qabs"), (Tsurf, "Tsurf"))]
+        _check(lib().vf_ts_get(self.s, *ps))
+
+    def close(self):
+        if getattr(self, "s", None) and self.s.value:
+            lib().vf_ts_free(self.s)
+            self.s = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def vf_last_solve_stats(h) -> dict:

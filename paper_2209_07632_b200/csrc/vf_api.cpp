@@ -214,6 +214,41 @@ int vf_solve_thermal(vf_handle hh, const void* Qdir, const void* albedo, const v
     })
 }
 
+int vf_ts_create(vf_handle hh, int nscen, int M, double depth, double ratio, double k_th, double rho_c, double H,
+                 const void* albedo, const void* emiss, const void* Qdir0, const void* T0, vf_tstate* out) {
+    GUARD({
+        Handle* h = reinterpret_cast<Handle*>(hh);
+        int rc = need_dev(h);
+        if (rc) return rc;
+        if (!out || !albedo || !emiss || !Qdir0 || !T0 || nscen <= 0 || M < 1 || M > 128 || !(depth > 0) ||
+            !(ratio > 0) || !(k_th > 0) || !(rho_c > 0))
+            return set_error(VF_EINVAL, "vf_ts_create: bad arguments");
+        TState* S = nullptr;
+        rc = device_ts_create(h, nscen, M, depth, ratio, k_th, rho_c, H, albedo, emiss, Qdir0, T0, &S);
+        *out = reinterpret_cast<vf_tstate>(S);
+        return rc;
+    })
+}
+
+int vf_ts_step(vf_tstate s, const void* Qdir, double dt, void* Tsurf) {
+    GUARD({
+        if (!s || !Qdir || !(dt > 0)) return set_error(VF_EINVAL, "vf_ts_step: bad arguments");
+        return device_ts_step(reinterpret_cast<TState*>(s), Qdir, dt, Tsurf);
+    })
+}
+
+int vf_ts_get(vf_tstate s, void* Qrefl, void* Qir, void* Qabs, void* Tsurf) {
+    GUARD({
+        if (!s) return set_error(VF_EINVAL, "vf_ts_get: null state");
+        return device_ts_get(reinterpret_cast<TState*>(s), Qrefl, Qir, Qabs, Tsurf);
+    })
+}
+
+int vf_ts_free(vf_tstate s) {
+    device_ts_free(reinterpret_cast<TState*>(s));
+    return VF_OK;
+}
+
 int vf_last_solve_stats(vf_handle hh, int* it1, double* r1, int* it2, double* r2) {
     if (!hh) return set_error(VF_EINVAL, "null handle");
     Handle* h = reinterpret_cast<Handle*>(hh);

@@ -1616,6 +1616,98 @@ __global__ void rows_decide_kernel(Ctl* ctl, const unsigned char* recv, int64_t 
     }
 }
 
+// ---- Alg. 6 time stepping (NEXT-1).  State in tree
+// order, row-major [r][c] over the nscen scenarios; column profiles
+// layer-major [j][r][c] (coalesced over r, c).
+// RHS of one step: X[:, c] = alpha (Qdir^(n+1) + Qrefl^(n)), X[:, s + c] =
+// Qrad^(n) + (1 - eps) Qir^(n); Qdir arrives in caller order (gathered by perm).
+template <typename T>
+__global__ void ts_rhs_kernel(const T* Qdir, const int32_t* perm, int64_t N, int ns, int kp, const T* alpha,
+                              const T* emis, const T* Qrefl, const T* Qir, const T* Qrad, T* Qd, T* X0, T* X1) {
+    const int64_t tot = N * ns;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / ns;
+        const int c = (int)(i - r * ns);
+        const T q = Qdir[(int64_t)perm[r] + (int64_t)c * N];
+        Qd[i] = q;
+        const T xa = alpha[r] * (q + Qrefl[i]), xb = Qrad[i] + (T(1) - emis[r]) * Qir[i];
+        if (X1) { X0[r] = xa; X1[r] = xb; }                       // ns = 1: two column vectors
+        else { X0[r * kp + c] = xa; X0[r * kp + ns + c] = xb; }
+    }
+}
+
+// After the product: clamp (reading A12), Q_abs^(n+1), one Crank-Nicolson
+// step of every column (reading A27: capacity-free surface node balanced at
+// n+1 with eps sigma T^4 linearised about T_0^(n); interior time-centred;
+// bottom flux H; Thomas algorithm), Q_rad, surface T to caller order.
+template <typename T>
+__global__ void ts_post_kernel(int64_t N, int ns, int kp, const uint8_t* active, const T* Y0, const T* Y1,
+                               const T* alpha, const T* emis, const T* Qd, T* Qrefl, T* Qir, T* Qabs, T* Qrad, T* prof,
+                               const double* z, int M, double k_th, double rho_c, double H, double dt,
+                               const int32_t* perm, T* Tout) {
+    const int64_t tot = N * ns;
+    double cp[129], dp[129];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / ns;
+        const int c = (int)(i - r * ns);
+        double qr = 0.0, qi = 0.0;
+        if (active[r]) {
+            qr = (double)(Y1 ? Y0[r] : Y0[r * kp + c]);
+            qi = (double)(Y1 ? Y1[r] : Y0[r * kp + ns + c]);
+        }
+        qr = qr > 0.0 ? qr : 0.0;
+        qi = qi > 0.0 ? qi : 0.0;
+        const double a = (double)alpha[r], e = (double)emis[r];
+        const double qabs = (1.0 - a) * ((double)Qd[i] + qr) + e * qi;
+        Qrefl[i] = (T)qr;
+        Qir[i] = (T)qi;
+        Qabs[i] = (T)qabs;
+        // column i: nodes j = 0..M at prof[(j * N + r) * ns + c]
+        const int64_t st = tot;
+        T* P = prof + i;
+        const double es = e * kSigmaSB;
+        const double t0 = (double)P[0], t1 = (double)P[st];
+        const double R = es * t0 * t0 * t0 * t0, dR = 4.0 * es * t0 * t0 * t0;
+        const double g1 = k_th / (z[1] - z[0]);
+        // surface row: (dR + g1) T0 - g1 T1 = qabs - R + dR t0
+        double b = dR + g1, cc = -g1, rr = qabs - R + dR * t0;
+        cp[0] = cc / b;
+        dp[0] = rr / b;
+        double tm = t0, tj = t1;
+        for (int j = 1; j <= M; ++j) {
+            const double dm = z[j] - z[j - 1];
+            const double gm = k_th / dm;
+            double aa = -0.5 * gm, bb, c2 = 0.0, r2;
+            if (j < M) {
+                const double dpl = z[j + 1] - z[j];
+                const double gp = k_th / dpl;
+                const double tp = (double)P[(int64_t)(j + 1) * st];
+                const double cap = rho_c * 0.5 * (dm + dpl) / dt;
+                bb = cap + 0.5 * (gm + gp);
+                c2 = -0.5 * gp;
+                r2 = cap * tj + 0.5 * (gp * (tp - tj) - gm * (tj - tm));
+                tm = tj;
+                tj = tp;
+            } else {
+                const double cap = rho_c * 0.5 * dm / dt;
+                bb = cap + 0.5 * gm;
+                r2 = cap * tj + 0.5 * (H - gm * (tj - tm)) + 0.5 * H;
+            }
+            const double den = bb - aa * cp[j - 1];
+            cp[j] = c2 / den;
+            dp[j] = (r2 - aa * dp[j - 1]) / den;
+        }
+        double tn = dp[M];
+        P[(int64_t)M * st] = (T)tn;
+        for (int j = M - 1; j >= 0; --j) {
+            tn = dp[j] - cp[j] * tn;
+            P[(int64_t)j * st] = (T)tn;
+        }
+        Qrad[i] = (T)(es * tn * tn * tn * tn);
+        if (Tout) Tout[(int64_t)perm[r] + (int64_t)c * N] = (T)tn;
+    }
+}
+
 }  // namespace
 
 // --------------------------------------------------------------- layout
@@ -3305,6 +3397,172 @@ void device_free(Handle* h) {
     stream::free_dev(&D->sl);
     delete D;
     h->dev = nullptr;
+}
+
+// ---- Alg. 6 state (vf_ts_*): see include/vf.h
+struct TState {
+    Handle* h = nullptr;
+    int ns = 0, kp = 0, M = 0;
+    double k_th = 0, rho_c = 0, H = 0;
+    int64_t steps = 0;
+    void *alpha = nullptr, *emis = nullptr, *Qrefl = nullptr, *Qir = nullptr, *Qabs = nullptr, *Qrad = nullptr,
+         *Qd = nullptr, *prof = nullptr, *Ts = nullptr;
+    double* z = nullptr;
+    void* XT[2] = {nullptr, nullptr};
+    void* Y[2] = {nullptr, nullptr};
+};
+
+namespace {
+
+template <typename T>
+__global__ void ts_init_kernel(const T* Qdir0, const T* T0, const int32_t* perm, int64_t N, int ns, int M,
+                               const T* alpha, double H, T* Qabs, T* Qrad, T* prof) {
+    const int64_t tot = N * ns;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / ns;
+        const int c = (int)(i - r * ns);
+        const int64_t o = (int64_t)perm[r] + (int64_t)c * N;
+        const T qa = (T(1) - alpha[r]) * Qdir0[o] + (T)H;          // Q_abs^(0) = (I - diag alpha) Q_dir^(0) + H
+        Qabs[i] = qa;
+        Qrad[i] = qa;                                             // Q_rad^(0) = Q_abs^(0)
+        for (int j = 0; j <= M; ++j) prof[(int64_t)j * tot + i] = T0[o];
+    }
+}
+
+template <typename T>
+int ts_create_t(Handle* h, int ns, int M, double depth, double ratio, double k_th, double rho_c, double H,
+                const void* albedo, const void* emiss, const void* Qdir0, const void* T0, TState** out) {
+    DeviceHMat* D = h->dev;
+    cudaStream_t st;
+    int rc;
+    if ((rc = stream_of(h, &st))) return rc;
+    std::unique_ptr<TState> S(new TState());
+    S->h = h; S->ns = ns; S->M = M; S->k_th = k_th; S->rho_c = rho_c; S->H = H;
+    S->kp = pad_k(2 * ns);
+    const int64_t N = D->N, w = sizeof(T), tot = N * ns;
+    auto mk = [&](void** p, size_t bytes) -> int {
+        CK(cudaMalloc(p, std::max<size_t>(bytes, 16)));
+        CK(cudaMemsetAsync(*p, 0, std::max<size_t>(bytes, 16), st));
+        return VF_OK;
+    };
+    if ((rc = mk(&S->alpha, N * w)) || (rc = mk(&S->emis, N * w)) || (rc = mk(&S->Qrefl, tot * w)) ||
+        (rc = mk(&S->Qir, tot * w)) || (rc = mk(&S->Qabs, tot * w)) || (rc = mk(&S->Qrad, tot * w)) ||
+        (rc = mk(&S->Qd, tot * w)) || (rc = mk(&S->prof, (M + 1) * tot * w)) || (rc = mk((void**)&S->z, (M + 1) * 8)))
+        return rc;
+    const bool two = ns == 1 && D->sl.ok && !h->comm && D->world == 1;
+    if (two) {
+        for (int q = 0; q < 2; ++q)
+            if ((rc = mk(&S->XT[q], (N + D->NT) * w)) || (rc = mk(&S->Y[q], N * w))) return rc;
+    } else {
+        if ((rc = mk(&S->XT[0], (N + D->NT) * S->kp * w)) || (rc = mk(&S->Y[0], N * S->kp * w))) return rc;
+    }
+    // layer grid (reading A27): thicknesses d_1 r^(j-1), j = 1..M, summing to depth
+    std::vector<double> z(M + 1, 0.0);
+    const double d1 = ratio != 1.0 ? depth * (ratio - 1.0) / (std::pow(ratio, M) - 1.0) : depth / M;
+    for (int j = 1; j <= M; ++j) z[j] = z[j - 1] + d1 * std::pow(ratio, j - 1);
+    CK(cudaMemcpyAsync(S->z, z.data(), (M + 1) * 8, cudaMemcpyHostToDevice, st));
+    const void *ad, *ed, *qd, *td;
+    if ((rc = stage_in(h, 0, albedo, N * w, st, &ad)) || (rc = stage_in(h, 1, emiss, N * w, st, &ed)) ||
+        (rc = stage_in(h, 2, Qdir0, tot * w, st, &qd)) || (rc = stage_in(h, 3, T0, tot * w, st, &td)))
+        return rc;
+    gather2_kernel<T><<<148, 256, 0, st>>>((const T*)ad, (const T*)ed, D->perm, N, (T*)S->alpha, (T*)S->emis);
+    ts_init_kernel<T><<<148 * 4, 256, 0, st>>>((const T*)qd, (const T*)td, D->perm, N, ns, M, (const T*)S->alpha, H,
+                                               (T*)S->Qabs, (T*)S->Qrad, (T*)S->prof);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));          // host inputs were staged: do not return before the copies finish
+    *out = S.release();
+    return VF_OK;
+}
+
+template <typename T>
+int ts_step_t(TState* S, const void* Qdir, double dt, void* Tsurf) {
+    Handle* h = S->h;
+    DeviceHMat* D = h->dev;
+    cudaStream_t st;
+    int rc;
+    if ((rc = stream_of(h, &st))) return rc;
+    const int64_t N = D->N, tot = N * S->ns;
+    const void* qd;
+    void* to = nullptr;
+    if ((rc = stage_in(h, 0, Qdir, tot * sizeof(T), st, &qd))) return rc;
+    if (Tsurf && (rc = stage_out_buf(h, 1, Tsurf, tot * sizeof(T), &to))) return rc;
+    reset_counters(h);
+    const int gb = (int)std::max<int64_t>(1, std::min<int64_t>((tot + 255) / 256, 148 * 8));
+    const bool two = S->XT[1] != nullptr;
+    ts_rhs_kernel<T><<<gb, 256, 0, st>>>((const T*)qd, D->perm, N, S->ns, S->kp, (const T*)S->alpha,
+                                         (const T*)S->emis, (const T*)S->Qrefl, (const T*)S->Qir, (const T*)S->Qrad,
+                                         (T*)S->Qd, (T*)S->XT[0], two ? (T*)S->XT[1] : nullptr);
+    h->launches_total++;
+    if (two) {                               // one F-hat stream per column (nrhs = 1 kernel)
+        for (int q = 0; q < 2; ++q) {
+            int grid = 0;
+            Timer tm(h, st, 2);
+            if ((rc = stream::matvec_k1(D->sl, D->dtype, S->XT[q], S->Y[q], st, &grid))) return rc;
+            h->launches_total++;
+        }
+    } else {
+        if ((rc = ensure_scratch(D, S->kp, st))) return rc;
+        HotArgs a = hot_args(D, S->kp, 2 * S->ns);
+        a.xt0 = S->XT[0];
+        a.Y = S->Y[0];
+        if ((rc = launch_hot<T, M_MATVEC>(h, a, st))) return rc;
+    }
+    ts_post_kernel<T><<<gb, 128, 0, st>>>(N, S->ns, S->kp, D->active, (const T*)S->Y[0], two ? (const T*)S->Y[1] : nullptr,
+                                          (const T*)S->alpha, (const T*)S->emis, (const T*)S->Qd, (T*)S->Qrefl,
+                                          (T*)S->Qir, (T*)S->Qabs, (T*)S->Qrad, (T*)S->prof, S->z, S->M, S->k_th,
+                                          S->rho_c, S->H, dt, D->perm, (T*)to);
+    h->launches_total++;
+    CK(cudaGetLastError());
+    if (to && (rc = stage_out_copy(Tsurf, to, tot * sizeof(T), st))) return rc;
+    if (qd != Qdir || (to && to != Tsurf) || h->timing) CK(cudaStreamSynchronize(st));
+    if (h->timing) collect_timing(h);
+    S->steps++;
+    return VF_OK;
+}
+
+template <typename T>
+int ts_get_t(TState* S, void* Qrefl, void* Qir, void* Qabs, void* Tsurf) {
+    Handle* h = S->h;
+    DeviceHMat* D = h->dev;
+    cudaStream_t st;
+    int rc;
+    if ((rc = stream_of(h, &st))) return rc;
+    const int64_t N = D->N, tot = N * S->ns;
+    void* srcs[4] = {S->Qrefl, S->Qir, S->Qabs, S->prof};     // prof layer 0 = surface T
+    void* dsts[4] = {Qrefl, Qir, Qabs, Tsurf};
+    for (int q = 0; q < 4; ++q) {
+        if (!dsts[q]) continue;
+        void* o;
+        if ((rc = stage_out_buf(h, 2 + q, dsts[q], tot * sizeof(T), &o))) return rc;
+        // tree [r][c] -> caller column-major (the kp = ns layout of permute_out)
+        launch_permute_out<T>(h, srcs[q], S->ns, S->ns, false, o, st);
+        if ((rc = stage_out_copy(dsts[q], o, tot * sizeof(T), st))) return rc;
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(st));
+    return VF_OK;
+}
+
+}  // namespace
+
+int device_ts_create(Handle* h, int ns, int M, double depth, double ratio, double k_th, double rho_c, double H,
+                     const void* albedo, const void* emiss, const void* Qdir0, const void* T0, TState** out) {
+    return h->dtype == VF_F64 ? ts_create_t<double>(h, ns, M, depth, ratio, k_th, rho_c, H, albedo, emiss, Qdir0, T0, out)
+                              : ts_create_t<float>(h, ns, M, depth, ratio, k_th, rho_c, H, albedo, emiss, Qdir0, T0, out);
+}
+int device_ts_step(TState* S, const void* Qdir, double dt, void* Tsurf) {
+    return S->h->dtype == VF_F64 ? ts_step_t<double>(S, Qdir, dt, Tsurf) : ts_step_t<float>(S, Qdir, dt, Tsurf);
+}
+int device_ts_get(TState* S, void* Qrefl, void* Qir, void* Qabs, void* Tsurf) {
+    return S->h->dtype == VF_F64 ? ts_get_t<double>(S, Qrefl, Qir, Qabs, Tsurf) : ts_get_t<float>(S, Qrefl, Qir, Qabs, Tsurf);
+}
+void device_ts_free(TState* S) {
+    if (!S) return;
+    cudaSetDevice(S->h->device);
+    void* ps[] = {S->alpha, S->emis, S->Qrefl, S->Qir, S->Qabs, S->Qrad, S->Qd, S->prof, S->z, S->XT[0], S->XT[1],
+                  S->Y[0], S->Y[1]};
+    for (void* p : ps) if (p) cudaFree(p);
+    delete S;
 }
 
 int device_matvec(Handle* h, const void* X, void* Y, int nrhs) {

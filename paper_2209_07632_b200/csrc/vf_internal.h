@@ -103,6 +103,13 @@ int device_solve_radiosity(Handle* h, const void* E, const void* rho, void* B, i
 int device_solve_thermal(Handle* h, const void* Qdir, const void* alb, const void* emi, void* T,
                          void* Qvis, void* Qir, int nrhs, int iters, double tol);
 int64_t device_bytes(const Handle* h);
+// Alg. 6 time stepping (vf_device.cu)
+struct TState;
+int device_ts_create(Handle* h, int ns, int M, double depth, double ratio, double k_th, double rho_c, double H,
+                     const void* albedo, const void* emiss, const void* Qdir0, const void* T0, TState** out);
+int device_ts_step(TState* S, const void* Qdir, double dt, void* Tsurf);
+int device_ts_get(TState* S, void* Qrefl, void* Qir, void* Qabs, void* Tsurf);
+void device_ts_free(TState* S);
 
 // truncated SVD (vf_svd.cpp)
 struct SvdResult {
