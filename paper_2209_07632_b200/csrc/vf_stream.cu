@@ -104,8 +104,12 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_k1_kernel(SArgs<T> a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr unsigned FULL = 0xffffffffu;
     unsigned char* ring = sm + (size_t)warp * NS * kSlot;
-    int32_t* xi = reinterpret_cast<int32_t*>(sm + (size_t)NW * NS * kSlot) + warp * kMaxTerms;
-    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + (size_t)NW * NS * kSlot + (size_t)NW * kMaxTerms * 4) + warp * NS;
+    // per warp: piece records [32] (int4) + start bitmap [kMaxTerms / 32] words
+    int4* prec = reinterpret_cast<int4*>(sm + (size_t)NW * NS * kSlot) + warp * kMaxPieces;
+    unsigned* pw = reinterpret_cast<unsigned*>(sm + (size_t)NW * NS * kSlot + (size_t)NW * kMaxPieces * 16) +
+                   warp * (kMaxTerms / 32);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(sm + (size_t)NW * NS * kSlot + (size_t)NW * kMaxPieces * 16 +
+                                                (size_t)NW * (kMaxTerms / 32) * 4) + warp * NS;
     if (threadIdx.x == 0) cta_arrived = 0;
     if (lane == 0)
         for (int s = 0; s < NS; ++s) mbar_init(bar + s, 1);
@@ -242,27 +246,44 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_k1_kernel(SArgs<T> a) {
                 if (lane >= off) { incl += v; cincl += cv; }
             }
             const int excl = incl - len, cexcl = cincl - clen;
-            // pass A: the XT row of every term, piece by piece (lanes over the piece's terms)
-            for (int q = 0; q < np; ++q) {
-                const int q_src = __shfl_sync(FULL, my.src, q), q_len = __shfl_sync(FULL, len, q);
-                const int q_kind = __shfl_sync(FULL, (int)my.kind, q);
-                const int q_ex = __shfl_sync(FULL, excl, q), q_cex = __shfl_sync(FULL, cexcl, q);
-                for (int e = lane; e < q_len; e += 32)
-                    xi[q_ex + e] = q_src + (q_kind ? (int)ix[q_cex + e] : e);
+            // piece lookup without a search: a bitmap of piece starts over the
+            // chunk's terms (word w covers terms 32w .. 32w+31); the piece of term
+            // t = 32w + l is (pieces starting before wave w) + popc(word_w up to
+            // bit l) - 1.  Piece records (src, first term, first u16 slot, kind) in smem.
+            constexpr int NWORD = kMaxTerms / 32;
+            if (lane < NWORD) pw[lane] = 0u;
+            __syncwarp();
+            if (lane < np) {
+                atomicOr(pw + (excl >> 5), 1u << (excl & 31));
+                prec[lane] = make_int4(my.src, excl, cexcl, (int)my.kind);
             }
             __syncwarp();
-            // pass B: every term's gather in flight, U per lane
+            const unsigned wl = lane < NWORD ? pw[lane] : 0u;
+            int wcnt = __popc(wl), wincl = wcnt;
+#pragma unroll
+            for (int off = 1; off < 32; off <<= 1) {
+                const int v = __shfl_up_sync(FULL, wincl, off);
+                if (lane >= off) wincl += v;
+            }
+            const int wexcl = wincl - wcnt;             // pieces starting before wave `lane`
+            const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
+            const int nw = (nt + 31) >> 5;
             constexpr int U = VF_SK1_U;
-            for (int t0 = 0; t0 < nt; t0 += 32 * U) {
+            for (int w0 = 0; w0 < nw; w0 += U) {
                 T v[U], x[U];
 #pragma unroll
                 for (int u = 0; u < U; ++u) {
-                    const int t = t0 + 32 * u + lane;
+                    const int w = w0 + u;
+                    const int t = 32 * w + lane;
                     v[u] = T(0);
                     x[u] = T(0);
+                    const unsigned word = pw[w < NWORD ? w : 0];
+                    const int base = __shfl_sync(FULL, wexcl, w & 31);
                     if (t < nt) {
+                        const int4 pr = prec[base + __popc(word & upto) - 1];
+                        const int e = t - pr.y;
                         v[u] = vals[t];
-                        x[u] = XT[xi[t]];
+                        x[u] = XT[pr.x + (pr.w ? (int)ix[pr.z + e] : e)];
                     }
                 }
 #pragma unroll
@@ -291,7 +312,7 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_k1_kernel(SArgs<T> a) {
 }  // namespace
 
 #ifndef VF_SK1_WARPS
-#define VF_SK1_WARPS 14
+#define VF_SK1_WARPS 16
 #endif
 #ifndef VF_SK1_STAGES
 #define VF_SK1_STAGES 3
@@ -299,7 +320,10 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_k1_kernel(SArgs<T> a) {
 constexpr int kNW = VF_SK1_WARPS;    // warps per CTA (one CTA per SM)
 constexpr int kNS = VF_SK1_STAGES;   // ring slots per warp
 
-size_t smem_bytes() { return (size_t)kNW * kNS * kSlot + (size_t)kNW * kMaxTerms * 4 + (size_t)kNW * kNS * 8; }
+size_t smem_bytes() {
+    return (size_t)kNW * kNS * kSlot + (size_t)kNW * kMaxPieces * 16 + (size_t)kNW * (kMaxTerms / 32) * 4 +
+           (size_t)kNW * kNS * 8;
+}
 
 #define SCK(call)                                                                        \
     do {                                                                                 \
