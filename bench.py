@@ -536,7 +536,9 @@ def _pad(n):
 def matvec_chunks(info, k, rows_mode):
     """The launches libvf's vf_matvec issues for k columns (matvec_impl's
     column rules): one entry per launch, its column count."""
-    big = not rows_mode and info["device_bytes"] > (256 << 20) and not info.get("stream_batched")
+    if not rows_mode and info.get("tiles", 0) > 0 and k > 8:
+        return [k]                                    # one streamed-tile launch
+    big = not rows_mode and info["device_bytes"] > (256 << 20)
     if big and 2 <= k <= 8:
         return [1] * k
     if big and k > 64:
@@ -639,7 +641,7 @@ def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
     if max(chunks) > 2:
         smax = pk.get("sm_max_mhz", 1965.0)
         peak_tf = fp64_peak_tflops(smax) if dt == "f64" else fp32_peak_tflops(smax)
-        dmma = bool(info.get("stream_batched")) and dt == "f64"
+        dmma = info.get("tiles", 0) > 0 and dt == "f64" and max(chunks) > 8
         bound = {"bound": "tensor" if dmma else "alu", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
                  "frac": ach_tf / peak_tf,
                  "peak_basis": (("derived FP64 DMMA peak (= the DFMA rate on B200): " if dmma else "derived: ")
@@ -653,6 +655,9 @@ def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
     if max(chunks) <= 2:
         kern = (f"stream_k1_kernel<{tn}> (bulk-copy chunk stream: phase 1 T = S V^T x, warp-granular grid barrier, "
                 "phase 2 row-owner accumulate)" if stream and max(chunks) == 1 else f"hot_kernel<{tn},1,VEC,M_MATVEC>")
+    elif info.get("tiles", 0) > 0 and dt == "f64":
+        kern = ("bt_kernel (streamed 16-row tiles, [K][16] weights x staged XT rows on FP64 tensor cores, DMMA "
+                "m8n8k4; phase 1 T tiles, grid barrier, phase 2 row tiles)")
     else:
         kern = f"hot_kernel<{tn},32,VEC,M_MATVEC> (wide per-row: warp across 32 VEC columns)"
     return {**bound, "traffic": traffic, "traffic_source": traffic_src,

@@ -250,6 +250,10 @@ typedef struct {
     int64_t stream_payload_bytes;
     int64_t stream_meta_bytes;
     int64_t stream_chunks;
+    /* streamed-tile layout of wide batches (FP64, F-hat beyond the resident
+       layout): tiles and sum over tiles of their K (16 K weights each)        */
+    int64_t tiles;
+    int64_t tile_sources;
 } vf_info_t;
 
 int vf_info(vf_handle h, vf_info_t* out);

@@ -1269,6 +1269,149 @@ __global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) 
     }
 }
 
+// ---- streamed-tile batched apply (nrhs >= 16 on an F-hat too large for the
+// resident layout, e.g. configs[2] at nrhs = 128).  A tile is up to 16 output
+// rows -- phase 1: <= 16 T rows of one SVD block (sources = its V rows),
+// phase 2: 16 consecutive active tree rows (sources = the union of their
+// dense / U runs and merged-CSR columns) -- with its weights stored as one
+// [K][16] block (zeros where a row has no term; S folded into V), so the
+// tile's product is a dense 16 x K by K x nrhs contraction on the FP64
+// tensor cores (DMMA m8n8k4).  Per slice of kBKS sources the CTA stages the
+// weight slice (streamed from HBM) and the sources' XT rows (L2) with cp.async
+// into a 2-slot ring; warp w owns a 16-column chunk (and a K-part when there
+// are fewer than 8 chunks).  Every source row is staged once per tile and
+// reused by all 16 rows (SURVEY §8(d) caveat: X_J slices reused across the
+// block row).  Tiles come from two global queues (phase 1, grid barrier,
+// phase 2); each output element is summed by one warp in a fixed order and
+// K-parts are added in part order: bitwise reproducible.
+constexpr int kBKS = 32;            // sources per staged slice
+constexpr int kBCols = 128;         // columns per pass over a tile
+struct BTile {
+    int32_t nrows, K;
+    int64_t w_off;                  // [K][16] weights (swizzled: row r of source j at j*16 + (r ^ 4 (j & 3)))
+    int64_t s_off;                  // K source XT rows
+    int64_t out_off;                // 16 output rows (tree rows, or T rows for phase 1)
+};
+struct BArgs {
+    const BTile* tiles;             // phase-1 tiles [0, n1), then phase-2 tiles [n1, n1 + n2)
+    int32_t n1, n2;
+    const double* W;
+    const int32_t* src;
+    const int32_t* outrow;
+    double* XT;                     // (N + NT) x kp, row-major, tree order
+    double* Y;                      // N x kp
+    int64_t N;
+    int kp;
+    int32_t* ctr;                   // [0] phase-1 queue, [1] phase-2 queue
+    Ctl* ctl;
+};
+
+__global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
+    extern __shared__ __align__(16) double bsm[];
+    __shared__ int s_item;
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int kr = lane & 3, mn = lane >> 2;
+    for (int phase = 1; phase <= 2; ++phase) {
+        const int nt = phase == 1 ? a.n1 : a.n2, base = phase == 1 ? 0 : a.n1;
+        for (;;) {
+            __syncthreads();
+            if (t == 0) s_item = atomicAdd(a.ctr + phase - 1, 1);
+            __syncthreads();
+            const int it = s_item;
+            if (it >= nt) break;
+            const BTile B = a.tiles[base + it];
+            const double* Wt = a.W + B.w_off;
+            const int32_t* S = a.src + B.s_off;
+            const int nsl = (B.K + kBKS - 1) / kBKS;
+            for (int cb = 0; cb < a.kp; cb += kBCols) {
+                const int KPB = min(kBCols, a.kp - cb);          // 16, 32, 64 or 128 columns
+                const int nch = KPB >> 4, nkp = 8 / nch;
+                const int cw = warp % nch, pw = warp / nch;
+                double* Wsm = bsm;                                 // [2][kBKS][16]
+                double* Xsm = bsm + 2 * kBKS * 16;                 // [2][kBKS][KPB]
+                auto stage = [&](int sl, int slot) {
+                    const int j0 = sl * kBKS, n = min(kBKS, B.K - j0);
+                    double* wd = Wsm + slot * kBKS * 16;
+                    double* xd = Xsm + slot * kBKS * KPB;
+                    for (int op = t; op < kBKS * 8; op += 256) {   // 16-B copies of the weight slice
+                        const int j = op >> 3;
+                        cpa<16>(wd + op * 2, Wt + (int64_t)j0 * 16 + op * 2, j < n ? 16 : 0);
+                    }
+                    const int per = KPB >> 1;                      // 16-B copies per staged row
+                    for (int op = t; op < kBKS * per; op += 256) {
+                        const int j = op / per, part = op - j * per;
+                        const int c = part * 2;
+                        const bool ok = j < n;
+                        const int64_t row = ok ? S[j0 + j] : 0;
+                        cpa<16>(xd + j * KPB + (c ^ (4 * (j & 3))), a.XT + row * a.kp + cb + c, ok ? 16 : 0);
+                    }
+                };
+                double dacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+                stage(0, 0);
+                cpa_commit();
+                for (int sl = 0; sl < nsl; ++sl) {
+                    if (sl + 1 < nsl) stage(sl + 1, (sl + 1) & 1);
+                    cpa_commit();
+                    cpa_wait<1>();
+                    __syncthreads();
+                    const double* W0 = Wsm + (sl & 1) * kBKS * 16;
+                    const double* X0 = Xsm + (sl & 1) * kBKS * KPB;
+                    const int cc = cw * 16;
+#pragma unroll
+                    for (int ks = 0; ks < kBKS / 4; ++ks) {
+                        if (ks % nkp != pw) continue;
+                        const int j = ks * 4 + kr;
+                        const int sw = 4 * kr;
+                        const double a0 = W0[j * 16 + (mn ^ sw)], a1 = W0[j * 16 + ((8 + mn) ^ sw)];
+                        const double b0 = X0[j * KPB + ((cc + mn) ^ sw)], b1 = X0[j * KPB + ((cc + 8 + mn) ^ sw)];
+                        dmma884(dacc[0], a0, b0);
+                        dmma884(dacc[1], a0, b1);
+                        dmma884(dacc[2], a1, b0);
+                        dmma884(dacc[3], a1, b1);
+                    }
+                    __syncthreads();                               // slot (sl & 1) free for slice sl + 2
+                }
+                cpa_wait<0>();
+                // K-parts of a column chunk meet in smem, added in part order
+                double* red = Xsm + 2 * kBKS * kBCols;             // [8 warps][4 tiles][32 lanes][2]
+                if (nkp > 1) {
+#pragma unroll
+                    for (int tl = 0; tl < 4; ++tl) {
+                        red[((warp * 4 + tl) * 32 + lane) * 2] = dacc[tl][0];
+                        red[((warp * 4 + tl) * 32 + lane) * 2 + 1] = dacc[tl][1];
+                    }
+                    __syncthreads();
+                    if (pw == 0) {
+#pragma unroll
+                        for (int tl = 0; tl < 4; ++tl) {
+                            double s0 = 0.0, s1 = 0.0;
+                            for (int q = 0; q < nkp; ++q) {
+                                const int w2 = q * nch + cw;
+                                s0 += red[((w2 * 4 + tl) * 32 + lane) * 2];
+                                s1 += red[((w2 * 4 + tl) * 32 + lane) * 2 + 1];
+                            }
+                            dacc[tl][0] = s0;
+                            dacc[tl][1] = s1;
+                        }
+                    }
+                }
+                if (pw == 0) {
+#pragma unroll
+                    for (int tl = 0; tl < 4; ++tl) {
+                        const int r = (tl >> 1) * 8 + mn;
+                        if (r >= B.nrows) continue;
+                        const int64_t orow = a.outrow[B.out_off + r];
+                        const int col = cb + cw * 16 + (tl & 1) * 8 + 2 * kr;
+                        double* dst = phase == 1 ? a.XT + (a.N + orow) * a.kp + col : a.Y + orow * a.kp + col;
+                        *reinterpret_cast<double2*>(dst) = make_double2(dacc[tl][0], dacc[tl][1]);
+                    }
+                }
+            }
+        }
+        if (phase == 1) grid_sync(a.ctl, gridDim.x);                // T rows complete before phase 2 reads them
+    }
+}
+
 // The persistent hot-path kernel (a2-a5).  MODE = M_MATVEC: phase 1, grid
 // barrier, phase 2 -> Y.  MODE = M_SOLVE: Jacobi iterations until every
 // column has r <= tol or `iters` is reached.  GROUPED selects the row-group
@@ -1797,6 +1940,13 @@ struct DeviceHMat {
     size_t slot_cap = 0;
     // chunk-stream layout of the nrhs = 1 apply (vf_stream.cu)
     stream::DevLayout sl;
+    // streamed-tile layout of wide batches on a large F-hat (bt_kernel, FP64)
+    bool bt_ok = false;
+    BTile* bt_tiles = nullptr;
+    double* bt_W = nullptr;
+    int32_t *bt_src = nullptr, *bt_out = nullptr, *bt_ctr = nullptr;
+    int32_t bt_n1 = 0, bt_n2 = 0;
+    int64_t bt_cells = 0;
     // staging for host pointers
     void* stage[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     size_t stage_cap[6] = {0, 0, 0, 0, 0, 0};
@@ -2632,6 +2782,92 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             D->res_scap = (int)std::max<int64_t>(smax, 4);
         }
     }
+    if (!D->res_ok && !h->sharded && sizeof(T) == 8 && !getenv("VF_NO_TILES") && (D->n_g1 + D->n_p2) > 0) {
+        // streamed-tile layout (bt_kernel): phase-1 tiles = the row groups of T
+        // rows (one SVD block, shared V rows), phase-2 tiles = 16 consecutive
+        // active rows with the union of their sources; LPT order by K per phase
+        struct HT { int phase; std::vector<int32_t> srcs; std::vector<double> w; int nrows; std::array<int32_t, 16> out; };
+        std::vector<HT> t1(g1v.size());
+        const int64_t n2t = (D->n_p2 + 15) / 16;
+        std::vector<HT> t2((size_t)n2t);
+#pragma omp parallel for schedule(dynamic, 16)
+        for (int64_t g = 0; g < (int64_t)g1v.size(); ++g) {
+            const Group& G = g1v[g];
+            const GSeg& sg = gsegv[G.seg_off];
+            HT& x = t1[g];
+            x.phase = 1; x.nrows = G.nrows;
+            x.srcs.resize(sg.len);
+            x.w.assign((size_t)sg.len * 16, 0.0);
+            for (int r = 0; r < 16; ++r) x.out[r] = r < G.nrows ? grow1v[g * kGroup + r] : 0;
+            for (int32_t j = 0; j < sg.len; ++j) {
+                x.srcs[j] = sg.kind ? idx[sg.src + j] : (int32_t)(sg.src + j);
+                for (int r = 0; r < G.nrows; ++r)
+                    x.w[(size_t)j * 16 + (r ^ (4 * (j & 3)))] =
+                        (double)vals[gvov[G.seg_off * kGroup + r] + j] * (double)p1_scale[grow1v[g * kGroup + r]];
+            }
+        }
+#pragma omp parallel for schedule(dynamic, 4)
+        for (int64_t tt = 0; tt < n2t; ++tt) {
+            HT& x = t2[tt];
+            x.phase = 2;
+            const int64_t r0 = tt * 16, r1 = std::min<int64_t>(r0 + 16, D->n_p2);
+            x.nrows = (int)(r1 - r0);
+            std::vector<std::array<int64_t, 3>> trip;          // (source XT row, tile row, value offset or -1-csr)
+            for (int64_t r = r0; r < r1; ++r) {
+                x.out[r - r0] = p2_rows[r];
+                for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1]; ++q) {
+                    const Seg& sg = segs[q];
+                    for (int32_t e = 0; e < sg.len; ++e)
+                        trip.push_back({sg.kind ? (int64_t)idx[sg.src + e] : sg.src + e, r - r0, sg.val_off + e});
+                }
+            }
+            for (int r = x.nrows; r < 16; ++r) x.out[r] = 0;
+            std::sort(trip.begin(), trip.end());
+            for (size_t e = 0; e < trip.size(); ++e)
+                if (e == 0 || trip[e][0] != trip[e - 1][0]) x.srcs.push_back((int32_t)trip[e][0]);
+            x.w.assign(x.srcs.size() * 16, 0.0);
+            size_t j = 0;
+            for (size_t e = 0; e < trip.size(); ++e) {
+                if (e > 0 && trip[e][0] != trip[e - 1][0]) ++j;
+                x.w[j * 16 + ((size_t)trip[e][1] ^ (4 * (j & 3)))] = (double)vals[trip[e][2]];
+            }
+        }
+        std::vector<int64_t> o1(t1.size()), o2(t2.size());
+        std::iota(o1.begin(), o1.end(), 0);
+        std::iota(o2.begin(), o2.end(), 0);
+        std::stable_sort(o1.begin(), o1.end(), [&](int64_t x, int64_t y) { return t1[x].srcs.size() > t1[y].srcs.size(); });
+        std::stable_sort(o2.begin(), o2.end(), [&](int64_t x, int64_t y) { return t2[x].srcs.size() > t2[y].srcs.size(); });
+        std::vector<BTile> tiles;
+        std::vector<double> W;
+        std::vector<int32_t> src, out;
+        int64_t wn = 0, sn = 0;
+        for (auto* v : {&t1, &t2}) for (auto& x : *v) { wn += (int64_t)x.w.size(); sn += (int64_t)x.srcs.size(); }
+        W.reserve(wn); src.reserve(sn);
+        auto add = [&](HT& x) {
+            BTile B{x.nrows, (int32_t)x.srcs.size(), (int64_t)W.size(), (int64_t)src.size(), (int64_t)out.size()};
+            W.insert(W.end(), x.w.begin(), x.w.end());
+            src.insert(src.end(), x.srcs.begin(), x.srcs.end());
+            out.insert(out.end(), x.out.begin(), x.out.end());
+            tiles.push_back(B);
+            std::vector<double>().swap(x.w);
+        };
+        for (int64_t q : o1) add(t1[q]);
+        for (int64_t q : o2) add(t2[q]);
+        if (tiles.empty()) tiles.push_back(BTile{});
+        if (W.empty()) W.resize(16, 0.0);
+        if (src.empty()) src.resize(4, 0);
+        if (out.empty()) out.resize(16, 0);
+        if ((rc = up((void**)&D->bt_tiles, tiles.data(), tiles.size() * sizeof(BTile))) ||
+            (rc = up((void**)&D->bt_W, W.data(), W.size() * 8)) ||
+            (rc = up((void**)&D->bt_src, src.data(), src.size() * 4)) ||
+            (rc = up((void**)&D->bt_out, out.data(), out.size() * 4)) ||
+            (rc = up((void**)&D->bt_ctr, nullptr, 16)))
+            return rc;
+        D->bt_n1 = (int32_t)t1.size();
+        D->bt_n2 = (int32_t)t2.size();
+        D->bt_cells = wn / 16;
+        D->bt_ok = true;
+    }
     if (!h->sharded && !getenv("VF_NO_STREAM")) {
         // the nrhs = 1 chunk stream (an F-hat copy in the layout of vf_stream.cu)
         stream::HostLayout SL;
@@ -2981,9 +3217,38 @@ int launch_res(Handle* h, HotArgs& a, cudaStream_t st) {
     return VF_OK;
 }
 
+// Cooperative launch of the streamed-tile kernel (2 CTAs per SM).
+int launch_bt(Handle* h, HotArgs& ha, cudaStream_t st) {
+    DeviceHMat* D = h->dev;
+    const size_t smem = (size_t)(2 * kBKS * 16 + 2 * kBKS * kBCols + 8 * 4 * 32 * 2) * 8;
+    CK(cudaFuncSetAttribute(bt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bt_kernel, 256, smem));
+    if (per_sm < 1) return set_error(VF_ECUDA, "bt_kernel cannot be resident");
+    int nsm = 148;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
+    const int grid = nsm * std::min(per_sm, 2);
+    BArgs b{D->bt_tiles, D->bt_n1, D->bt_n2, D->bt_W, D->bt_src, D->bt_out, (double*)ha.xt0, (double*)ha.Y, D->N,
+            ha.kp, D->bt_ctr, D->ctl};
+    CK(cudaMemsetAsync(D->bt_ctr, 0, 16, st));
+    CK(cudaMemsetAsync(D->ctl, 0, offsetof(Ctl, bar_gen), st));
+    void* args[] = {&b};
+    {
+        Timer tm(h, st, 2);
+        CK(cudaLaunchCooperativeKernel((const void*)bt_kernel, dim3(grid), dim3(256), args, smem, st));
+    }
+    h->launches_total++;
+    D->last_grid = grid;
+    return VF_OK;
+}
+
 template <typename T, int MODE>
 int launch_hot(Handle* h, HotArgs& a, cudaStream_t st) {
     const int kp = a.kp;
+    // wide batches on an F-hat that does not fit the resident layout: streamed tiles (FP64 matvec)
+    if (MODE == M_MATVEC && std::is_same<T, double>::value && kp >= 16 && h->dev->bt_ok &&
+        (kp <= kBCols ? (kp == 16 || kp == 32 || kp == 64 || kp == 128) : kp % kBCols == 0))
+        return launch_bt(h, a, st);
     if (kp >= 16 && kp % 16 == 0 && h->dev->res_ok &&
         (size_t)h->dev->res_wcap * sizeof(T) + (size_t)h->dev->res_scap * 4 + (size_t)kRS * kKS * 16 * sizeof(T) +
                 (size_t)kp * 8 + 2048 + (size_t)kRW * 4 * 32 * 2 * 8 + 4096 +
@@ -3165,7 +3430,10 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     cudaStream_t st;
     int rc;
     if ((rc = check_k(nrhs)) || (rc = stream_of(h, &st))) return rc;
-    const int kp = pad_k(nrhs);
+    // more than 8 columns on a streamed-tile layout: one bt_kernel launch with the
+    // columns padded to 16, 32, 64 or a multiple of 128
+    const bool bt = D->bt_ok && sizeof(T) == 8 && !(D->world > 1 || h->comm) && nrhs > 8 && !getenv("VF_NO_TILES_MV");
+    const int kp = bt ? (nrhs <= 16 ? 16 : nrhs <= 32 ? 32 : nrhs <= 64 ? 64 : (nrhs + 127) / 128 * 128) : pad_k(nrhs);
     if ((rc = ensure_scratch(D, kp, st))) return rc;
     reset_counters(h);
     const size_t vb = (size_t)D->N * nrhs * sizeof(T);
@@ -3224,7 +3492,7 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     // loses more to register pressure at VEC = 4 than it saves in F-hat
     // reads).  VF_MV_CHUNK=c forces chunks of c columns (tests), 0 = off.
     const char* ch = getenv("VF_MV_CHUNK");
-    const int chunk = ch ? atoi(ch) : (D->bytes > ((int64_t)256 << 20) ? 64 : 0);
+    const int chunk = bt ? 0 : ch ? atoi(ch) : (D->bytes > ((int64_t)256 << 20) ? 64 : 0);
     if (split) {
         for (int c = 0; c < nrhs; ++c)
             if ((rc = apply((const T*)Xd + (size_t)c * D->N, (T*)Yd + (size_t)c * D->N, 1, 1))) return rc;
@@ -3395,6 +3663,8 @@ void device_free(Handle* h) {
     for (auto& e : D->evpool) if (e) cudaEventDestroy(e);
     for (auto& kv : D->sched) { cudaFree(kv.second.ptr); cudaFree(kv.second.items); }
     stream::free_dev(&D->sl);
+    void* bps[] = {D->bt_tiles, D->bt_W, D->bt_src, D->bt_out, D->bt_ctr};
+    for (void* p : bps) if (p) cudaFree(p);
     delete D;
     h->dev = nullptr;
 }
@@ -3587,7 +3857,9 @@ int64_t device_alg_flops(const Handle* h) { return h->dev ? h->dev->alg_flops_pe
 int64_t device_active_rows(const Handle* h) { return h->dev ? h->dev->n_p2 : -1; }
 void device_phase_info(const Handle* h, int64_t* out9) {
     const DeviceHMat* D = h->dev;
-    if (!D) { for (int i = 0; i < 13; ++i) out9[i] = 0; return; }
+    if (!D) { for (int i = 0; i < 15; ++i) out9[i] = 0; return; }
+    out9[13] = D->bt_ok ? (int64_t)D->bt_n1 + D->bt_n2 : 0;
+    out9[14] = D->bt_ok ? D->bt_cells : 0;
     out9[9] = D->res_ok ? 1 : 0;
     out9[10] = D->sl.ok ? D->sl.payload_bytes : 0;
     out9[11] = D->sl.ok ? D->sl.meta_bytes : 0;
