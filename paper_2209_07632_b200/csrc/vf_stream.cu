@@ -27,7 +27,7 @@
 #include "vf_stream.h"
 
 #ifndef VF_SK1_U
-#define VF_SK1_U 8       // phase-2 terms in flight per lane
+#define VF_SK1_U 2       // phase-2 quads (4 terms) in flight per lane
 #endif
 
 namespace vf {
@@ -82,6 +82,21 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+
+// 4 consecutive chunk values from shared memory (16-B aligned: quads start at 4q)
+template <typename T> struct Quad;
+template <> struct Quad<double> {
+    static __device__ __forceinline__ void ld(const double* p, double* v) {
+        const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+    }
+};
+template <> struct Quad<float> {
+    static __device__ __forceinline__ void ld(const float* p, float* v) {
+        const float4 a = *reinterpret_cast<const float4*>(p);
+        v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    }
+};
 
 template <typename T>
 struct SArgs {
@@ -266,28 +281,46 @@ __global__ void __launch_bounds__(NW * 32, 1) stream_k1_kernel(SArgs<T> a) {
                 if (lane >= off) wincl += v;
             }
             const int wexcl = wincl - wcnt;             // pieces starting before wave `lane`
-            const unsigned upto = lane == 31 ? 0xffffffffu : ((2u << lane) - 1u);
-            const int nw = (nt + 31) >> 5;
-            constexpr int U = VF_SK1_U;
-            for (int w0 = 0; w0 < nw; w0 += U) {
-                T v[U], x[U];
+            // lane l takes quads q = 32 i + l of 4 consecutive terms (a warp covers 128
+            // consecutive terms per round: neighbouring lanes gather neighbouring
+            // columns); one bitmap lookup per quad, a piece boundary inside the quad
+            // advances to the next record
+            const int nq = (nt + 3) >> 2;
+            constexpr int UQ = VF_SK1_U;
+            for (int q0 = 0; q0 < nq; q0 += 32 * UQ) {
+                T v[UQ][4], x[UQ][4];
 #pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    const int w = w0 + u;
-                    const int t = 32 * w + lane;
-                    v[u] = T(0);
-                    x[u] = T(0);
-                    const unsigned word = pw[w < NWORD ? w : 0];
-                    const int base = __shfl_sync(FULL, wexcl, w & 31);
-                    if (t < nt) {
-                        const int4 pr = prec[base + __popc(word & upto) - 1];
-                        const int e = t - pr.y;
-                        v[u] = vals[t];
-                        x[u] = XT[pr.x + (pr.w ? (int)ix[pr.z + e] : e)];
+                for (int u = 0; u < UQ; ++u) {
+                    const int q = q0 + 32 * u + lane;
+                    const int t0 = 4 * q;
+                    const int wi = min(t0 >> 5, NWORD - 1);
+                    const unsigned word = pw[wi];
+                    const int base = __shfl_sync(FULL, wexcl, wi);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) { v[u][j] = T(0); x[u][j] = T(0); }
+                    if (t0 < nt) {
+                        const int b = t0 & 31;
+                        int p = base + __popc(word & ((2u << b) - 1u)) - 1;
+                        const unsigned inner = (word >> (b + 1)) & 7u;
+                        Quad<T>::ld(vals + t0, v[u]);
+                        int4 pr = prec[p];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            if (j > 0 && ((inner >> (j - 1)) & 1u)) pr = prec[++p];
+                            const int t = t0 + j;
+                            if (t < nt) {
+                                const int e = t - pr.y;
+                                x[u][j] = XT[pr.x + (pr.w ? (int)ix[pr.z + e] : e)];
+                            } else {
+                                v[u][j] = T(0);
+                            }
+                        }
                     }
                 }
 #pragma unroll
-                for (int u = 0; u < U; ++u) acc = fma(v[u], x[u], acc);
+                for (int u = 0; u < UQ; ++u)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) acc = fma(v[u][j], x[u][j], acc);
             }
             if (h.flags & 1) {
                 T s = acc;
