@@ -216,6 +216,19 @@ int vf_ts_step(vf_tstate s, const void* Qdir, double dt, void* Tsurf);
 int vf_ts_get(vf_tstate s, void* Qrefl, void* Qir, void* Qabs, void* Tsurf);
 int vf_ts_free(vf_tstate s);
 
+/* TEST HOOK (not part of the apply/solve path): one ROWS-mode exchange with
+ * world ranks emulated on the current device in sequence -- every rank's
+ * pack (own rows [bounds[g], bounds[g+1]) of its new iterate + the sum over
+ * its nblk CTA partials per column), the allgather as device copies of the
+ * send slots, every rank's unpack and stop decision -- the kernels the
+ * multi-GPU solve runs, exercised at world > 1 on one GPU.  HOST arrays:
+ * xrank world x N x kp (rank g's iterate, row-major tree order), part
+ * world x kp x nblk, enorm2 k; outputs xout world x N x kp, resid k, and per
+ * rank the iteration count and stop flag after the decision. */
+int vf_selftest_rows_exchange(int world, int kp, int k, int64_t N, const int64_t* bounds, const double* xrank,
+                              const double* part, int nblk, const double* enorm2, double tol, int iters, int iter0,
+                              double* xout, double* resid, int* iter_after, int* done_after);
+
 typedef struct {
     int64_t N;             /* facets                                               */
     int dtype;             /* VF_F64 / VF_F32                                      */

@@ -108,6 +108,7 @@ def lib():
             "vf_ts_step": ([ctypes.c_void_p, P, d, P], i),
             "vf_ts_get": ([ctypes.c_void_p, P, P, P, P], i),
             "vf_ts_free": ([ctypes.c_void_p], i),
+            "vf_selftest_rows_exchange": ([i, i, i, I, P, P, P, i, P, d, i, i, P, P, P, P], i),
             "vf_info": ([H, ctypes.POINTER(vf_info_t)], i),
             "vf_enable_kernel_timing": ([H, i], i),
             "vf_kernel_timing": ([H, ctypes.POINTER(d), ctypes.POINTER(i), ctypes.POINTER(d),
@@ -291,6 +292,27 @@ def vf_solve_thermal(h, Qdir, albedo, emiss, T, Qvis=None, Qir=None, iters: int 
     if kt != k:
         raise ValueError("Qdir/T column counts differ")
     _check(lib().vf_solve_thermal(h, pq, pa, pe, pt, pv, pi, int(k), int(iters), float(tol)))
+
+
+def vf_selftest_rows_exchange(bounds, xrank, part, enorm2, tol, iters, iter0):
+    """Test hook: one ROWS exchange with len(bounds) - 1 ranks emulated on the
+    current device (see include/vf.h).  xrank (world, N, kp), part
+    (world, kp, nblk), enorm2 (k,).  Returns (xout, resid, iter_after, done_after)."""
+    bounds = np.ascontiguousarray(bounds, dtype=np.int64)
+    xrank = np.ascontiguousarray(xrank, dtype=np.float64)
+    part = np.ascontiguousarray(part, dtype=np.float64)
+    enorm2 = np.ascontiguousarray(enorm2, dtype=np.float64)
+    world, N, kp = xrank.shape
+    nblk = part.shape[2]
+    k = enorm2.size
+    xout = np.zeros_like(xrank)
+    resid = np.zeros(k)
+    it = np.zeros(world, dtype=np.int32)
+    dn = np.zeros(world, dtype=np.int32)
+    _check(lib().vf_selftest_rows_exchange(world, kp, k, N, bounds.ctypes.data, xrank.ctypes.data, part.ctypes.data,
+                                           nblk, enorm2.ctypes.data, float(tol), int(iters), int(iter0),
+                                           xout.ctypes.data, resid.ctypes.data, it.ctypes.data, dn.ctypes.data))
+    return xout, resid, it, dn
 
 
 class TimeStepper:

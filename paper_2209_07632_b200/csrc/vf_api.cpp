@@ -9,6 +9,8 @@
 #include <new>
 #include <string>
 
+#include <cuda_runtime.h>
+
 #include "vf_internal.h"
 
 namespace vf {
@@ -241,6 +243,20 @@ int vf_ts_get(vf_tstate s, void* Qrefl, void* Qir, void* Qabs, void* Tsurf) {
     GUARD({
         if (!s) return set_error(VF_EINVAL, "vf_ts_get: null state");
         return device_ts_get(reinterpret_cast<TState*>(s), Qrefl, Qir, Qabs, Tsurf);
+    })
+}
+
+int vf_selftest_rows_exchange(int world, int kp, int k, int64_t N, const int64_t* bounds, const double* xrank,
+                              const double* part, int nblk, const double* enorm2, double tol, int iters, int iter0,
+                              double* xout, double* resid, int* iter_after, int* done_after) {
+    GUARD({
+        if (world < 1 || kp < 1 || k < 1 || k > kp || N < 1 || !bounds || !xrank || !part || nblk < 1 || !enorm2 ||
+            !xout || !resid || !iter_after || !done_after)
+            return set_error(VF_EINVAL, "vf_selftest_rows_exchange: bad arguments");
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) { cudaGetLastError(); return set_error(VF_ENODEV, "no device"); }
+        return selftest_rows_exchange(world, kp, k, N, bounds, xrank, part, nblk, enorm2, tol, iters, iter0, xout,
+                                      resid, iter_after, done_after);
     })
 }
 

@@ -3835,6 +3835,76 @@ void device_ts_free(TState* S) {
     delete S;
 }
 
+// Test hook (vf_selftest_rows_exchange): the ROWS exchange kernels of one
+// Jacobi iteration with world > 1, all ranks emulated on this device in
+// sequence (pack of every rank, then the allgather as device copies of every
+// send slot into every rank's receive buffer, then unpack + decide of every
+// rank).  No launch waits on another, so one GPU can run it.
+int selftest_rows_exchange(int world, int kp, int k, int64_t N, const int64_t* bounds, const double* xrank,
+                           const double* part, int nblk, const double* enorm2, double tol, int iters, int iter0,
+                           double* xout, double* resid, int* iter_after, int* done_after) {
+    int64_t rows_max = 0;
+    for (int g = 0; g < world; ++g) rows_max = std::max<int64_t>(rows_max, bounds[g + 1] - bounds[g]);
+    const size_t tail = ((size_t)rows_max * kp * 8 + 15) & ~(size_t)15;
+    const size_t slot = (tail + (size_t)kp * 8 + 15) & ~(size_t)15;
+    const size_t xb = (size_t)N * kp * 8;
+    std::vector<void*> bufs;
+    auto mk = [&](size_t bytes) -> void* {
+        void* p = nullptr;
+        if (cudaMalloc(&p, std::max<size_t>(bytes, 16)) != cudaSuccess) return nullptr;
+        cudaMemset(p, 0, std::max<size_t>(bytes, 16));
+        bufs.push_back(p);
+        return p;
+    };
+    int rc = VF_OK;
+    std::vector<double*> x0(world), x1(world), prt(world);
+    std::vector<unsigned char*> snd(world), rcv(world);
+    std::vector<Ctl*> ctl(world);
+    int64_t* bd = (int64_t*)mk((world + 1) * 8);
+    double* en = (double*)mk(k * 8);
+    double* rs = (double*)mk(k * 8);
+    for (int g = 0; g < world; ++g) {
+        x0[g] = (double*)mk(xb); x1[g] = (double*)mk(xb); prt[g] = (double*)mk((size_t)kp * nblk * 8);
+        snd[g] = (unsigned char*)mk(slot); rcv[g] = (unsigned char*)mk(slot * world); ctl[g] = (Ctl*)mk(sizeof(Ctl));
+        if (!x0[g] || !x1[g] || !prt[g] || !snd[g] || !rcv[g] || !ctl[g]) rc = set_error(VF_ENOMEM, "selftest alloc");
+    }
+    if (!bd || !en || !rs) rc = set_error(VF_ENOMEM, "selftest alloc");
+    if (rc == VF_OK) {
+        cudaMemcpy(bd, bounds, (world + 1) * 8, cudaMemcpyHostToDevice);
+        cudaMemcpy(en, enorm2, k * 8, cudaMemcpyHostToDevice);
+        Ctl c0{};
+        c0.iter = iter0;
+        for (int g = 0; g < world; ++g) {
+            cudaMemcpy(ctl[g], &c0, sizeof(Ctl), cudaMemcpyHostToDevice);
+            // the new iterate B_{it+1} lives in xt1 when it is even, xt0 when odd (rows_pack_kernel)
+            cudaMemcpy((iter0 & 1) ? x0[g] : x1[g], xrank + (size_t)g * N * kp, xb, cudaMemcpyHostToDevice);
+            cudaMemcpy(prt[g], part + (size_t)g * kp * nblk, (size_t)kp * nblk * 8, cudaMemcpyHostToDevice);
+            const int64_t lo = bounds[g], own = bounds[g + 1] - bounds[g];
+            rows_pack_kernel<double><<<rows_grid(own * kp), 256>>>(ctl[g], x0[g], x1[g], nullptr, lo, own, kp, prt[g],
+                                                                  nblk, (int64_t)tail, snd[g]);
+        }
+        for (int d = 0; d < world; ++d)                  // the allgather: slot g of every receiver <- sender g
+            for (int g = 0; g < world; ++g) cudaMemcpy(rcv[d] + (size_t)g * slot, snd[g], slot, cudaMemcpyDeviceToDevice);
+        for (int g = 0; g < world; ++g) {
+            rows_unpack_kernel<double><<<rows_grid(rows_max * kp), 256>>>(ctl[g], x0[g], x1[g], nullptr, bd, world, kp,
+                                                                         (int64_t)slot, rcv[g]);
+            rows_decide_kernel<<<1, 256>>>(ctl[g], rcv[g], (int64_t)slot, (int64_t)tail, world, k, en, rs, tol, iters);
+        }
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) rc = set_error(VF_ECUDA, std::string("selftest: ") + cudaGetErrorString(e));
+        for (int g = 0; g < world && rc == VF_OK; ++g) {
+            cudaMemcpy(xout + (size_t)g * N * kp, (iter0 & 1) ? x0[g] : x1[g], xb, cudaMemcpyDeviceToHost);
+            Ctl ch;
+            cudaMemcpy(&ch, ctl[g], sizeof(Ctl), cudaMemcpyDeviceToHost);
+            iter_after[g] = ch.iter;
+            done_after[g] = ch.done;
+        }
+        if (rc == VF_OK) cudaMemcpy(resid, rs, k * 8, cudaMemcpyDeviceToHost);
+    }
+    for (void* p : bufs) cudaFree(p);
+    return rc;
+}
+
 int device_matvec(Handle* h, const void* X, void* Y, int nrhs) {
     return h->dtype == VF_F64 ? matvec_impl<double>(h, X, Y, nrhs) : matvec_impl<float>(h, X, Y, nrhs);
 }

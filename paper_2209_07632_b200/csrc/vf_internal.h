@@ -110,6 +110,9 @@ int device_ts_create(Handle* h, int ns, int M, double depth, double ratio, doubl
 int device_ts_step(TState* S, const void* Qdir, double dt, void* Tsurf);
 int device_ts_get(TState* S, void* Qrefl, void* Qir, void* Qabs, void* Tsurf);
 void device_ts_free(TState* S);
+int selftest_rows_exchange(int world, int kp, int k, int64_t N, const int64_t* bounds, const double* xrank,
+                           const double* part, int nblk, const double* enorm2, double tol, int iters, int iter0,
+                           double* xout, double* resid, int* iter_after, int* done_after);
 
 // truncated SVD (vf_svd.cpp)
 struct SvdResult {

@@ -125,3 +125,39 @@ def test_rows_noconv_and_solve_needs_comm(scenes, tmp_path_factory):
     assert e.value.code == vf.VF_ENOCONV
     assert M1.stats()["iters1"] == 3
     assert rel(host(B), B0) <= 1e-12
+
+
+@pytest.mark.parametrize("world,kp,k", [(2, 1, 1), (3, 2, 2), (5, 16, 13), (8, 1, 1), (8, 64, 64)])
+@pytest.mark.parametrize("iter0", [0, 3])
+def test_rows_exchange_kernels_at_world_above_one(world, kp, k, iter0):
+    """The ROWS exchange kernels (pack, unpack, decide) at world = 2..8, all
+    ranks emulated on this one GPU with the allgather done as device copies
+    (vf_selftest_rows_exchange): after the exchange every rank holds every
+    rank's own rows, and all ranks reach the same residuals (sum over ranks in
+    rank order of each rank's CTA partials summed in CTA order, over ||E||),
+    iteration count and stop flag -- the protocol of tests/test_rows_shard.py."""
+    rng = np.random.default_rng(world * 100 + kp)
+    N = 1000 + world * 37
+    cuts = np.sort(rng.choice(np.arange(1, N), world - 1, replace=False))
+    bounds = np.concatenate([[0], cuts, [N]]).astype(np.int64)
+    xrank = rng.random((world, N, kp))
+    nblk = 7
+    part = rng.random((world, kp, nblk)) * 1e-6
+    enorm2 = rng.random(k) + 0.5
+    for tol in (1e-12, 1.0):
+        xout, resid, it, dn = vf.vf_selftest_rows_exchange(bounds, xrank, part, enorm2, tol, 10, iter0)
+        want = np.zeros((N, kp))
+        for g in range(world):
+            want[bounds[g]:bounds[g + 1]] = xrank[g, bounds[g]:bounds[g + 1]]
+        for g in range(world):
+            assert np.array_equal(xout[g], want), g
+        tot = np.zeros(kp)
+        for g in range(world):                       # rank order; each rank's partials in CTA order
+            s = np.zeros(kp)
+            for b in range(nblk):
+                s = s + part[g, :, b]
+            tot = tot + s
+        r = np.sqrt(tot[:k]) / np.sqrt(enorm2)
+        np.testing.assert_allclose(resid, r, rtol=1e-15, atol=0)
+        assert np.all(it == iter0 + 1)
+        assert np.all(dn == (1 if tol == 1.0 else 0))
