@@ -300,16 +300,58 @@ __device__ __forceinline__ void row_accumulate(const Seg* __restrict__ segs, int
 // 4-aligned in idx (upload_impl), the arrays are padded so chunk over-reads
 // stay in bounds, and out-of-range terms are masked to exact zeros.  The sum
 // order is fixed by the layout: results are bitwise reproducible.
+// F-hat value / index stream of the nrhs = 1 kernel: read-once data, loaded
+// without allocating in L1 (VF_K1_NA: ld.global.nc.L1::no_allocate, so the
+// L1 keeps the x lines the gathers reuse) and marked evict-first in L2 (the
+// X/T rows stay resident there)
+#ifndef VF_K1_NA
+#define VF_K1_NA 1
+#endif
+__device__ __forceinline__ uint64_t l2_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double2 ld_stream_d2(const double2* p) {
+#if VF_K1_NA
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;\n"
+                 : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(l2_evict_first()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ float4 ld_stream_f4(const float4* p) {
+#if VF_K1_NA
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;\n"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(l2_evict_first()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ int4 ld_stream_i4(const int4* p) {
+#if VF_K1_NA
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0, %1, %2, %3}, [%4], %5;\n"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p), "l"(l2_evict_first()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
 template <typename T> struct V4;
 template <> struct V4<double> {
     static __device__ __forceinline__ void ld(const double* p, double* v) {
-        const double2 a = __ldg(reinterpret_cast<const double2*>(p)), b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+        const double2 a = ld_stream_d2(reinterpret_cast<const double2*>(p)), b = ld_stream_d2(reinterpret_cast<const double2*>(p) + 1);
         v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
     }
 };
 template <> struct V4<float> {
     static __device__ __forceinline__ void ld(const float* p, float* v) {
-        const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+        const float4 a = ld_stream_f4(reinterpret_cast<const float4*>(p));
         v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
     }
 };
@@ -410,7 +452,7 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
                     vx[c] = VF_XVEC && !g_kind && e + 3 < g_len && ((g_src + e) & (16 / sizeof(T) - 1)) == 0;
                     l1[c] = L1X && (g_kind || g_src < nx);
                     if (g_kind) {
-                        const int4 q = __ldg(reinterpret_cast<const int4*>(idx + g_src + e));
+                        const int4 q = ld_stream_i4(reinterpret_cast<const int4*>(idx + g_src + e));
                         xr[c][0] = q.x; xr[c][1] = q.y; xr[c][2] = q.z; xr[c][3] = q.w;
                         // sorted CSR columns often run consecutively (tree order keeps
                         // near-field neighbours together): one aligned vector load then
@@ -1276,7 +1318,7 @@ __global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) 
 // dense / U runs and merged-CSR columns) -- with its weights stored as one
 // [K][16] block (zeros where a row has no term; S folded into V), so the
 // tile's product is a dense 16 x K by K x nrhs contraction on the FP64
-// tensor cores (DMMA m8n8k4).  Per slice of kBKS sources the CTA stages the
+// tensor cores (DMMA m8n8k4).  Per slice of KS sources the CTA stages the
 // weight slice (streamed from HBM) and the sources' XT rows (L2) with cp.async
 // into a 2-slot ring; warp w owns a 16-column chunk (and a K-part when there
 // are fewer than 8 chunks).  Every source row is staged once per tile and
@@ -1284,8 +1326,12 @@ __global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) 
 // block row).  Tiles come from two global queues (phase 1, grid barrier,
 // phase 2); each output element is summed by one warp in a fixed order and
 // K-parts are added in part order: bitwise reproducible.
-constexpr int kBKS = 32;            // sources per staged slice
 constexpr int kBCols = 128;         // columns per pass over a tile
+#ifndef VF_BT_STAGES
+#define VF_BT_STAGES 4
+#endif
+constexpr int kBStages = VF_BT_STAGES;   // cp.async ring depth (slices of 16 or 32 sources)
+constexpr int kBSlice = 2560;             // doubles per ring slot: max of 16 x (16 + 128), 32 x (16 + 64)
 struct BTile {
     int32_t nrows, K;
     int64_t w_off;                  // [K][16] weights (swizzled: row r of source j at j*16 + (r ^ 4 (j & 3)))
@@ -1322,23 +1368,24 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
             const BTile B = a.tiles[base + it];
             const double* Wt = a.W + B.w_off;
             const int32_t* S = a.src + B.s_off;
-            const int nsl = (B.K + kBKS - 1) / kBKS;
             for (int cb = 0; cb < a.kp; cb += kBCols) {
                 const int KPB = min(kBCols, a.kp - cb);          // 16, 32, 64 or 128 columns
+                const int KS = KPB >= 64 ? 16 : 32;              // sources per slice (kBStages slices in flight)
+                const int nsl = (B.K + KS - 1) / KS;
                 const int nch = KPB >> 4, nkp = 8 / nch;
                 const int cw = warp % nch, pw = warp / nch;
-                double* Wsm = bsm;                                 // [2][kBKS][16]
-                double* Xsm = bsm + 2 * kBKS * 16;                 // [2][kBKS][KPB]
+                double* Wsm = bsm;                                 // [kBStages][KS][16]
+                double* Xsm = bsm + kBStages * KS * 16;            // [kBStages][KS][KPB] (fits kBStages x kBSlice)
                 auto stage = [&](int sl, int slot) {
-                    const int j0 = sl * kBKS, n = min(kBKS, B.K - j0);
-                    double* wd = Wsm + slot * kBKS * 16;
-                    double* xd = Xsm + slot * kBKS * KPB;
-                    for (int op = t; op < kBKS * 8; op += 256) {   // 16-B copies of the weight slice
+                    const int j0 = sl * KS, n = min(KS, B.K - j0);
+                    double* wd = Wsm + slot * KS * 16;
+                    double* xd = Xsm + slot * KS * KPB;
+                    for (int op = t; op < KS * 8; op += 256) {     // 16-B copies of the weight slice
                         const int j = op >> 3;
                         cpa<16>(wd + op * 2, Wt + (int64_t)j0 * 16 + op * 2, j < n ? 16 : 0);
                     }
                     const int per = KPB >> 1;                      // 16-B copies per staged row
-                    for (int op = t; op < kBKS * per; op += 256) {
+                    for (int op = t; op < KS * per; op += 256) {
                         const int j = op / per, part = op - j * per;
                         const int c = part * 2;
                         const bool ok = j < n;
@@ -1347,19 +1394,20 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                     }
                 };
                 double dacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-                stage(0, 0);
-                cpa_commit();
-                for (int sl = 0; sl < nsl; ++sl) {
-                    if (sl + 1 < nsl) stage(sl + 1, (sl + 1) & 1);
-                    cpa_commit();
-                    cpa_wait<1>();
-                    __syncthreads();
-                    const double* W0 = Wsm + (sl & 1) * kBKS * 16;
-                    const double* X0 = Xsm + (sl & 1) * kBKS * KPB;
-                    const int cc = cw * 16;
 #pragma unroll
-                    for (int ks = 0; ks < kBKS / 4; ++ks) {
-                        if (ks % nkp != pw) continue;
+                for (int p = 0; p < kBStages - 1; ++p) {
+                    if (p < nsl) stage(p, p);
+                    cpa_commit();
+                }
+                for (int sl = 0; sl < nsl; ++sl) {
+                    if (sl + kBStages - 1 < nsl) stage(sl + kBStages - 1, (sl + kBStages - 1) % kBStages);
+                    cpa_commit();
+                    cpa_wait<kBStages - 1>();
+                    __syncthreads();
+                    const double* W0 = Wsm + (sl % kBStages) * KS * 16;
+                    const double* X0 = Xsm + (sl % kBStages) * KS * KPB;
+                    const int cc = cw * 16;
+                    for (int ks = pw; ks < KS / 4; ks += nkp) {
                         const int j = ks * 4 + kr;
                         const int sw = 4 * kr;
                         const double a0 = W0[j * 16 + (mn ^ sw)], a1 = W0[j * 16 + ((8 + mn) ^ sw)];
@@ -1369,11 +1417,11 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                         dmma884(dacc[2], a1, b0);
                         dmma884(dacc[3], a1, b1);
                     }
-                    __syncthreads();                               // slot (sl & 1) free for slice sl + 2
+                    __syncthreads();                               // slot free for the slice kBStages ahead
                 }
                 cpa_wait<0>();
                 // K-parts of a column chunk meet in smem, added in part order
-                double* red = Xsm + 2 * kBKS * kBCols;             // [8 warps][4 tiles][32 lanes][2]
+                double* red = bsm + kBStages * kBSlice;            // [8 warps][4 tiles][32 lanes][2]
                 if (nkp > 1) {
 #pragma unroll
                     for (int tl = 0; tl < 4; ++tl) {
@@ -1406,6 +1454,7 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                         *reinterpret_cast<double2*>(dst) = make_double2(dacc[tl][0], dacc[tl][1]);
                     }
                 }
+                __syncthreads();                                   // red / ring reuse by the next pass
             }
         }
         if (phase == 1) grid_sync(a.ctl, gridDim.x);                // T rows complete before phase 2 reads them
@@ -2835,8 +2884,11 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         std::vector<int64_t> o1(t1.size()), o2(t2.size());
         std::iota(o1.begin(), o1.end(), 0);
         std::iota(o2.begin(), o2.end(), 0);
-        std::stable_sort(o1.begin(), o1.end(), [&](int64_t x, int64_t y) { return t1[x].srcs.size() > t1[y].srcs.size(); });
-        std::stable_sort(o2.begin(), o2.end(), [&](int64_t x, int64_t y) { return t2[x].srcs.size() > t2[y].srcs.size(); });
+        // queue order = tree order (phase 1: by first V row), so that CTAs working on
+        // neighbouring tiles share source rows in L2; the dynamic queue balances the load
+        std::stable_sort(o1.begin(), o1.end(), [&](int64_t x, int64_t y) {
+            return (t1[x].srcs.empty() ? 0 : t1[x].srcs[0]) < (t1[y].srcs.empty() ? 0 : t1[y].srcs[0]);
+        });
         std::vector<BTile> tiles;
         std::vector<double> W;
         std::vector<int32_t> src, out;
@@ -3220,7 +3272,8 @@ int launch_res(Handle* h, HotArgs& a, cudaStream_t st) {
 // Cooperative launch of the streamed-tile kernel (2 CTAs per SM).
 int launch_bt(Handle* h, HotArgs& ha, cudaStream_t st) {
     DeviceHMat* D = h->dev;
-    const size_t smem = (size_t)(2 * kBKS * 16 + 2 * kBKS * kBCols + 8 * 4 * 32 * 2) * 8;
+    // ring: max over the column widths of KS (16 + KPB) doubles per slice (KPB 64: 32 x 80); red: 8 x 4 x 32 x 2
+    const size_t smem = (size_t)(kBStages * kBSlice + 8 * 4 * 32 * 2) * 8;
     CK(cudaFuncSetAttribute(bt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bt_kernel, 256, smem));
