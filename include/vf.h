@@ -267,6 +267,9 @@ typedef struct {
        layout): tiles and sum over tiles of their K (16 K weights each)        */
     int64_t tiles;
     int64_t tile_sources;
+    /* bytes one nrhs = 1 vf_matvec streams in the row layout of hot_kernel
+       (values, S, V row indices, 16-bit CSR offsets; 0 if that layout is off) */
+    int64_t k1_payload_bytes;
 } vf_info_t;
 
 int vf_info(vf_handle h, vf_info_t* out);

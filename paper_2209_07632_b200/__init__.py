@@ -73,7 +73,8 @@ class vf_info_t(ctypes.Structure):
                 ("p1_flops_per_col", ctypes.c_int64), ("p2_flops_per_col", ctypes.c_int64),
                 ("groups1", ctypes.c_int64), ("groups2", ctypes.c_int64), ("resident", ctypes.c_int64),
                 ("stream_payload_bytes", ctypes.c_int64), ("stream_meta_bytes", ctypes.c_int64),
-                ("stream_chunks", ctypes.c_int64), ("tiles", ctypes.c_int64), ("tile_sources", ctypes.c_int64)]
+                ("stream_chunks", ctypes.c_int64), ("tiles", ctypes.c_int64), ("tile_sources", ctypes.c_int64),
+                ("k1_payload_bytes", ctypes.c_int64)]
 
 
 _lib = None

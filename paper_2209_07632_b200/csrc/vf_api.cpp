@@ -22,7 +22,7 @@ int set_error(int code, const std::string& msg) {
 int64_t device_alg_bytes(const Handle* h);
 int64_t device_alg_flops(const Handle* h);
 int64_t device_active_rows(const Handle* h);
-void device_phase_info(const Handle* h, int64_t* out15);
+void device_phase_info(const Handle* h, int64_t* out16);
 }  // namespace vf
 
 using namespace vf;
@@ -332,14 +332,14 @@ int vf_info(vf_handle hh, vf_info_t* out) {
     out->visible_pairs = h->visible_pairs;
     out->build_seconds = h->build_seconds;
     out->device = h->dev ? h->device : -1;
-    int64_t ph[15];
+    int64_t ph[16];
     device_phase_info(h, ph);
     out->groups1 = ph[7]; out->groups2 = ph[8];
     out->t_rows = ph[0]; out->p1_bytes = ph[1]; out->p2_bytes = ph[2]; out->p1_src_rows = ph[3];
     out->p2_src_rows = ph[4]; out->p1_flops_per_col = ph[5]; out->p2_flops_per_col = ph[6];
     out->resident = ph[9];
     out->stream_payload_bytes = ph[10]; out->stream_meta_bytes = ph[11]; out->stream_chunks = ph[12];
-    out->tiles = ph[13]; out->tile_sources = ph[14];
+    out->tiles = ph[13]; out->tile_sources = ph[14]; out->k1_payload_bytes = ph[15];
     return VF_OK;
 }
 

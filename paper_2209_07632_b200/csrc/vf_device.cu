@@ -395,11 +395,26 @@ template <bool L1X> struct XV4<float, L1X> {
 #ifndef VF_MV_L1
 #define VF_MV_L1 1      // matvec: gather x through L1 (X read-only; T rows not cached before the barrier)
 #endif
+__device__ __forceinline__ uint2 ld_stream_u2(const uint2* p) {
+#if VF_K1_NA
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;\n"
+                 : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(l2_evict_first()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+// idx16 / seg_base (optional): CSR segments as 16-bit column offsets from a
+// per-segment base (the matvec row layout of upload_impl), 8 B per 4 terms
+// instead of 16 B
 template <typename T, bool L1X>
 __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int64_t s0, int64_t s1,
                                                const T* __restrict__ vals, const int32_t* __restrict__ idx,
                                                const T* xt, int lane, int64_t nx,
-                                               const int32_t* tready = nullptr, const int32_t* seg_blk = nullptr) {
+                                               const int32_t* tready = nullptr, const int32_t* seg_blk = nullptr,
+                                               const uint16_t* __restrict__ idx16 = nullptr,
+                                               const int32_t* __restrict__ seg_base = nullptr) {
     // chunks of 4 terms in flight per lane: FP32 chunks carry 2/3 of the bytes
     // of FP64 ones, so two are in flight there (VF_K1_CH_F32)
     constexpr int CH = sizeof(T) == 4 ? VF_K1_CH_F32 : VF_K1_CH;
@@ -408,7 +423,11 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
     for (int64_t sb = s0; sb < s1; sb += 32) {
         const int ns = (int)(s1 - sb < 32 ? s1 - sb : 32);
         Seg my{0, 0, 0, 0};
-        if (lane < ns) my = segs[sb + lane];
+        int32_t my_base = 0;
+        if (lane < ns) {
+            my = segs[sb + lane];
+            if (idx16) my_base = seg_base[sb + lane];
+        }
         if (tready && lane < ns) {                   // barrier-free matvec: this lane's U run needs block b's T rows
             const int32_t b = __ldg(seg_blk + sb + lane);
             if (b >= 0) {
@@ -446,12 +465,18 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
                 const int g_len = __shfl_sync(FULL, my.len, g);
                 const int g_kind = __shfl_sync(FULL, my.kind, g);
                 const int g_excl = __shfl_sync(FULL, excl, g);
+                const int g_base = idx16 ? __shfl_sync(FULL, my_base, g) : 0;
                 if (cc < total) {
                     const int e = (cc - g_excl) * 4;
                     V4<T>::ld(vals + g_off + e, w[c]);
                     vx[c] = VF_XVEC && !g_kind && e + 3 < g_len && ((g_src + e) & (16 / sizeof(T) - 1)) == 0;
                     l1[c] = L1X && (g_kind || g_src < nx);
-                    if (g_kind) {
+                    if (g_kind && idx16) {
+                        const uint2 q = ld_stream_u2(reinterpret_cast<const uint2*>(idx16 + g_src + e));
+                        xr[c][0] = g_base + (int32_t)(q.x & 0xffffu); xr[c][1] = g_base + (int32_t)(q.x >> 16);
+                        xr[c][2] = g_base + (int32_t)(q.y & 0xffffu); xr[c][3] = g_base + (int32_t)(q.y >> 16);
+                        vx[c] = false;
+                    } else if (g_kind) {
                         const int4 q = ld_stream_i4(reinterpret_cast<const int4*>(idx + g_src + e));
                         xr[c][0] = q.x; xr[c][1] = q.y; xr[c][2] = q.z; xr[c][3] = q.w;
                         // sorted CSR columns often run consecutively (tree order keeps
@@ -463,7 +488,7 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
                     }
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
-                        if (e + u >= g_len) { w[c][u] = T(0); xr[c][u] = g_kind ? 0 : (int32_t)g_src; }
+                        if (e + u >= g_len) { w[c][u] = T(0); xr[c][u] = g_kind ? g_base : (int32_t)g_src; }
                 } else {
                     vx[c] = false;
                     l1[c] = false;
@@ -584,6 +609,11 @@ struct HotArgs {
     const int32_t* g1_blk;
     int32_t* qctr;
     const int32_t* p2_order;
+    // nrhs = 1 matvec rows with 16-bit CSR offsets (optional; upload_impl)
+    const Seg* segs16;
+    const int64_t* p2_segptr16;
+    const uint16_t* idx16;
+    const int32_t* seg_base16;
     unsigned long long* trace;    // optional: [iter][event][cta] globaltimer (VF_TRACE_FILE)
     int trace_iters;
 };
@@ -743,8 +773,11 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
             const int64_t r = a.p2_order[nxt];
             int fut = 0;
             if (lane == 0) fut = atomicAdd(a.qctr, 1);
-            const T acc = row_accumulate_k1<T, VF_MV_L1 != 0>(a.segs, a.p2_segptr[r], a.p2_segptr[r + 1], vals, a.idx,
-                                                              xc, lane, a.N, a.tready, a.seg_blk);
+            const T acc = a.idx16 ? row_accumulate_k1<T, VF_MV_L1 != 0>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
+                                                                         vals, a.idx, xc, lane, a.N, nullptr, nullptr,
+                                                                         a.idx16, a.seg_base16)
+                                  : row_accumulate_k1<T, VF_MV_L1 != 0>(a.segs, a.p2_segptr[r], a.p2_segptr[r + 1],
+                                                                         vals, a.idx, xc, lane, a.N, a.tready, a.seg_blk);
             if (lane == 0) static_cast<T*>(a.Y)[a.p2_rows[r]] = acc;
             nxt = __shfl_sync(0xffffffffu, fut, 0);
         }
@@ -1989,6 +2022,12 @@ struct DeviceHMat {
     size_t slot_cap = 0;
     // chunk-stream layout of the nrhs = 1 apply (vf_stream.cu)
     stream::DevLayout sl;
+    // nrhs = 1 matvec rows with 16-bit CSR column offsets (row_accumulate_k1)
+    Seg* segs16 = nullptr;
+    int64_t* p2_segptr16 = nullptr;
+    uint16_t* idx16 = nullptr;
+    int32_t* seg_base16 = nullptr;
+    int64_t k1_payload = 0;          // bytes one nrhs = 1 apply streams: values + V indices + u16 CSR offsets
     // streamed-tile layout of wide batches on a large F-hat (bt_kernel, FP64)
     bool bt_ok = false;
     BTile* bt_tiles = nullptr;
@@ -2831,6 +2870,57 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             D->res_scap = (int)std::max<int64_t>(smax, 4);
         }
     }
+    if (!h->sharded && !getenv("VF_K1_U32")) {
+        // phase-2 rows for the nrhs = 1 matvec with the merged CSR row cut into runs
+        // whose column span < 2^16: 16-bit offsets from a per-run base
+        std::vector<Seg> s16;
+        std::vector<int64_t> ptr16(1, 0);
+        std::vector<uint16_t> i16;
+        std::vector<int32_t> base16;
+        int64_t pay = D->p1_bytes;                              // phase 1 unchanged (values, S, V indices)
+        bool ok16 = true;
+        const int64_t span16 = getenv("VF_U16_SPAN") ? std::min(65536, std::max(2, atoi(getenv("VF_U16_SPAN")))) : 65536;
+        for (int64_t r = 0; r < (int64_t)p2_rows.size() && ok16; ++r) {
+            for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1] && ok16; ++q) {
+                const Seg& sg = segs[q];
+                if (sg.kind == 0) {
+                    s16.push_back(sg); base16.push_back(0);
+                    pay += (int64_t)sizeof(T) * sg.len;
+                    continue;
+                }
+                constexpr int32_t A = 16 / (int32_t)sizeof(T);    // runs start on 16-B value boundaries
+                for (int32_t e = 0; e < sg.len;) {
+                    const int32_t base = idx[sg.src + e];
+                    int32_t f = e + 1;
+                    while (f < sg.len && idx[sg.src + f] - base < span16) ++f;
+                    if (f < sg.len && (f - e) % A) {
+                        if (f - e > A) f = e + (f - e) / A * A;
+                        else { ok16 = false; break; }                // a gap >= 2^16 inside one 16-B unit
+                    }
+                    while (i16.size() % 4) i16.push_back(0);       // 8-B aligned run start (uint2 loads)
+                    Seg x{sg.val_off + e, (int64_t)i16.size(), f - e, 1};
+                    for (int32_t u = e; u < f; ++u) i16.push_back((uint16_t)(idx[sg.src + u] - base));
+                    s16.push_back(x); base16.push_back(base);
+                    pay += (int64_t)(sizeof(T) + 2) * (f - e);
+                    e = f;
+                }
+            }
+            ptr16.push_back((int64_t)s16.size());
+        }
+        // value offsets of split runs stay 16-B aligned only if the run starts on
+        // an even term: the kernel's quad loads need it, so fall back otherwise
+        bool aligned = ok16 && (int64_t)ptr16.size() == (int64_t)p2_rows.size() + 1;
+        for (const Seg& x : s16) aligned = aligned && ((x.val_off * (int64_t)sizeof(T)) % 16 == 0);
+        for (int pad = 0; pad < 8; ++pad) i16.push_back(0);
+        if (aligned && !s16.empty()) {
+            if ((rc = up((void**)&D->segs16, s16.data(), s16.size() * sizeof(Seg))) ||
+                (rc = up((void**)&D->p2_segptr16, ptr16.data(), ptr16.size() * 8)) ||
+                (rc = up((void**)&D->idx16, i16.data(), i16.size() * 2)) ||
+                (rc = up((void**)&D->seg_base16, base16.data(), base16.size() * 4)))
+                return rc;
+            D->k1_payload = pay;
+        }
+    }
     if (!D->res_ok && !h->sharded && sizeof(T) == 8 && !getenv("VF_NO_TILES") && (D->n_g1 + D->n_p2) > 0) {
         // streamed-tile layout (bt_kernel): phase-1 tiles = the row groups of T
         // rows (one SVD block, shared V rows), phase-2 tiles = 16 consecutive
@@ -3508,6 +3598,7 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
         if (kpn == 1 && !getenv("VF_MV_STATIC") && !getenv("VF_MV_FLAGS")) {
             CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
             a.qctr = D->tready + D->n_svd; a.p2_order = D->p2_order;
+            if (D->idx16) { a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16; }
         }
         if (kpn == 1 && getenv("VF_MV_FLAGS") && !getenv("VF_MV_BARRIER")) {
             CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
@@ -3716,7 +3807,8 @@ void device_free(Handle* h) {
     for (auto& e : D->evpool) if (e) cudaEventDestroy(e);
     for (auto& kv : D->sched) { cudaFree(kv.second.ptr); cudaFree(kv.second.items); }
     stream::free_dev(&D->sl);
-    void* bps[] = {D->bt_tiles, D->bt_W, D->bt_src, D->bt_out, D->bt_ctr};
+    void* bps[] = {D->bt_tiles, D->bt_W, D->bt_src, D->bt_out, D->bt_ctr, D->segs16, D->p2_segptr16, D->idx16,
+                   D->seg_base16};
     for (void* p : bps) if (p) cudaFree(p);
     delete D;
     h->dev = nullptr;
@@ -3980,7 +4072,8 @@ int64_t device_alg_flops(const Handle* h) { return h->dev ? h->dev->alg_flops_pe
 int64_t device_active_rows(const Handle* h) { return h->dev ? h->dev->n_p2 : -1; }
 void device_phase_info(const Handle* h, int64_t* out9) {
     const DeviceHMat* D = h->dev;
-    if (!D) { for (int i = 0; i < 15; ++i) out9[i] = 0; return; }
+    if (!D) { for (int i = 0; i < 16; ++i) out9[i] = 0; return; }
+    out9[15] = D->k1_payload;
     out9[13] = D->bt_ok ? (int64_t)D->bt_n1 + D->bt_n2 : 0;
     out9[14] = D->bt_ok ? D->bt_cells : 0;
     out9[9] = D->res_ok ? 1 : 0;

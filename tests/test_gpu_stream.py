@@ -162,3 +162,41 @@ def test_stream_column_split_bitwise(meshes, tmp_path):
         y = empty(S.N)
         M.matvec(dev(X[:, c:c + 1]), y)
         assert torch.equal(y[:, 0], Y[:, c])
+
+
+_ROWK1 = r"""
+import json, os, sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import oracle, oracle.hmatrix as hm, paper_2209_07632_b200 as vf, scenegen as sg
+out = {{}}
+for name, (V, F) in (("cap", sg.cfg1_mesh()), ("rough", sg.rough_small_mesh(24, amp=0.05))):
+    S = oracle.Scene(V, F)
+    H = hm.compress(S.x, S.F_dense(), 1e-6, min_size=2048)
+    p = "/tmp/vf_rowk1_%s.hvfm" % name
+    hm.write_hvfm(H, p)
+    M = vf.ViewFactorMatrix.load(p, device=0)
+    X = sg.random_rhs(S.N, 1, seed=5)
+    Y = torch.empty((1, S.N), dtype=torch.float64, device="cuda").T
+    M.matvec(torch.from_numpy(np.ascontiguousarray(X.T)).cuda().T, Y)
+    R = hm.hmatvec(H, X)
+    i = M.refresh()
+    out[name] = dict(err=float(np.linalg.norm(Y.cpu().numpy() - R) / np.linalg.norm(R)),
+                     k1=int(i["k1_payload_bytes"]), stream=int(i["stream_chunks"]))
+print(json.dumps(out))
+"""
+
+
+@pytest.mark.parametrize("env", [{"VF_NO_STREAM": "1"}, {"VF_NO_STREAM": "1", "VF_U16_SPAN": "7"},
+                                 {"VF_NO_STREAM": "1", "VF_K1_U32": "1"}])
+def test_row_kernel_k1_u16_offsets(env):
+    """The row-segment nrhs = 1 kernel (hot_kernel<T,1,1>, the stream layout
+    off): 16-bit CSR offsets from per-run bases (forced short spans cut every
+    merged CSR row into many runs), or 32-bit columns (VF_K1_U32): <= 1e-12
+    vs the oracle's Alg. 5 on the same blocks."""
+    r = subprocess.run([sys.executable, "-c", _ROWK1.format(root=ROOT)], env=dict(os.environ, **env),
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    for name, d in out.items():
+        assert d["err"] <= 1e-12 and d["stream"] == 0, (name, d)
+        assert (d["k1"] > 0) == ("VF_K1_U32" not in env), (name, d)
