@@ -2042,6 +2042,19 @@ struct DeviceHMat {
 
 namespace {
 
+// Which nrhs = 1 kernel vf_matvec uses: the row-segment hot_kernel<T,1,1>
+// ("rows", default: measured faster on configs[2]) or the
+// bulk-copy chunk stream ("stream").  VF_K1_KERNEL overrides; read at upload
+// (the stream layout is only built when selected).
+#ifndef VF_K1_DEFAULT_STREAM
+#define VF_K1_DEFAULT_STREAM 0
+#endif
+bool k1_use_stream() {
+    const char* e = getenv("VF_K1_KERNEL");
+    if (e) return std::strcmp(e, "stream") == 0;
+    return VF_K1_DEFAULT_STREAM != 0;
+}
+
 // ---- chunk-stream layout of the nrhs = 1 apply (vf_stream.h / vf_stream.cu).
 // Phase-1 items: (row group g of <= 16 consecutive T rows of one SVD block,
 // part of its V rows); chunk = header, [int32 X rows if J_b is not a
@@ -3010,7 +3023,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         D->bt_cells = wn / 16;
         D->bt_ok = true;
     }
-    if (!h->sharded && !getenv("VF_NO_STREAM")) {
+    if (!h->sharded && !getenv("VF_NO_STREAM") && k1_use_stream()) {
         // the nrhs = 1 chunk stream (an F-hat copy in the layout of vf_stream.cu)
         stream::HostLayout SL;
         build_stream<T>(N, vals, idx, segs, p2_segptr, p2_rows, g1v, gsegv, gvov, grow1v, p1_scale, SL);
@@ -3567,6 +3580,34 @@ int check_k(int nrhs) {
     return VF_OK;
 }
 
+// One nrhs = 1 apply in tree order on the replicated (unsharded) operator:
+// Y = F-hat XT[0:N] with T rows written into XT[N:] -- the chunk-stream kernel
+// if its layout was built, else the row-segment kernel with the LPT row queue
+// and (if built) 16-bit CSR offsets.
+template <typename T>
+int apply_k1(Handle* h, void* XT, void* Y, cudaStream_t st) {
+    DeviceHMat* D = h->dev;
+    int rc;
+    if (D->sl.ok) {
+        int grid = 0;
+        {
+            Timer tm(h, st, 2);
+            if ((rc = stream::matvec_k1(D->sl, D->dtype, XT, Y, st, &grid))) return rc;
+        }
+        h->launches_total++;
+        D->last_grid = grid;
+        return VF_OK;
+    }
+    HotArgs a = hot_args(D, 1, 1);
+    a.xt0 = XT;
+    a.Y = Y;
+    CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
+    a.qctr = D->tready + D->n_svd;
+    a.p2_order = D->p2_order;
+    if (D->idx16) { a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16; }
+    return launch_hot<T, M_MATVEC>(h, a, st);
+}
+
 template <typename T>
 int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     DeviceHMat* D = h->dev;
@@ -3607,14 +3648,8 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
         }
         const bool rows = D->world > 1 || h->comm;
         if (rows) CK(cudaMemsetAsync(D->Yp, 0, (size_t)D->N * kpn * sizeof(T), st));   // rows of other ranks: 0 ...
-        if (kpn == 1 && D->sl.ok && !rows) {
-            int grid = 0;
-            {
-                Timer tm(h, st, 2);
-                if ((rc = stream::matvec_k1(D->sl, D->dtype, D->xt[0], D->Yp, st, &grid))) return rc;   // XT = [Xp ; T]
-            }
-            h->launches_total++;
-            D->last_grid = grid;
+        if (kpn == 1 && !rows && !getenv("VF_MV_STATIC") && !getenv("VF_MV_FLAGS")) {
+            if ((rc = apply_k1<T>(h, D->xt[0], D->Yp, st))) return rc;              // XT = [Xp ; T]
         } else if ((rc = launch_hot<T, M_MATVEC>(h, a, st))) {
             return rc;
         }
@@ -3864,7 +3899,7 @@ int ts_create_t(Handle* h, int ns, int M, double depth, double ratio, double k_t
         (rc = mk(&S->Qir, tot * w)) || (rc = mk(&S->Qabs, tot * w)) || (rc = mk(&S->Qrad, tot * w)) ||
         (rc = mk(&S->Qd, tot * w)) || (rc = mk(&S->prof, (M + 1) * tot * w)) || (rc = mk((void**)&S->z, (M + 1) * 8)))
         return rc;
-    const bool two = ns == 1 && D->sl.ok && !h->comm && D->world == 1;
+    const bool two = ns == 1 && !h->comm && D->world == 1;
     if (two) {
         for (int q = 0; q < 2; ++q)
             if ((rc = mk(&S->XT[q], (N + D->NT) * w)) || (rc = mk(&S->Y[q], N * w))) return rc;
@@ -3909,12 +3944,9 @@ int ts_step_t(TState* S, const void* Qdir, double dt, void* Tsurf) {
                                          (T*)S->Qd, (T*)S->XT[0], two ? (T*)S->XT[1] : nullptr);
     h->launches_total++;
     if (two) {                               // one F-hat stream per column (nrhs = 1 kernel)
-        for (int q = 0; q < 2; ++q) {
-            int grid = 0;
-            Timer tm(h, st, 2);
-            if ((rc = stream::matvec_k1(D->sl, D->dtype, S->XT[q], S->Y[q], st, &grid))) return rc;
-            h->launches_total++;
-        }
+        if ((rc = ensure_scratch(D, 1, st))) return rc;
+        for (int q = 0; q < 2; ++q)
+            if ((rc = apply_k1<T>(h, S->XT[q], S->Y[q], st))) return rc;
     } else {
         if ((rc = ensure_scratch(D, S->kp, st))) return rc;
         HotArgs a = hot_args(D, S->kp, 2 * S->ns);

@@ -4,7 +4,9 @@ phase-1 parts) against the FP64 oracle's Alg. 5 on the same blocks, and
 against the row-segment kernel it replaces.  Forced layouts (env, read at
 upload): VF_P1_PART (V rows per phase-1 item -> multi-part groups combined by
 the last part), VF_U16_SPAN (span of a 16-bit CSR run -> many runs per row),
-VF_NO_STREAM (no stream layout: the round-1 hot_kernel<T,1,1>)."""
+VF_NO_STREAM (no stream layout: the round-1 hot_kernel<T,1,1>).  The stream
+kernel is opt-in (VF_K1_KERNEL=stream, read at upload): the
+tests of it set that variable."""
 import json
 import os
 import subprocess
@@ -22,6 +24,12 @@ pytestmark = pytest.mark.gpu
 torch = pytest.importorskip("torch")
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(autouse=True)
+def _stream_kernel(request, monkeypatch):
+    if "row_kernel" not in request.node.name:
+        monkeypatch.setenv("VF_K1_KERNEL", "stream")
 
 
 def dev(a, dtype=np.float64):
@@ -135,7 +143,8 @@ def test_stream_forced_parts_and_runs(env):
     combined in part order by the last part) and CSR rows cut into many 16-bit
     runs: still <= 1e-12 vs the oracle's Alg. 5, and bitwise repeatable (the
     part counters reset themselves between launches)."""
-    r = subprocess.run([sys.executable, "-c", _FORCED.format(root=ROOT)], env=dict(os.environ, **env),
+    r = subprocess.run([sys.executable, "-c", _FORCED.format(root=ROOT)],
+                       env=dict(os.environ, VF_K1_KERNEL="stream", **env),
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     out = json.loads(r.stdout.strip().splitlines()[-1])
@@ -193,7 +202,8 @@ def test_row_kernel_k1_u16_offsets(env):
     off): 16-bit CSR offsets from per-run bases (forced short spans cut every
     merged CSR row into many runs), or 32-bit columns (VF_K1_U32): <= 1e-12
     vs the oracle's Alg. 5 on the same blocks."""
-    r = subprocess.run([sys.executable, "-c", _ROWK1.format(root=ROOT)], env=dict(os.environ, **env),
+    r = subprocess.run([sys.executable, "-c", _ROWK1.format(root=ROOT)],
+                       env={k: v for k, v in dict(os.environ, **env).items() if k != "VF_K1_KERNEL"},
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     out = json.loads(r.stdout.strip().splitlines()[-1])
