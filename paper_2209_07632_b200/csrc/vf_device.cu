@@ -1409,7 +1409,18 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                 const int cw = warp % nch, pw = warp / nch;
                 double* Wsm = bsm;                                 // [kBStages][KS][16]
                 double* Xsm = bsm + kBStages * KS * 16;            // [kBStages][KS][KPB] (fits kBStages x kBSlice)
-                auto stage = [&](int sl, int slot) {
+                const int per = KPB >> 1;                          // 16-B copies per staged row (<= 4 rows per thread)
+                // source rows of a slice, fetched into registers one slice before they are staged
+                // (the XT copies' addresses depend on them: no global-load latency in the staging)
+                auto load_idx = [&](int sl, int32_t* rg) {
+                    const int j0 = sl * KS;
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const int op = t + 256 * m, j = op / per;
+                        rg[m] = (op < KS * per && sl < nsl && j0 + j < B.K) ? __ldg(S + j0 + j) : -1;
+                    }
+                };
+                auto stage = [&](int sl, int slot, const int32_t* rg) {
                     const int j0 = sl * KS, n = min(KS, B.K - j0);
                     double* wd = Wsm + slot * KS * 16;
                     double* xd = Xsm + slot * KS * KPB;
@@ -1417,23 +1428,28 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                         const int j = op >> 3;
                         cpa<16>(wd + op * 2, Wt + (int64_t)j0 * 16 + op * 2, j < n ? 16 : 0);
                     }
-                    const int per = KPB >> 1;                      // 16-B copies per staged row
-                    for (int op = t; op < KS * per; op += 256) {
-                        const int j = op / per, part = op - j * per;
-                        const int c = part * 2;
-                        const bool ok = j < n;
-                        const int64_t row = ok ? S[j0 + j] : 0;
-                        cpa<16>(xd + j * KPB + (c ^ (4 * (j & 3))), a.XT + row * a.kp + cb + c, ok ? 16 : 0);
+#pragma unroll
+                    for (int m = 0; m < 4; ++m) {
+                        const int op = t + 256 * m;
+                        if (op < KS * per) {
+                            const int j = op / per, c = (op - j * per) * 2;
+                            const bool ok = rg[m] >= 0;
+                            cpa<16>(xd + j * KPB + (c ^ (4 * (j & 3))), a.XT + (int64_t)(ok ? rg[m] : 0) * a.kp + cb + c,
+                                    ok ? 16 : 0);
+                        }
                     }
                 };
                 double dacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+                int32_t rg[4];
 #pragma unroll
                 for (int p = 0; p < kBStages - 1; ++p) {
-                    if (p < nsl) stage(p, p);
+                    if (p < nsl) { load_idx(p, rg); stage(p, p, rg); }
                     cpa_commit();
                 }
+                load_idx(kBStages - 1, rg);
                 for (int sl = 0; sl < nsl; ++sl) {
-                    if (sl + kBStages - 1 < nsl) stage(sl + kBStages - 1, (sl + kBStages - 1) % kBStages);
+                    if (sl + kBStages - 1 < nsl) stage(sl + kBStages - 1, (sl + kBStages - 1) % kBStages, rg);
+                    load_idx(sl + kBStages, rg);                   // in flight during this slice's DMMA
                     cpa_commit();
                     cpa_wait<kBStages - 1>();
                     __syncthreads();
