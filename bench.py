@@ -619,9 +619,15 @@ def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
     stream = info.get("stream_chunks", 0) > 0 and not rows_mode
 
     def alg_bytes(kp):
-        # F-hat payload: the chunk stream's values + 16-bit CSR offsets + phase-1 row lists
-        # for nrhs = 1 (stream_k1_kernel), else values + 32-bit indices of the row layout
-        fh = info["stream_payload_bytes"] if (stream and kp == 1) else info["p1_bytes"] + info["p2_bytes"]
+        # F-hat payload one apply streams: for nrhs = 1 the bytes of the layout the kernel
+        # reads (chunk stream: values + 16-bit CSR offsets + phase-1 row lists; row layout:
+        # values + S + V row indices + 16-bit CSR offsets), else values + 32-bit indices
+        if kp == 1 and stream:
+            fh = info["stream_payload_bytes"]
+        elif kp == 1 and info.get("k1_payload_bytes", 0) > 0 and not rows_mode:
+            fh = info["k1_payload_bytes"]
+        else:
+            fh = info["p1_bytes"] + info["p2_bytes"]
         return (fh + (info["p1_src_rows"] + info["p2_src_rows"]) * kp * w
                 + info["t_rows"] * kp * w + info["active_rows"] * kp * w * solve_rows)
     avg = tm["ms_hot"] / max(tm["l_hot"], 1)
@@ -654,7 +660,10 @@ def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
     tn = "double" if dt == "f64" else "float"
     if max(chunks) <= 2:
         kern = (f"stream_k1_kernel<{tn}> (bulk-copy chunk stream: phase 1 T = S V^T x, warp-granular grid barrier, "
-                "phase 2 row-owner accumulate)" if stream and max(chunks) == 1 else f"hot_kernel<{tn},1,VEC,M_MATVEC>")
+                "phase 2 row-owner accumulate)" if stream and max(chunks) == 1 else
+                f"hot_kernel<{tn},1,1,M_MATVEC> (phase 1 T = S V^T x, grid barrier, phase 2 row-owner accumulate with "
+                "an LPT row queue; F-hat loads L1::no_allocate + L2 evict-first"
+                + (", 16-bit CSR offsets)" if info.get("k1_payload_bytes", 0) > 0 else ")"))
     elif info.get("tiles", 0) > 0 and dt == "f64":
         kern = ("bt_kernel (streamed 16-row tiles, [K][16] weights x staged XT rows on FP64 tensor cores, DMMA "
                 "m8n8k4; phase 1 T tiles, grid barrier, phase 2 row tiles)")

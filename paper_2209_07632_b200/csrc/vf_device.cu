@@ -2650,6 +2650,51 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         return VF_OK;
     };
     int rc;
+    // phase-2 rows for the nrhs = 1 matvec with each merged CSR row cut into runs
+    // whose column span < 2^16: 16-bit offsets from a per-run base.  A run that
+    // does not start on a 16-B value boundary gets an aligned copy of its values
+    // appended to vals (the kernel's quad loads need the alignment).
+    std::vector<Seg> s16;
+    std::vector<int64_t> ptr16(1, 0);
+    std::vector<uint16_t> i16;
+    std::vector<int32_t> base16;
+    int64_t pay16 = 0;
+    const bool use16 = !h->sharded && !getenv("VF_K1_U32");
+    if (use16) {
+        const int64_t span16 = getenv("VF_U16_SPAN") ? std::min(65536, std::max(2, atoi(getenv("VF_U16_SPAN")))) : 65536;
+        pay16 = D->p1_bytes;                                   // phase 1 unchanged (values, S, V indices)
+        for (int64_t r = 0; r < (int64_t)p2_rows.size(); ++r) {
+            for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1]; ++q) {
+                const Seg sg = segs[q];
+                if (sg.kind == 0) {
+                    s16.push_back(sg); base16.push_back(0);
+                    pay16 += (int64_t)sizeof(T) * sg.len;
+                    continue;
+                }
+                for (int32_t e = 0; e < sg.len;) {
+                    const int32_t base = idx[sg.src + e];
+                    int32_t f = e + 1;
+                    while (f < sg.len && idx[sg.src + f] - base < span16) ++f;
+                    int64_t voff = sg.val_off + e;
+                    if ((voff * (int64_t)sizeof(T)) % 16) {           // realign: copy this run's values
+                        std::vector<T> cp(vals.begin() + voff, vals.begin() + voff + (f - e));
+                        voff = (int64_t)vals.size();
+                        for (T v : cp) vals.push_back(v);
+                        while ((vals.size() * sizeof(T)) % 16) vals.push_back(T(0));
+                    }
+                    while (i16.size() % 4) i16.push_back(0);       // 8-B aligned run start (uint2 loads)
+                    s16.push_back(Seg{voff, (int64_t)i16.size(), f - e, 1});
+                    for (int32_t u = e; u < f; ++u) i16.push_back((uint16_t)(idx[sg.src + u] - base));
+                    base16.push_back(base);
+                    pay16 += (int64_t)(sizeof(T) + 2) * (f - e);
+                    e = f;
+                }
+            }
+            ptr16.push_back((int64_t)s16.size());
+        }
+        for (int pad = 0; pad < 8; ++pad) i16.push_back(0);
+        for (int pad = 0; pad < 8; ++pad) vals.push_back(T(0));
+    }
     if ((rc = up(&D->vals, vals.data(), vals.size() * sizeof(T)))) return rc;
     if ((rc = up((void**)&D->idx, idx.data(), idx.size() * 4))) return rc;
     if ((rc = up((void**)&D->segs, segs.data(), segs.size() * sizeof(Seg)))) return rc;
@@ -2899,56 +2944,15 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             D->res_scap = (int)std::max<int64_t>(smax, 4);
         }
     }
-    if (!h->sharded && !getenv("VF_K1_U32")) {
-        // phase-2 rows for the nrhs = 1 matvec with the merged CSR row cut into runs
-        // whose column span < 2^16: 16-bit offsets from a per-run base
-        std::vector<Seg> s16;
-        std::vector<int64_t> ptr16(1, 0);
-        std::vector<uint16_t> i16;
-        std::vector<int32_t> base16;
-        int64_t pay = D->p1_bytes;                              // phase 1 unchanged (values, S, V indices)
-        bool ok16 = true;
-        const int64_t span16 = getenv("VF_U16_SPAN") ? std::min(65536, std::max(2, atoi(getenv("VF_U16_SPAN")))) : 65536;
-        for (int64_t r = 0; r < (int64_t)p2_rows.size() && ok16; ++r) {
-            for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1] && ok16; ++q) {
-                const Seg& sg = segs[q];
-                if (sg.kind == 0) {
-                    s16.push_back(sg); base16.push_back(0);
-                    pay += (int64_t)sizeof(T) * sg.len;
-                    continue;
-                }
-                constexpr int32_t A = 16 / (int32_t)sizeof(T);    // runs start on 16-B value boundaries
-                for (int32_t e = 0; e < sg.len;) {
-                    const int32_t base = idx[sg.src + e];
-                    int32_t f = e + 1;
-                    while (f < sg.len && idx[sg.src + f] - base < span16) ++f;
-                    if (f < sg.len && (f - e) % A) {
-                        if (f - e > A) f = e + (f - e) / A * A;
-                        else { ok16 = false; break; }                // a gap >= 2^16 inside one 16-B unit
-                    }
-                    while (i16.size() % 4) i16.push_back(0);       // 8-B aligned run start (uint2 loads)
-                    Seg x{sg.val_off + e, (int64_t)i16.size(), f - e, 1};
-                    for (int32_t u = e; u < f; ++u) i16.push_back((uint16_t)(idx[sg.src + u] - base));
-                    s16.push_back(x); base16.push_back(base);
-                    pay += (int64_t)(sizeof(T) + 2) * (f - e);
-                    e = f;
-                }
-            }
-            ptr16.push_back((int64_t)s16.size());
-        }
-        // value offsets of split runs stay 16-B aligned only if the run starts on
-        // an even term: the kernel's quad loads need it, so fall back otherwise
-        bool aligned = ok16 && (int64_t)ptr16.size() == (int64_t)p2_rows.size() + 1;
-        for (const Seg& x : s16) aligned = aligned && ((x.val_off * (int64_t)sizeof(T)) % 16 == 0);
-        for (int pad = 0; pad < 8; ++pad) i16.push_back(0);
-        if (aligned && !s16.empty()) {
-            if ((rc = up((void**)&D->segs16, s16.data(), s16.size() * sizeof(Seg))) ||
-                (rc = up((void**)&D->p2_segptr16, ptr16.data(), ptr16.size() * 8)) ||
-                (rc = up((void**)&D->idx16, i16.data(), i16.size() * 2)) ||
-                (rc = up((void**)&D->seg_base16, base16.data(), base16.size() * 4)))
-                return rc;
-            D->k1_payload = pay;
-        }
+    if (use16 && !s16.empty()) {
+        if ((rc = up((void**)&D->segs16, s16.data(), s16.size() * sizeof(Seg))) ||
+            (rc = up((void**)&D->p2_segptr16, ptr16.data(), ptr16.size() * 8)) ||
+            (rc = up((void**)&D->idx16, i16.data(), i16.size() * 2)) ||
+            (rc = up((void**)&D->seg_base16, base16.data(), base16.size() * 4)))
+            return rc;
+        D->k1_payload = pay16;
+        std::vector<Seg>().swap(s16);
+        std::vector<uint16_t>().swap(i16);
     }
     if (!D->res_ok && !h->sharded && sizeof(T) == 8 && !getenv("VF_NO_TILES") && (D->n_g1 + D->n_p2) > 0) {
         // streamed-tile layout (bt_kernel): phase-1 tiles = the row groups of T
