@@ -1510,6 +1510,200 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
     }
 }
 
+// ---- FP32 streamed tiles on the 5th-generation tensor cores (tcgen05,
+// kind::tf32, accumulator in TMEM) with 3xTF32 splitting, so the FP32 result
+// keeps single-precision accuracy (BASELINE north_star: "TF32/FP32 paths where
+// the stated tolerance allows"; parity <= 1e-5).  Same tiles as bt_kernel.
+// The MMA is D (columns x tile rows) += X^T (columns x sources) W (sources x
+// rows): M = 64 or 128 columns, N = 16 rows, K = 8 sources per instruction;
+// both operands MN-major in SWIZZLE_NONE core matrices (8 source rows x 16 B):
+// element (mn, k) at (mn/4) SBO + (k/8) 128 + (k%8) 16 + (mn%4) 4 bytes.
+// X slices are staged raw with cp.async, split in shared memory into
+// hi = tf32(x) and lo = x - hi; W arrives pre-split (two blobs).  Per K step
+// three MMAs: hi*hi, hi*lo, lo*hi.  One thread issues, tcgen05.commit signals
+// one mbarrier per ring slot (slot reuse) and one per tile (epilogue);
+// warps 0-3 read the 128 TMEM lanes (tcgen05.ld 32x32b.x16) and store.
+constexpr int kTS = 32;            // sources per slice (4 K steps)
+constexpr int kTStages = 3;
+struct TArgs {
+    const BTile* tiles;
+    int32_t n1, n2;
+    const float* Whi;
+    const float* Wlo;
+    const int32_t* src;
+    const int32_t* outrow;
+    float* XT;
+    float* Y;
+    int64_t N;
+    int kp;
+    int32_t* ctr;
+    Ctl* ctl;
+};
+__device__ __forceinline__ unsigned tc_smem(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t tc_desc(unsigned addr, unsigned lbo, unsigned sbo) {
+    return (uint64_t)((addr >> 4) & 0x3fff) | ((uint64_t)((lbo >> 4) & 0x3fff) << 16) |
+           ((uint64_t)((sbo >> 4) & 0x3fff) << 32) | ((uint64_t)1 << 46);      // version 1, SWIZZLE_NONE
+}
+__device__ __forceinline__ void tc_mma(uint32_t tmem, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+    asm volatile("{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n"
+                 ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(tc_smem(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_wait(uint64_t* bar, unsigned parity) {
+    unsigned ok = 0;
+    unsigned long long spins = 0;
+    while (!ok) {
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                     : "=r"(ok) : "r"(tc_smem(bar)), "r"(parity) : "memory");
+        if (++spins > (1ull << 26)) __trap();
+    }
+}
+
+__global__ void __launch_bounds__(128, 2) bt_tc_kernel(TArgs a) {
+    extern __shared__ __align__(1024) unsigned char tsm[];
+    __shared__ uint32_t tmem_base;
+    __shared__ __align__(8) uint64_t bar_slot[kTStages];
+    __shared__ __align__(8) uint64_t bar_tile;
+    __shared__ int s_item;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(tc_smem(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (t == 0) {
+        for (int q = 0; q < kTStages; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc_smem(bar_slot + q)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc_smem(&bar_tile)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = tmem_base;
+    unsigned slot_uses[kTStages] = {0, 0, 0};   // completed MMA batches per slot (parity tracking)
+    unsigned tile_uses = 0;
+    for (int phase = 1; phase <= 2; ++phase) {
+        const int nt = phase == 1 ? a.n1 : a.n2, base = phase == 1 ? 0 : a.n1;
+        for (;;) {
+            __syncthreads();
+            if (t == 0) s_item = atomicAdd(a.ctr + phase - 1, 1);
+            __syncthreads();
+            const int it = s_item;
+            if (it >= nt) break;
+            const BTile B = a.tiles[base + it];
+            const float* Wh = a.Whi + B.w_off;
+            const float* Wl = a.Wlo + B.w_off;
+            const int32_t* S = a.src + B.s_off;
+            const int nsl = (B.K + kTS - 1) / kTS;
+            for (int cb = 0; cb < a.kp; cb += 128) {
+                const int MB = min(128, a.kp - cb);              // 64 or 128 columns (the MMA's M)
+                const unsigned sboA = (kTS / 8) * 128, sboB = (kTS / 8) * 128;
+                const size_t abytes = (size_t)MB * kTS * 4, bbytes = (size_t)16 * kTS * 4;
+                const size_t sbytes = 2 * abytes + 2 * bbytes;     // A_hi, A_lo, B_hi, B_lo
+                const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
+                                       ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(MB >> 4) << 24);
+                auto bufA = [&](int slot, int h) { return tsm + slot * sbytes + h * abytes; };
+                auto bufB = [&](int slot, int h) { return tsm + slot * sbytes + 2 * abytes + h * bbytes; };
+                auto stage = [&](int sl, int slot) {
+                    const int j0 = sl * kTS, n = min(kTS, B.K - j0);
+                    unsigned char* Alo = bufA(slot, 1);
+                    const int per = MB >> 2;                       // 16-B chunks per source row
+                    for (int op = t; op < kTS * per; op += 128) {
+                        const int j = op / per, c4 = op - j * per;
+                        const bool ok = j < n;
+                        const int64_t row = ok ? S[j0 + j] : 0;
+                        cpa<16>(Alo + c4 * sboA + (j >> 3) * 128 + (j & 7) * 16, a.XT + row * a.kp + cb + c4 * 4, ok ? 16 : 0);
+                    }
+                    for (int op = t; op < kTS * 4 * 2; op += 128) {  // W hi / lo: 4 chunks (16 rows) per source
+                        const int hsel = op / (kTS * 4), o2 = op - hsel * kTS * 4;
+                        const int j = o2 >> 2, r4 = o2 & 3;
+                        const bool ok = j < n;
+                        const float* w = hsel ? Wl : Wh;
+                        cpa<16>(bufB(slot, hsel) + r4 * sboB + (j >> 3) * 128 + (j & 7) * 16,
+                                w + (int64_t)(j0 + (ok ? j : 0)) * 16 + r4 * 4, ok ? 16 : 0);
+                    }
+                };
+                for (int p = 0; p < kTStages - 1; ++p) {
+                    if (p < nsl) {
+                        if (slot_uses[p] > 0) tc_wait(bar_slot + p, (slot_uses[p] - 1) & 1);   // MMAs done with it
+                        stage(p, p);
+                    }
+                    cpa_commit();
+                }
+                for (int sl = 0; sl < nsl; ++sl) {
+                    const int slot = sl % kTStages;
+                    if (sl + kTStages - 1 < nsl) {
+                        const int ns_ = (sl + kTStages - 1) % kTStages;
+                        if (slot_uses[ns_] > 0) tc_wait(bar_slot + ns_, (slot_uses[ns_] - 1) & 1);
+                        stage(sl + kTStages - 1, ns_);
+                    }
+                    cpa_commit();
+                    cpa_wait<kTStages - 1>();
+                    __syncthreads();
+                    {   // split the staged X slice: hi = tf32(x) into A_hi, lo = x - hi in place
+                        float* Alo = reinterpret_cast<float*>(bufA(slot, 1));
+                        float* Ahi = reinterpret_cast<float*>(bufA(slot, 0));
+                        for (int e = t; e < MB * kTS; e += 128) {
+                            const float x = Alo[e];
+                            uint32_t hb;
+                            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x));
+                            const float hi = __uint_as_float(hb);
+                            Ahi[e] = hi;
+                            Alo[e] = x - hi;
+                        }
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                    __syncthreads();
+                    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                    if (t == 0) {
+                        const unsigned ah = tc_smem(bufA(slot, 0)), al = tc_smem(bufA(slot, 1));
+                        const unsigned bh = tc_smem(bufB(slot, 0)), bl = tc_smem(bufB(slot, 1));
+                        for (int ks = 0; ks < kTS / 8; ++ks) {
+                            const unsigned ko = ks * 128;
+                            const uint32_t first = (sl == 0 && ks == 0) ? 0u : 1u;
+                            tc_mma(tmem, tc_desc(ah + ko, 128, sboA), tc_desc(bh + ko, 128, sboB), idesc, first);
+                            tc_mma(tmem, tc_desc(ah + ko, 128, sboA), tc_desc(bl + ko, 128, sboB), idesc, 1u);
+                            tc_mma(tmem, tc_desc(al + ko, 128, sboA), tc_desc(bh + ko, 128, sboB), idesc, 1u);
+                        }
+                        tc_commit(bar_slot + slot);
+                    }
+                    ++slot_uses[slot];
+                }
+                cpa_wait<0>();
+                if (t == 0) tc_commit(&bar_tile);
+                tc_wait(&bar_tile, tile_uses & 1);
+                ++tile_uses;
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                if (warp * 32 < MB) {
+                    uint32_t r[16];
+                    const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
+                    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                                   "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                                   "=r"(r[14]), "=r"(r[15])
+                                 : "r"(ta));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                    const int col = cb + warp * 32 + lane;
+                    for (int rr = 0; rr < B.nrows; ++rr) {
+                        const int64_t orow = a.outrow[B.out_off + rr];
+                        float* dst = phase == 1 ? a.XT + (a.N + orow) * a.kp + col : a.Y + orow * a.kp + col;
+                        *dst = __uint_as_float(r[rr]);
+                    }
+                }
+                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                __syncthreads();                                   // TMEM read before the next tile's first MMA
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            }
+        }
+        if (phase == 1) grid_sync(a.ctl, gridDim.x);
+    }
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(tmem));
+}
+
 // The persistent hot-path kernel (a2-a5).  MODE = M_MATVEC: phase 1, grid
 // barrier, phase 2 -> Y.  MODE = M_SOLVE: Jacobi iterations until every
 // column has r <= tol or `iters` is reached.  GROUPED selects the row-group
@@ -2048,6 +2242,7 @@ struct DeviceHMat {
     bool bt_ok = false;
     BTile* bt_tiles = nullptr;
     double* bt_W = nullptr;
+    float *bt_Whi = nullptr, *bt_Wlo = nullptr;   // FP32 handles: 3xTF32 split weights (bt_tc_kernel)
     int32_t *bt_src = nullptr, *bt_out = nullptr, *bt_ctr = nullptr;
     int32_t bt_n1 = 0, bt_n2 = 0;
     int64_t bt_cells = 0;
@@ -2954,7 +3149,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         std::vector<Seg>().swap(s16);
         std::vector<uint16_t>().swap(i16);
     }
-    if (!D->res_ok && !h->sharded && sizeof(T) == 8 && !getenv("VF_NO_TILES") && (D->n_g1 + D->n_p2) > 0) {
+    if (!D->res_ok && !h->sharded && !getenv("VF_NO_TILES") && (D->n_g1 + D->n_p2) > 0) {
         // streamed-tile layout (bt_kernel): phase-1 tiles = the row groups of T
         // rows (one SVD block, shared V rows), phase-2 tiles = 16 consecutive
         // active rows with the union of their sources; LPT order by K per phase
@@ -3032,8 +3227,28 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         if (W.empty()) W.resize(16, 0.0);
         if (src.empty()) src.resize(4, 0);
         if (out.empty()) out.resize(16, 0);
+        if (sizeof(T) == 8) {
+            if ((rc = up((void**)&D->bt_W, W.data(), W.size() * 8))) return rc;
+        } else {
+            // FP32 handles: the weights split for 3xTF32 (hi = tf32 round-to-nearest-away of
+            // the float value, what cvt.rna.tf32.f32 gives; lo = w - hi)
+            std::vector<float> hi(W.size()), lo(W.size());
+            for (size_t e = 0; e < W.size(); ++e) {
+                const float w = (float)W[e];
+                uint32_t u;
+                std::memcpy(&u, &w, 4);
+                u = (u + 0x1000u) & 0xffffe000u;
+                float hf;
+                std::memcpy(&hf, &u, 4);
+                if (!std::isfinite(hf)) hf = w;
+                hi[e] = hf;
+                lo[e] = w - hf;
+            }
+            std::vector<double>().swap(W);
+            if ((rc = up((void**)&D->bt_Whi, hi.data(), hi.size() * 4)) || (rc = up((void**)&D->bt_Wlo, lo.data(), lo.size() * 4)))
+                return rc;
+        }
         if ((rc = up((void**)&D->bt_tiles, tiles.data(), tiles.size() * sizeof(BTile))) ||
-            (rc = up((void**)&D->bt_W, W.data(), W.size() * 8)) ||
             (rc = up((void**)&D->bt_src, src.data(), src.size() * 4)) ||
             (rc = up((void**)&D->bt_out, out.data(), out.size() * 4)) ||
             (rc = up((void**)&D->bt_ctr, nullptr, 16)))
@@ -3418,9 +3633,37 @@ int launch_bt(Handle* h, HotArgs& ha, cudaStream_t st) {
     return VF_OK;
 }
 
+// Cooperative launch of the FP32 tcgen05 tile kernel (2 CTAs x 4 warps per SM).
+int launch_bt_tc(Handle* h, HotArgs& ha, cudaStream_t st) {
+    DeviceHMat* D = h->dev;
+    const size_t smem = (size_t)kTStages * (2 * 128 * kTS * 4 + 2 * 16 * kTS * 4);
+    CK(cudaFuncSetAttribute(bt_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bt_tc_kernel, 128, smem));
+    if (per_sm < 1) return set_error(VF_ECUDA, "bt_tc_kernel cannot be resident");
+    int nsm = 148;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
+    const int grid = nsm * std::min(per_sm, 2);
+    TArgs b{D->bt_tiles, D->bt_n1, D->bt_n2, D->bt_Whi, D->bt_Wlo, D->bt_src, D->bt_out, (float*)ha.xt0, (float*)ha.Y,
+            D->N, ha.kp, D->bt_ctr, D->ctl};
+    CK(cudaMemsetAsync(D->bt_ctr, 0, 16, st));
+    CK(cudaMemsetAsync(D->ctl, 0, offsetof(Ctl, bar_gen), st));
+    void* args[] = {&b};
+    {
+        Timer tm(h, st, 2);
+        CK(cudaLaunchCooperativeKernel((const void*)bt_tc_kernel, dim3(grid), dim3(128), args, smem, st));
+    }
+    h->launches_total++;
+    D->last_grid = grid;
+    return VF_OK;
+}
+
 template <typename T, int MODE>
 int launch_hot(Handle* h, HotArgs& a, cudaStream_t st) {
     const int kp = a.kp;
+    if (MODE == M_MATVEC && std::is_same<T, float>::value && kp >= 128 && kp % 128 == 0 && h->dev->bt_ok &&
+        h->dev->bt_Whi)
+        return launch_bt_tc(h, a, st);
     // wide batches on an F-hat that does not fit the resident layout: streamed tiles (FP64 matvec)
     if (MODE == M_MATVEC && std::is_same<T, double>::value && kp >= 16 && h->dev->bt_ok &&
         (kp <= kBCols ? (kp == 16 || kp == 32 || kp == 64 || kp == 128) : kp % kBCols == 0))
@@ -3636,8 +3879,12 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     if ((rc = check_k(nrhs)) || (rc = stream_of(h, &st))) return rc;
     // more than 8 columns on a streamed-tile layout: one bt_kernel launch with the
     // columns padded to 16, 32, 64 or a multiple of 128
-    const bool bt = D->bt_ok && sizeof(T) == 8 && !(D->world > 1 || h->comm) && nrhs > 8 && !getenv("VF_NO_TILES_MV");
-    const int kp = bt ? (nrhs <= 16 ? 16 : nrhs <= 32 ? 32 : nrhs <= 64 ? 64 : (nrhs + 127) / 128 * 128) : pad_k(nrhs);
+    const bool bt = D->bt_ok && !(D->world > 1 || h->comm) && nrhs > 8 && !getenv("VF_NO_TILES_MV");
+    // FP64 tiles (bt_kernel): 16, 32, 64 or a multiple of 128 columns; FP32 tiles on tcgen05
+    // (bt_tc_kernel): the MMA's M = 128 columns per pass
+    const int kp = !bt ? pad_k(nrhs)
+                   : sizeof(T) == 4 ? (nrhs + 127) / 128 * 128
+                                    : (nrhs <= 16 ? 16 : nrhs <= 32 ? 32 : nrhs <= 64 ? 64 : (nrhs + 127) / 128 * 128);
     if ((rc = ensure_scratch(D, kp, st))) return rc;
     reset_counters(h);
     const size_t vb = (size_t)D->N * nrhs * sizeof(T);
@@ -3862,7 +4109,7 @@ void device_free(Handle* h) {
     for (auto& e : D->evpool) if (e) cudaEventDestroy(e);
     for (auto& kv : D->sched) { cudaFree(kv.second.ptr); cudaFree(kv.second.items); }
     stream::free_dev(&D->sl);
-    void* bps[] = {D->bt_tiles, D->bt_W, D->bt_src, D->bt_out, D->bt_ctr, D->segs16, D->p2_segptr16, D->idx16,
+    void* bps[] = {D->bt_tiles, D->bt_W, D->bt_Whi, D->bt_Wlo, D->bt_src, D->bt_out, D->bt_ctr, D->segs16, D->p2_segptr16, D->idx16,
                    D->seg_base16};
     for (void* p : bps) if (p) cudaFree(p);
     delete D;

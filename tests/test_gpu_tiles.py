@@ -49,3 +49,39 @@ def test_tiles_same_blocks(handles, k):
         Y2 = torch.empty_like(Y)
         M.matvec(Xd, Y2)
         assert torch.equal(Y, Y2)
+
+
+@pytest.fixture(scope="module")
+def handles_f32(tmp_path_factory):
+    out = []
+    os.environ["VF_NO_RESIDENT"] = "1"
+    try:
+        for name, (V, F), ms in (("cap", sg.cfg1_mesh(), 2048),
+                                 ("terrain", sg.cfg3_mesh(n=24, crater_D=1000.0 * 24 / 256), 4096)):
+            S = oracle.Scene(V, F)
+            H = hm.compress(S.x, S.F_dense(), 1e-5, dtype="f32", min_size=ms)
+            p = str(tmp_path_factory.mktemp("btf") / f"{name}.hvfm")
+            hm.write_hvfm(H, p)
+            M = vf.ViewFactorMatrix.load(p, device=0)
+            assert M.refresh()["tiles"] > 0
+            out.append((name, S, H, M))
+    finally:
+        del os.environ["VF_NO_RESIDENT"]
+    return out
+
+
+@pytest.mark.parametrize("k", [9, 64, 128, 130, 256])
+def test_tiles_f32_tcgen05_3xtf32(handles_f32, k):
+    """FP32 streamed tiles on the 5th-generation tensor cores (bt_tc_kernel:
+    tcgen05.mma kind::tf32, TMEM accumulator, 3xTF32 split): <= 1e-5 vs the
+    oracle's Alg. 5 of the same (FP32-rounded) blocks, bitwise repeatable."""
+    for name, S, H, M in handles_f32:
+        X = sg.random_rhs(S.N, k, seed=21 + k).astype(np.float32).astype(np.float64)
+        Xd = torch.from_numpy(np.ascontiguousarray(X.T.astype(np.float32))).cuda().T
+        Y = torch.empty((k, S.N), dtype=torch.float32, device="cuda").T
+        M.matvec(Xd, Y)
+        R = hm.hmatvec(H, X)
+        assert np.linalg.norm(Y.cpu().numpy().astype(np.float64) - R) / np.linalg.norm(R) <= 1e-5, (name, k)
+        Y2 = torch.empty_like(Y)
+        M.matvec(Xd, Y2)
+        assert torch.equal(Y, Y2)
