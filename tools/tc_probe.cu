@@ -17,6 +17,10 @@ __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)_
 __device__ __forceinline__ int off_mn(int mn, int k, int sbo, int lbo) {
     return (mn >> 2) * sbo + (k >> 3) * lbo + (k & 7) * 16 + (mn & 3) * 4;
 }
+// K-major SWIZZLE_NONE: element (mn, k) at (mn/8)*SBO + (k/4)*LBO + (mn%8)*16 + (k%4)*4 bytes
+__device__ __forceinline__ int off_k(int mn, int k, int sbo, int lbo) {
+    return (mn >> 3) * sbo + (k >> 2) * lbo + (mn & 7) * 16 + (k & 3) * 4;
+}
 __device__ __forceinline__ uint64_t sdesc(unsigned addr, unsigned lbo, unsigned sbo) {
     uint64_t d = 0;
     d |= (uint64_t)((addr >> 4) & 0x3fff);
@@ -33,16 +37,18 @@ __global__ void probe(const float* A /*M x K row-major*/, const float* B /*K x N
     __shared__ uint32_t tbase;
     __shared__ __align__(8) uint64_t bar;
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
-    // A operand: (mn = m, k); SBO = (K/8)*128 (all K rows of a 4-wide MN group), LBO = 128
-    const int sboA = (K / 8) * 128, lboA = 128;
-    const int sboB = (K / 8) * 128, lboB = 128;
+    const bool kmaj = mode >= 2;
+    // MN-major: SBO = (K/8)*128 (all K rows of a 4-wide MN group), LBO = 128 (next 8 K rows)
+    // K-major:  SBO = 128 (next 8 MN rows), LBO = (MN/8)*128 (next 4 K elements)
+    const int sboA = kmaj ? 128 : (K / 8) * 128, lboA = kmaj ? (M / 8) * 128 : 128;
+    const int sboB = kmaj ? 128 : (K / 8) * 128, lboB = kmaj ? (N / 8) * 128 : 128;
     for (int i = t; i < M * K; i += blockDim.x) {
         const int m = i / K, k = i % K;
-        *reinterpret_cast<float*>(sa + off_mn(m, k, sboA, lboA)) = A[m * K + k];
+        *reinterpret_cast<float*>(sa + (kmaj ? off_k(m, k, sboA, lboA) : off_mn(m, k, sboA, lboA))) = A[m * K + k];
     }
     for (int i = t; i < N * K; i += blockDim.x) {
         const int n = i / K, k = i % K;
-        *reinterpret_cast<float*>(sb + off_mn(n, k, sboB, lboB)) = B[k * N + n];
+        *reinterpret_cast<float*>(sb + (kmaj ? off_k(n, k, sboB, lboB) : off_mn(n, k, sboB, lboB))) = B[k * N + n];
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(smem_u32(&tbase)));
@@ -50,6 +56,7 @@ __global__ void probe(const float* A /*M x K row-major*/, const float* B /*K x N
     }
     if (t == 0) {
         asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bar)));
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -58,21 +65,31 @@ __global__ void probe(const float* A /*M x K row-major*/, const float* B /*K x N
     const uint32_t tm = tbase;
     // idesc: c_format F32 (bit 4), a/b format TF32 (2 at bits 7 and 10), a/b MN-major (bits 15, 16),
     // N >> 3 at bit 17, M >> 4 at bit 24
-    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) | ((uint32_t)(N >> 3) << 17) |
+    const uint32_t mj = kmaj ? 0u : 1u;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (mj << 15) | (mj << 16) | ((uint32_t)(N >> 3) << 17) |
                            ((uint32_t)(M >> 4) << 24);
-    if (t == 0) {
+    if (mode == 4 && warp < 4) {          // tcgen05.st / ld round trip
+        uint32_t v = 1000u + (unsigned)(warp * 32 + lane);
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};\n" ::"r"(tm + ((uint32_t)(warp * 32) << 16)), "r"(v));
+        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+    }
+    if (t == 0 && mode != 4) {
         for (int ks = 0; ks < K / 8; ++ks) {
-            const uint64_t da = mode == 0 ? sdesc(smem_u32(sa) + ks * lboA, lboA, sboA) : sdesc(smem_u32(sa) + ks * lboA, sboA, lboA);
-            const uint64_t db = mode == 0 ? sdesc(smem_u32(sb) + ks * lboB, lboB, sboB) : sdesc(smem_u32(sb) + ks * lboB, sboB, lboB);
+            // K step of 8: MN-major -> next 8-row K group (+LBO); K-major -> 2 K chunks of 4 (+2 LBO)
+            const unsigned ka = kmaj ? 2 * ks * lboA : ks * lboA, kb = kmaj ? 2 * ks * lboB : ks * lboB;
+            const bool sw = (mode & 1) != 0;
+            const uint64_t da = !sw ? sdesc(smem_u32(sa) + ka, lboA, sboA) : sdesc(smem_u32(sa) + ka, sboA, lboA);
+            const uint64_t db = !sw ? sdesc(smem_u32(sb) + kb, lboB, sboB) : sdesc(smem_u32(sb) + kb, sboB, lboB);
             const uint32_t acc = ks > 0 ? 1u : 0u;
             asm volatile(
                 "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                 " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tm),
                 "l"(da), "l"(db), "r"(idesc), "r"(acc));
         }
+    }
+    if (t == 0)
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&bar))
                      : "memory");
-    }
     // wait for the MMAs
     {
         unsigned ok = 0;
@@ -113,7 +130,7 @@ int main() {
     cudaMemcpy(dA, A.data(), A.size() * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(dB, B.data(), B.size() * 4, cudaMemcpyHostToDevice);
     int anybad = 0;
-    for (int mode = 0; mode < 2; ++mode) {
+    for (int mode = 0; mode < 5; ++mode) {
         cudaMemset(dD, 0, D.size() * 4);
         probe<<<1, 256>>>(dA, dB, dD, mode);
         cudaError_t e = cudaDeviceSynchronize();
@@ -125,6 +142,7 @@ int main() {
         for (int i = 0; i < M * N; ++i) { mx = fmax(mx, fabs(D[i] - R[i])); bad += fabs(D[i] - R[i]) > 1e-4; }
         printf("mode %d: max abs err %g, bad %d of %d; D[0..3] %g %g %g %g ref %g %g %g %g\n", mode, mx, bad, M * N,
                D[0], D[1], D[2], D[3], R[0], R[1], R[2], R[3]);
+        if (mode == 4) printf("st/ld round trip: D[0] %g (expect bits of 1000 -> %g)\n", D[0], __builtin_bit_cast(float, 1000u));
         anybad |= mode == 0 && bad;
     }
     return anybad;
