@@ -1515,20 +1515,21 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
 // keeps single-precision accuracy (BASELINE north_star: "TF32/FP32 paths where
 // the stated tolerance allows"; parity <= 1e-5).  Same tiles as bt_kernel.
 // The MMA is D (columns x tile rows) += X^T (columns x sources) W (sources x
-// rows): M = 64 or 128 columns, N = 16 rows, K = 8 sources per instruction;
-// both operands MN-major in SWIZZLE_NONE core matrices (8 source rows x 16 B):
-// element (mn, k) at (mn/4) SBO + (k/8) 128 + (k%8) 16 + (mn%4) 4 bytes.
-// X slices are staged raw with cp.async, split in shared memory into
-// hi = tf32(x) and lo = x - hi; W arrives pre-split (two blobs).  Per K step
-// three MMAs: hi*hi, hi*lo, lo*hi.  One thread issues, tcgen05.commit signals
-// one mbarrier per ring slot (slot reuse) and one per tile (epilogue);
-// warps 0-3 read the 128 TMEM lanes (tcgen05.ld 32x32b.x16) and store.
+// rows): M = 128 columns, N = 16 rows, K = 8 sources per instruction; both
+// operands K-major in SWIZZLE_NONE core matrices (8 rows x 16 B = 4 sources):
+// element (mn, k) at (mn/8) 128 + (k/4) LBO + (mn%8) 16 + (k%4) 4 bytes,
+// LBO = (MN/8) 128 (tools/tc_probe.cu checks this convention).  The X slice
+// is staged raw (row-major) with cp.async and split in shared memory into
+// hi = tf32(x) and lo = x - hi while being transposed into the K-major
+// layout; the weights arrive pre-split and pre-arranged per 32-source slice
+// (two blobs).  Per K step three MMAs: hi*hi, hi*lo, lo*hi.  One thread
+// issues; tcgen05.commit signals an mbarrier once per slice; warps 0-3 read
+// the 128 TMEM lanes (tcgen05.ld 32x32b.x16) and store.
 constexpr int kTS = 32;            // sources per slice (4 K steps)
-constexpr int kTStages = 3;
 struct TArgs {
     const BTile* tiles;
     int32_t n1, n2;
-    const float* Whi;
+    const float* Whi;              // per tile: ceil(K/32) slices of [16 rows x 32 sources] K-major (2 KB)
     const float* Wlo;
     const int32_t* src;
     const int32_t* outrow;
@@ -1561,12 +1562,15 @@ __device__ __forceinline__ void tc_wait(uint64_t* bar, unsigned parity) {
         if (++spins > (1ull << 26)) __trap();
     }
 }
+constexpr int kTRaw = kTS * 128 * 4;              // raw X slice, row-major [32 sources][128 columns]
+constexpr int kTA = 128 * kTS * 4;                // one K-major A operand (hi or lo)
+constexpr int kTB = 16 * kTS * 4;                 // one K-major B operand (hi or lo)
+constexpr int kTSmem = 3 * (kTRaw + 2 * kTB) + 2 * (2 * kTA);   // 3 staging slots, 2 A buffer pairs
 
-__global__ void __launch_bounds__(128, 2) bt_tc_kernel(TArgs a) {
+__global__ void __launch_bounds__(256, 1) bt_tc_kernel(TArgs a) {
     extern __shared__ __align__(1024) unsigned char tsm[];
     __shared__ uint32_t tmem_base;
-    __shared__ __align__(8) uint64_t bar_slot[kTStages];
-    __shared__ __align__(8) uint64_t bar_tile;
+    __shared__ __align__(8) uint64_t bar_mma;
     __shared__ int s_item;
     const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
     if (warp == 0) {
@@ -1574,16 +1578,19 @@ __global__ void __launch_bounds__(128, 2) bt_tc_kernel(TArgs a) {
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (t == 0) {
-        for (int q = 0; q < kTStages; ++q) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc_smem(bar_slot + q)));
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc_smem(&bar_tile)));
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(tc_smem(&bar_mma)));
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = tmem_base;
-    unsigned slot_uses[kTStages] = {0, 0, 0};   // completed MMA batches per slot (parity tracking)
-    unsigned tile_uses = 0;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    constexpr unsigned LBOA = (128 / 8) * 128, LBOB = (16 / 8) * 128;
+    unsigned mma_issued = 0;                              // slices whose MMAs were committed (CTA-wide count)
+    auto raw = [&](int st) { return tsm + st * (kTRaw + 2 * kTB); };
+    auto bsl = [&](int st, int h) { return tsm + st * (kTRaw + 2 * kTB) + kTRaw + h * kTB; };
+    auto abuf = [&](int q, int h) { return tsm + 3 * (kTRaw + 2 * kTB) + q * 2 * kTA + h * kTA; };
     for (int phase = 1; phase <= 2; ++phase) {
         const int nt = phase == 1 ? a.n1 : a.n2, base = phase == 1 ? 0 : a.n1;
         for (;;) {
@@ -1593,65 +1600,58 @@ __global__ void __launch_bounds__(128, 2) bt_tc_kernel(TArgs a) {
             const int it = s_item;
             if (it >= nt) break;
             const BTile B = a.tiles[base + it];
-            const float* Wh = a.Whi + B.w_off;
-            const float* Wl = a.Wlo + B.w_off;
             const int32_t* S = a.src + B.s_off;
             const int nsl = (B.K + kTS - 1) / kTS;
             for (int cb = 0; cb < a.kp; cb += 128) {
-                const int MB = min(128, a.kp - cb);              // 64 or 128 columns (the MMA's M)
-                const unsigned sboA = (kTS / 8) * 128, sboB = (kTS / 8) * 128;
-                const size_t abytes = (size_t)MB * kTS * 4, bbytes = (size_t)16 * kTS * 4;
-                const size_t sbytes = 2 * abytes + 2 * bbytes;     // A_hi, A_lo, B_hi, B_lo
-                const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
-                                       ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(MB >> 4) << 24);
-                auto bufA = [&](int slot, int h) { return tsm + slot * sbytes + h * abytes; };
-                auto bufB = [&](int slot, int h) { return tsm + slot * sbytes + 2 * abytes + h * bbytes; };
-                auto stage = [&](int sl, int slot) {
+                auto stage = [&](int sl, int st) {
                     const int j0 = sl * kTS, n = min(kTS, B.K - j0);
-                    unsigned char* Alo = bufA(slot, 1);
-                    const int per = MB >> 2;                       // 16-B chunks per source row
-                    for (int op = t; op < kTS * per; op += 128) {
-                        const int j = op / per, c4 = op - j * per;
+                    unsigned char* rw = raw(st);
+                    for (int op = t; op < kTS * 32; op += 256) {          // 32 16-B chunks per 512-B row
+                        const int j = op >> 5, c4 = op & 31;
                         const bool ok = j < n;
                         const int64_t row = ok ? S[j0 + j] : 0;
-                        cpa<16>(Alo + c4 * sboA + (j >> 3) * 128 + (j & 7) * 16, a.XT + row * a.kp + cb + c4 * 4, ok ? 16 : 0);
+                        cpa<16>(rw + j * 512 + c4 * 16, a.XT + row * a.kp + cb + c4 * 4, ok ? 16 : 0);
                     }
-                    for (int op = t; op < kTS * 4 * 2; op += 128) {  // W hi / lo: 4 chunks (16 rows) per source
-                        const int hsel = op / (kTS * 4), o2 = op - hsel * kTS * 4;
-                        const int j = o2 >> 2, r4 = o2 & 3;
-                        const bool ok = j < n;
-                        const float* w = hsel ? Wl : Wh;
-                        cpa<16>(bufB(slot, hsel) + r4 * sboB + (j >> 3) * 128 + (j & 7) * 16,
-                                w + (int64_t)(j0 + (ok ? j : 0)) * 16 + r4 * 4, ok ? 16 : 0);
+                    const int64_t wo = B.w_off + (int64_t)sl * kTS * 16;  // this slice's pre-arranged weights
+                    for (int op = t; op < 2 * (kTB / 16); op += 256) {
+                        const int h = op / (kTB / 16), u = op - h * (kTB / 16);
+                        cpa<16>(bsl(st, h) + u * 16, (h ? a.Wlo : a.Whi) + wo + u * 4, 16);
                     }
                 };
-                for (int p = 0; p < kTStages - 1; ++p) {
-                    if (p < nsl) {
-                        if (slot_uses[p] > 0) tc_wait(bar_slot + p, (slot_uses[p] - 1) & 1);   // MMAs done with it
-                        stage(p, p);
-                    }
-                    cpa_commit();
-                }
+                if (nsl > 0) stage(0, 0);
+                cpa_commit();
+                if (nsl > 1) stage(1, 1);
+                cpa_commit();
                 for (int sl = 0; sl < nsl; ++sl) {
-                    const int slot = sl % kTStages;
-                    if (sl + kTStages - 1 < nsl) {
-                        const int ns_ = (sl + kTStages - 1) % kTStages;
-                        if (slot_uses[ns_] > 0) tc_wait(bar_slot + ns_, (slot_uses[ns_] - 1) & 1);
-                        stage(sl + kTStages - 1, ns_);
+                    if (sl + 2 < nsl) {
+                        // stage (sl + 2) % 3 held slice sl - 1: wait until its MMAs have read it
+                        if (sl >= 1) tc_wait(&bar_mma, (mma_issued - 1) & 1);
+                        stage(sl + 2, (sl + 2) % 3);
                     }
                     cpa_commit();
-                    cpa_wait<kTStages - 1>();
+                    cpa_wait<2>();
+                    if (sl >= 1 && sl + 2 >= nsl) tc_wait(&bar_mma, (mma_issued - 1) & 1);   // A[(sl) % 2] free
                     __syncthreads();
-                    {   // split the staged X slice: hi = tf32(x) into A_hi, lo = x - hi in place
-                        float* Alo = reinterpret_cast<float*>(bufA(slot, 1));
-                        float* Ahi = reinterpret_cast<float*>(bufA(slot, 0));
-                        for (int e = t; e < MB * kTS; e += 128) {
-                            const float x = Alo[e];
-                            uint32_t hb;
-                            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x));
-                            const float hi = __uint_as_float(hb);
-                            Ahi[e] = hi;
-                            Alo[e] = x - hi;
+                    {   // split + transpose: hi = tf32(x), lo = x - hi into K-major A[sl % 2]
+                        const float* rw = reinterpret_cast<const float*>(raw(sl % 3));
+                        unsigned char* ah = abuf(sl & 1, 0);
+                        unsigned char* al = abuf(sl & 1, 1);
+                        for (int task = t; task < 128 * (kTS / 4); task += 256) {
+                            const int c = task & 127, j4 = task >> 7;
+                            float4 hv, lv;
+                            float* hp = &hv.x;
+                            float* lp = &lv.x;
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) {
+                                const float x = rw[(4 * j4 + q) * 128 + c];
+                                uint32_t hb;
+                                asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x));
+                                hp[q] = __uint_as_float(hb);
+                                lp[q] = x - hp[q];
+                            }
+                            const int off = (c >> 3) * 128 + j4 * LBOA + (c & 7) * 16;
+                            *reinterpret_cast<float4*>(ah + off) = hv;
+                            *reinterpret_cast<float4*>(al + off) = lv;
                         }
                     }
                     asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
@@ -1659,25 +1659,25 @@ __global__ void __launch_bounds__(128, 2) bt_tc_kernel(TArgs a) {
                     __syncthreads();
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                     if (t == 0) {
-                        const unsigned ah = tc_smem(bufA(slot, 0)), al = tc_smem(bufA(slot, 1));
-                        const unsigned bh = tc_smem(bufB(slot, 0)), bl = tc_smem(bufB(slot, 1));
+                        const unsigned ah = tc_smem(abuf(sl & 1, 0)), al = tc_smem(abuf(sl & 1, 1));
+                        const unsigned bh = tc_smem(bsl(sl % 3, 0)), bl = tc_smem(bsl(sl % 3, 1));
+#pragma unroll
                         for (int ks = 0; ks < kTS / 8; ++ks) {
-                            const unsigned ko = ks * 128;
                             const uint32_t first = (sl == 0 && ks == 0) ? 0u : 1u;
-                            tc_mma(tmem, tc_desc(ah + ko, 128, sboA), tc_desc(bh + ko, 128, sboB), idesc, first);
-                            tc_mma(tmem, tc_desc(ah + ko, 128, sboA), tc_desc(bl + ko, 128, sboB), idesc, 1u);
-                            tc_mma(tmem, tc_desc(al + ko, 128, sboA), tc_desc(bh + ko, 128, sboB), idesc, 1u);
+                            const uint64_t dah = tc_desc(ah + 2 * ks * LBOA, LBOA, 128), dal = tc_desc(al + 2 * ks * LBOA, LBOA, 128);
+                            const uint64_t dbh = tc_desc(bh + 2 * ks * LBOB, LBOB, 128), dbl = tc_desc(bl + 2 * ks * LBOB, LBOB, 128);
+                            tc_mma(tmem, dah, dbh, idesc, first);
+                            tc_mma(tmem, dah, dbl, idesc, 1u);
+                            tc_mma(tmem, dal, dbh, idesc, 1u);
                         }
-                        tc_commit(bar_slot + slot);
+                        tc_commit(&bar_mma);
                     }
-                    ++slot_uses[slot];
+                    ++mma_issued;
                 }
                 cpa_wait<0>();
-                if (t == 0) tc_commit(&bar_tile);
-                tc_wait(&bar_tile, tile_uses & 1);
-                ++tile_uses;
+                if (nsl > 0) tc_wait(&bar_mma, (mma_issued - 1) & 1);       // the tile's last MMAs
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                if (warp * 32 < MB) {
+                if (warp < 4) {
                     uint32_t r[16];
                     const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
                     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
@@ -1687,10 +1687,12 @@ __global__ void __launch_bounds__(128, 2) bt_tc_kernel(TArgs a) {
                                  : "r"(ta));
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
                     const int col = cb + warp * 32 + lane;
-                    for (int rr = 0; rr < B.nrows; ++rr) {
+#pragma unroll
+                    for (int rr = 0; rr < 16; ++rr) {
+                        if (rr >= B.nrows) break;
                         const int64_t orow = a.outrow[B.out_off + rr];
                         float* dst = phase == 1 ? a.XT + (a.N + orow) * a.kp + col : a.Y + orow * a.kp + col;
-                        *dst = __uint_as_float(r[rr]);
+                        *dst = nsl > 0 ? __uint_as_float(r[rr]) : 0.0f;
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -3213,9 +3215,35 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         int64_t wn = 0, sn = 0;
         for (auto* v : {&t1, &t2}) for (auto& x : *v) { wn += (int64_t)x.w.size(); sn += (int64_t)x.srcs.size(); }
         W.reserve(wn); src.reserve(sn);
+        std::vector<float> Whi, Wlo;                  // FP32: 3xTF32 split, K-major per 32-source slice
+        auto tf32_hi = [](float w) {                  // cvt.rna.tf32.f32: round to nearest, ties away
+            uint32_t u;
+            std::memcpy(&u, &w, 4);
+            u = (u + 0x1000u) & 0xffffe000u;
+            float h;
+            std::memcpy(&h, &u, 4);
+            return std::isfinite(h) ? h : w;
+        };
         auto add = [&](HT& x) {
             BTile B{x.nrows, (int32_t)x.srcs.size(), (int64_t)W.size(), (int64_t)src.size(), (int64_t)out.size()};
-            W.insert(W.end(), x.w.begin(), x.w.end());
+            if (sizeof(T) == 4) {
+                // slice sl: element (row r, source j' = j - 32 sl) at (r/8) 32 + (j'/4) 64 + (r%8) 4 + j'%4 floats
+                const int64_t K = (int64_t)x.srcs.size(), nsl = (K + 31) / 32;
+                B.w_off = (int64_t)Whi.size();
+                Whi.resize(Whi.size() + nsl * 512, 0.0f);
+                Wlo.resize(Wlo.size() + nsl * 512, 0.0f);
+                for (int64_t j = 0; j < K; ++j)
+                    for (int r = 0; r < 16; ++r) {
+                        const float w = (float)x.w[(size_t)j * 16 + (r ^ (4 * (j & 3)))];
+                        const int64_t jj = j & 31;
+                        const int64_t o = B.w_off + (j >> 5) * 512 + (r >> 3) * 32 + (jj >> 2) * 64 + (r & 7) * 4 + (jj & 3);
+                        const float h = tf32_hi(w);
+                        Whi[o] = h;
+                        Wlo[o] = w - h;
+                    }
+            } else {
+                W.insert(W.end(), x.w.begin(), x.w.end());
+            }
             src.insert(src.end(), x.srcs.begin(), x.srcs.end());
             out.insert(out.end(), x.out.begin(), x.out.end());
             tiles.push_back(B);
@@ -3230,22 +3258,8 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         if (sizeof(T) == 8) {
             if ((rc = up((void**)&D->bt_W, W.data(), W.size() * 8))) return rc;
         } else {
-            // FP32 handles: the weights split for 3xTF32 (hi = tf32 round-to-nearest-away of
-            // the float value, what cvt.rna.tf32.f32 gives; lo = w - hi)
-            std::vector<float> hi(W.size()), lo(W.size());
-            for (size_t e = 0; e < W.size(); ++e) {
-                const float w = (float)W[e];
-                uint32_t u;
-                std::memcpy(&u, &w, 4);
-                u = (u + 0x1000u) & 0xffffe000u;
-                float hf;
-                std::memcpy(&hf, &u, 4);
-                if (!std::isfinite(hf)) hf = w;
-                hi[e] = hf;
-                lo[e] = w - hf;
-            }
-            std::vector<double>().swap(W);
-            if ((rc = up((void**)&D->bt_Whi, hi.data(), hi.size() * 4)) || (rc = up((void**)&D->bt_Wlo, lo.data(), lo.size() * 4)))
+            if (Whi.empty()) { Whi.resize(512, 0.0f); Wlo.resize(512, 0.0f); }
+            if ((rc = up((void**)&D->bt_Whi, Whi.data(), Whi.size() * 4)) || (rc = up((void**)&D->bt_Wlo, Wlo.data(), Wlo.size() * 4)))
                 return rc;
         }
         if ((rc = up((void**)&D->bt_tiles, tiles.data(), tiles.size() * sizeof(BTile))) ||
@@ -3633,17 +3647,17 @@ int launch_bt(Handle* h, HotArgs& ha, cudaStream_t st) {
     return VF_OK;
 }
 
-// Cooperative launch of the FP32 tcgen05 tile kernel (2 CTAs x 4 warps per SM).
+// Cooperative launch of the FP32 tcgen05 tile kernel (one CTA of 8 warps per SM).
 int launch_bt_tc(Handle* h, HotArgs& ha, cudaStream_t st) {
     DeviceHMat* D = h->dev;
-    const size_t smem = (size_t)kTStages * (2 * 128 * kTS * 4 + 2 * 16 * kTS * 4);
+    const size_t smem = (size_t)kTSmem;
     CK(cudaFuncSetAttribute(bt_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bt_tc_kernel, 128, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bt_tc_kernel, 256, smem));
     if (per_sm < 1) return set_error(VF_ECUDA, "bt_tc_kernel cannot be resident");
     int nsm = 148;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
-    const int grid = nsm * std::min(per_sm, 2);
+    const int grid = nsm;                                  // one CTA per SM (TMEM: 32 columns each)
     TArgs b{D->bt_tiles, D->bt_n1, D->bt_n2, D->bt_Whi, D->bt_Wlo, D->bt_src, D->bt_out, (float*)ha.xt0, (float*)ha.Y,
             D->N, ha.kp, D->bt_ctr, D->ctl};
     CK(cudaMemsetAsync(D->bt_ctr, 0, 16, st));
@@ -3651,7 +3665,7 @@ int launch_bt_tc(Handle* h, HotArgs& ha, cudaStream_t st) {
     void* args[] = {&b};
     {
         Timer tm(h, st, 2);
-        CK(cudaLaunchCooperativeKernel((const void*)bt_tc_kernel, dim3(grid), dim3(128), args, smem, st));
+        CK(cudaLaunchCooperativeKernel((const void*)bt_tc_kernel, dim3(grid), dim3(256), args, smem, st));
     }
     h->launches_total++;
     D->last_grid = grid;
