@@ -525,6 +525,115 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
     return acc;
 }
 
+// nrhs = 1, wave-interleaved (VF_K1_WAVE): lane l takes terms base + l of a
+// row's concatenated segments, so one gather instruction touches 32
+// CONSECUTIVE terms -- consecutive CSR columns / contiguous x runs -- i.e. a
+// few cache lines instead of the 128-term spread of the quad mapping above
+// (fewer L1/TEX wavefronts, the limiter of that kernel on configs[2]).  The
+// segment of a wave is found once (warp-uniform binary search on the wave's
+// first term) and lanes past a segment boundary advance with a ballot loop.
+// Values and 16-bit CSR offsets are scalar streaming loads; U waves in flight.
+__device__ __forceinline__ double ld_stream_d(const double* p) {
+#if VF_K1_NA
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n" : "=d"(v) : "l"(p), "l"(l2_evict_first()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ float ld_stream_f(const float* p) {
+#if VF_K1_NA
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;\n" : "=f"(v) : "l"(p), "l"(l2_evict_first()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+__device__ __forceinline__ unsigned ld_stream_u16(const uint16_t* p) {
+    unsigned short v;
+#if VF_K1_NA
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;\n" : "=h"(v) : "l"(p), "l"(l2_evict_first()));
+#else
+    v = __ldg(p);
+#endif
+    return v;
+}
+template <typename T> __device__ __forceinline__ T ld_stream_s(const T* p);
+template <> __device__ __forceinline__ double ld_stream_s<double>(const double* p) { return ld_stream_d(p); }
+template <> __device__ __forceinline__ float ld_stream_s<float>(const float* p) { return ld_stream_f(p); }
+#ifndef VF_K1_WU
+#define VF_K1_WU 4
+#endif
+#ifndef VF_K1_WAVE_DEFAULT
+#define VF_K1_WAVE_DEFAULT 0
+#endif
+template <typename T>
+__device__ __forceinline__ T row_accumulate_wave(const Seg* __restrict__ segs, int64_t s0, int64_t s1,
+                                                 const T* __restrict__ vals, const uint16_t* __restrict__ idx16,
+                                                 const int32_t* __restrict__ seg_base, const T* xt, int lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int U = VF_K1_WU;
+    T acc[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) acc[u] = T(0);
+    for (int64_t sb = s0; sb < s1; sb += 32) {
+        const int ns = (int)(s1 - sb < 32 ? s1 - sb : 32);
+        Seg my{0, 0, 0, 0};
+        int32_t my_base = 0;
+        if (lane < ns) { my = segs[sb + lane]; my_base = seg_base[sb + lane]; }
+        int incl = my.len;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, off);
+            if (lane >= off) incl += v;
+        }
+        const int excl = incl - my.len;
+        const int total = __shfl_sync(FULL, incl, 31);
+        int g0 = 0;                                                // segment of the current wave's first term
+        for (int w0 = 0; w0 < total; w0 += 32 * U) {
+            T v[U], x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int wb = w0 + 32 * u;
+                v[u] = T(0);
+                x[u] = T(0);
+                if (wb < total) {                                  // warp-uniform
+                    while (g0 + 1 < ns && __shfl_sync(FULL, excl, (g0 + 1) & 31) <= wb) ++g0;   // uniform walk
+                    const int t = wb + lane;
+                    int g = g0;
+                    for (;;) {                                     // lanes past a boundary advance
+                        const int nb = __shfl_sync(FULL, excl, (g + 1) & 31);
+                        const bool adv = g + 1 < ns && nb <= t;
+                        if (!__any_sync(FULL, adv)) break;
+                        g += adv ? 1 : 0;
+                    }
+                    const int64_t g_off = __shfl_sync(FULL, my.val_off, g);
+                    const int64_t g_src = __shfl_sync(FULL, my.src, g);
+                    const int g_kind = __shfl_sync(FULL, my.kind, g);
+                    const int g_excl = __shfl_sync(FULL, excl, g);
+                    const int g_base = __shfl_sync(FULL, my_base, g);
+                    if (t < total) {
+                        const int e = t - g_excl;
+                        v[u] = ld_stream_s<T>(vals + g_off + e);
+                        const int64_t xr = g_kind ? (int64_t)g_base + ld_stream_u16(idx16 + g_src + e) : g_src + e;
+                        x[u] = XLD(xt + xr);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) acc[u] = fma(v[u], x[u], acc[u]);
+        }
+    }
+    T a = acc[0];
+#pragma unroll
+    for (int u = 1; u < U; ++u) a += acc[u];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(FULL, a, off);
+    return a;
+}
+
 // Software grid barrier for a cooperative (co-resident) launch.  Traps
 // instead of hanging if a CTA never arrives.
 __device__ __forceinline__ void grid_sync(Ctl* ctl, unsigned nblk) {
@@ -673,9 +782,13 @@ __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_
         constexpr int H = kGroup / 2;                 // rows per pass (register budget)
         double mine = 0.0;
         for (int h0 = 0; h0 < G.nrows; h0 += H) {
-            int64_t vo[H];                            // value offsets (64-bit: F-hat may exceed 2^31 values)
+            // value offsets: a 64-bit base (F-hat may exceed 2^31 values) + 32-bit deltas
+            // (a group's V columns are consecutive runs of vals)
+            const T* vb = vals + a.gvo[G.seg_off * kGroup + h0];
+            int32_t vo[H];
 #pragma unroll
-            for (int r = 0; r < H; ++r) vo[r] = h0 + r < G.nrows ? a.gvo[G.seg_off * kGroup + h0 + r] : -1;
+            for (int r = 0; r < H; ++r)
+                vo[r] = h0 + r < G.nrows ? (int32_t)(a.gvo[G.seg_off * kGroup + h0 + r] - a.gvo[G.seg_off * kGroup + h0]) : -1;
             T acc[H];
 #pragma unroll
             for (int r = 0; r < H; ++r) acc[r] = T(0);
@@ -685,7 +798,7 @@ __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_
                 const T x = __ldcg(xc + row);
                 T v[H];
 #pragma unroll
-                for (int r = 0; r < H; ++r) v[r] = vo[r] >= 0 ? __ldg(vals + vo[r] + j) : T(0);
+                for (int r = 0; r < H; ++r) v[r] = vo[r] >= 0 ? __ldg(vb + vo[r] + j) : T(0);
 #pragma unroll
                 for (int r = 0; r < H; ++r) acc[r] = fma(v[r], x, acc[r]);
             }
@@ -773,7 +886,9 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
             const int64_t r = a.p2_order[nxt];
             int fut = 0;
             if (lane == 0) fut = atomicAdd(a.qctr, 1);
-            const T acc = a.idx16 ? row_accumulate_k1<T, VF_MV_L1 != 0>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
+            const T acc = (VF_K1_WAVE_DEFAULT && a.idx16) ? row_accumulate_wave<T>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
+                                                                       vals, a.idx16, a.seg_base16, xc, lane)
+                        : a.idx16 ? row_accumulate_k1<T, VF_MV_L1 != 0>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
                                                                          vals, a.idx, xc, lane, a.N, nullptr, nullptr,
                                                                          a.idx16, a.seg_base16)
                                   : row_accumulate_k1<T, VF_MV_L1 != 0>(a.segs, a.p2_segptr[r], a.p2_segptr[r + 1],
