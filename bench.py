@@ -646,13 +646,22 @@ def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
     traffic, traffic_src = ncu_traffic(f"{workload}_k{k}_{dt}")
     if max(chunks) > 2:
         smax = pk.get("sm_max_mhz", 1965.0)
-        peak_tf = fp64_peak_tflops(smax) if dt == "f64" else fp32_peak_tflops(smax)
-        dmma = info.get("tiles", 0) > 0 and dt == "f64" and max(chunks) > 8
-        bound = {"bound": "tensor" if dmma else "alu", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                 "frac": ach_tf / peak_tf,
-                 "peak_basis": (("derived FP64 DMMA peak (= the DFMA rate on B200): " if dmma else "derived: ")
-                                + f"148 SM x {64 if dt == 'f64' else 128} FMA/clk x 2 x {smax:.0f} MHz "
-                                  f"(sm_max of {pk_kind} MEASURED_PEAKS.json)")}
+        tiles = info.get("tiles", 0) > 0 and max(chunks) > 8
+        if tiles and dt == "f32":
+            # tcgen05 kind::tf32 with 3xTF32: the measured bf16 peak x the nominal tf32/bf16 ratio
+            # (1.1 / 2.25 PFLOP/s dense), / 3 MMAs per useful product
+            peak_tf = pk.get("bf16_tflops", 1619.6) * (1.1 / 2.25) / 3.0
+            bound = {"bound": "tensor", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s", "frac": ach_tf / peak_tf,
+                     "peak_basis": f"3xTF32 on tcgen05: {pk_kind} MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 "
+                                   "(nominal tf32/bf16 dense ratio) / 3"}
+        else:
+            peak_tf = fp64_peak_tflops(smax) if dt == "f64" else fp32_peak_tflops(smax)
+            dmma = tiles and dt == "f64"
+            bound = {"bound": "tensor" if dmma else "alu", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
+                     "frac": ach_tf / peak_tf,
+                     "peak_basis": (("derived FP64 DMMA peak (= the DFMA rate on B200): " if dmma else "derived: ")
+                                    + f"148 SM x {64 if dt == 'f64' else 128} FMA/clk x 2 x {smax:.0f} MHz "
+                                      f"(sm_max of {pk_kind} MEASURED_PEAKS.json)")}
     else:
         bound = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm,
                  "peak_basis": f"{pk_kind} MEASURED_PEAKS.json hbm_gbs (copy bandwidth, 'burst' figure for a kernel "
@@ -667,6 +676,9 @@ def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
     elif info.get("tiles", 0) > 0 and dt == "f64":
         kern = ("bt_kernel (streamed 16-row tiles, [K][16] weights x staged XT rows on FP64 tensor cores, DMMA "
                 "m8n8k4; phase 1 T tiles, grid barrier, phase 2 row tiles)")
+    elif info.get("tiles", 0) > 0:
+        kern = ("bt_tc_kernel (streamed 16-row tiles on tcgen05 kind::tf32, TMEM accumulator, 3xTF32 split; "
+                "phase 1 T tiles, grid barrier, phase 2 row tiles)")
     else:
         kern = f"hot_kernel<{tn},32,VEC,M_MATVEC> (wide per-row: warp across 32 VEC columns)"
     return {**bound, "traffic": traffic, "traffic_source": traffic_src,
