@@ -859,6 +859,69 @@ def run_terrain(args, rank, world, local_rank):
         dist.destroy_process_group()
 
 
+def run_alg6(args, rank, world, local_rank):
+    """NEXT-1 line: Alg. 6 time stepping on the configs[2] terrain,
+    one scenario, a sun circling at 5 deg elevation in `--alg6-steps-per-day`
+    steps per lunar day, M = 30 subsurface layers to 0.5 m (reading A27).  One
+    step = the 2-column F-hat product (two nrhs = 1 applies) + the
+    Crank-Nicolson column update of every facet.  metric: time steps / s."""
+    import torch
+    import paper_2209_07632_b200 as vf
+    import scenegen as sg
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    M, V, F, binfo = terrain_fhat(args, local_rank)
+    info = M.refresh()
+    N = info["N"]
+    stream = torch.cuda.current_stream(dev)
+    M.set_stream(stream.cuda_stream)
+    nday = args.alg6_steps_per_day
+    suns = sg.sun_dirs(5.0, nday)
+    Q = M.insolation(suns, S_SUN)                                     # N x nday (host, untimed)
+    Qd = torch.from_numpy(np.ascontiguousarray(Q.T)).to(dev)          # row n = step n's N-vector
+    alb = np.full(N, ALBEDO)
+    emi = np.full(N, EMISS)
+    T0 = np.full((N, 1), 200.0, order="F")
+    layers, depth = 30, 0.5
+    st = vf.TimeStepper(M, alb, emi, np.asfortranarray(Q[:, :1]), T0, layers=layers, depth=depth, ratio=1.2,
+                        k_th=0.005, rho_c=1.2e6)
+    dt = 29.53 * 86400.0 / nday
+    Tn = torch.empty((1, N), dtype=torch.float64, device=dev).T
+    n = [1]
+
+    def step():
+        q = Qd[n[0] % nday].reshape(N, 1)
+        st.step(q, dt, Tn)
+        n[0] += 1
+        return 1
+
+    tm = time_steps(M, vf, step, args.steps, args.warmup, stream, None, local_rank, per_step_sync=False)
+    t_ms = tm["t_ms"]
+    value = args.steps / (t_ms / 1e3)
+    if rank == 0:
+        pk, pk_kind = peaks()
+        w = 8
+        kb = info.get("k1_payload_bytes") or (info["p1_bytes"] + info["p2_bytes"])
+        bytes_apply = kb + (info["p1_src_rows"] + info["p2_src_rows"] + info["t_rows"] + info["active_rows"]) * w
+        avg = tm["ms_hot"] / max(tm["l_hot"], 1)
+        ach = bytes_apply / (avg * 1e-3) / 1e9 if avg > 0 else 0.0
+        hbm = pk.get("hbm_gbs", 6559.0)
+        line = {"metric": "Alg. 6 time steps per second (2-column F-hat product + Crank-Nicolson columns)",
+                "value": value, "unit": "steps/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic",
+                "config": {"workload": f"NEXT-1 Alg. 6 on BASELINE configs[2] ({N} facets), one scenario, sun at 5 deg "
+                                       f"elevation, {nday} steps per lunar day, {layers} layers to {depth} m",
+                           "N": N, "layers": layers, **binfo},
+                "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                             "kernel": "the nrhs = 1 apply (two per step)", "avg_launch_ms": avg,
+                             "launches": tm["l_hot"], "share_of_step": tm["ms_hot"] / t_ms if t_ms > 0 else None,
+                             "alg_bytes_per_apply": bytes_apply},
+                "gpu_launches": tm["launches"], "clocks": tm["clocks"]}
+        print(json.dumps(line), flush=True)
+    st.close()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -868,10 +931,11 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--workload", default="cfg3", choices=["cfg2", "cfg3", "cfg5"],
+    ap.add_argument("--workload", default="cfg3", choices=["cfg2", "cfg3", "cfg5", "alg6"],
                     help="cfg3: BASELINE configs[2] matvec (default); cfg2: configs[1] batched thermal solve; "
                          "cfg5: configs[4] ROWS-sharded single-sun solve on the cfg3 mesh")
     ap.add_argument("--nrhs", type=int, default=1)
+    ap.add_argument("--alg6-steps-per-day", type=int, default=48)
     ap.add_argument("--batched", type=int, default=128,
                     help="cfg3 with nrhs = 1: also time this many columns (configs[2]'s batched case; 0 = off)")
     ap.add_argument("--tol", type=float, default=1e-5)
@@ -889,6 +953,8 @@ def main():
         return
     if args.workload == "cfg2":
         run_gpu(args, rank, world, local_rank)
+    elif args.workload == "alg6":
+        run_alg6(args, rank, world, local_rank)
     else:
         run_terrain(args, rank, world, local_rank)
 
