@@ -770,10 +770,16 @@ __device__ __forceinline__ void solve_epilogue(const HotArgs& a, const T* xc, T*
 #endif
 constexpr int kP1Unroll = VF_P1_UNROLL;
 template <typename T>
+__device__ __forceinline__ void phase1_part_k1(const HotArgs& a, T* xc, int64_t pi, int lane);
+template <typename T>
 __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_t gwarp, int lane) {
+    for (int32_t q = a.s1_ptr[gwarp]; q < a.s1_ptr[gwarp + 1]; ++q) phase1_part_k1<T>(a, xc, a.s1_items[q], lane);
+}
+// one phase-1 part item pi: (row group of one SVD block, part of its V rows)
+template <typename T>
+__device__ __forceinline__ void phase1_part_k1(const HotArgs& a, T* xc, int64_t pi, int lane) {
     const T* vals = static_cast<const T*>(a.vals);
-    for (int32_t q = a.s1_ptr[gwarp]; q < a.s1_ptr[gwarp + 1]; ++q) {
-        const int64_t pi = a.s1_items[q];                 // part item
+    {
         const int64_t gi = a.pp_group[pi];
         const int j0 = a.pp_begin[pi], jn = j0 + a.pp_len[pi];
         const int np = a.pp_n[pi];
@@ -1821,6 +1827,249 @@ __global__ void __launch_bounds__(256, 1) bt_tc_kernel(TArgs a) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(tmem));
 }
 
+// ---- nrhs = 1 pipelined apply (k1p_kernel; SURVEY §8(a) a2 + a3, Alg. 5
+// P:263-276 at one right-hand side -- the HBM-bound per-time-step MVP).
+// Why: the row kernel above keeps one 4-term chunk per lane in flight and
+// then gathers its x values, so each round costs an HBM latency PLUS a gather
+// latency, and by Little's law ~32 warps/SM x 1.3 KB per ~1.5 us caps it near
+// 4 TB/s.  Here every warp owns a ring of D round slots in shared memory: a
+// round = one 4-term chunk per lane (values, 16-bit CSR offsets via 16/8-B
+// cp.async with the L2 evict-first policy, plus a 16-B descriptor the lane
+// writes itself), issued D - 1 rounds ahead of the round being consumed, so
+// the F-hat stream stays in flight while the x gathers of the current round
+// resolve.  A lane only ever reads back its own slot entries
+// (cp.async.wait_group makes them visible to the issuing thread), so rounds
+// need no warp barrier.  The issuer runs ahead across row boundaries (the
+// next row's ticket is fetched early).
+// One queue for both phases: tickets [0, n_pp) are phase-1 part items in LPT
+// order (T = S V^T x, phase1_part_k1), the rest phase-2 rows in LPT order.
+// No grid barrier: each row's X-sourced runs come first in its segment list
+// (upload_impl), and before a round touching a U_b run's T rows is consumed
+// the warp waits until all n_pp phase-1 items have finished (a counter with
+// release/acquire) -- every phase-1 item is dequeued before any row, by a
+// running warp that waits on nothing, so the wait always ends.  Each row is
+// still summed by one warp in a fixed lane/round order: bitwise reproducible.
+#ifndef VF_K1P_D
+#define VF_K1P_D 4
+#endif
+#ifndef VF_K1P_CTAS
+#define VF_K1P_CTAS 4
+#endif
+constexpr int kK1pD = VF_K1P_D;
+__device__ __forceinline__ void cpa16_ef(unsigned d, const void* g, int src_bytes, uint64_t pol) {
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2, %3;\n" ::"r"(d), "l"(g), "r"(src_bytes), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void cpa8_ef(unsigned d, const void* g, int src_bytes, uint64_t pol) {
+    asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2, %3;\n" ::"r"(d), "l"(g), "r"(src_bytes), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+template <typename T>
+__host__ __device__ constexpr size_t k1p_warp_bytes() {
+    return (size_t)kK1pD * 32 * (4 * sizeof(T) + 8 + 8) + (size_t)kK1pD * 4;
+}
+// descriptor (int2): x = first XT row (runs) or run base (CSR); y = valid terms
+// (0..4) | CSR << 3 | T rows << 4 | aligned vector x << 5 | last round of its row << 6
+template <typename T>
+__global__ void __launch_bounds__(kThreads, VF_K1P_CTAS) k1p_kernel(HotArgs a, int32_t* ctr, const int32_t* p1_order,
+                                                                    int32_t n_pp) {
+    extern __shared__ __align__(16) unsigned char k1p_sm[];
+    constexpr unsigned FULL = 0xffffffffu;
+    constexpr int D = kK1pD;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    unsigned char* wbase = k1p_sm + (size_t)warp * k1p_warp_bytes<T>();
+    T* sv = reinterpret_cast<T*>(wbase);                                          // [D][32][4]
+    uint2* six = reinterpret_cast<uint2*>(wbase + (size_t)D * 32 * 4 * sizeof(T));   // [D][32]
+    int2* smeta = reinterpret_cast<int2*>(wbase + (size_t)D * 32 * (4 * sizeof(T) + 8));   // [D][32]
+    int* srow = reinterpret_cast<int*>(wbase + (size_t)D * 32 * (4 * sizeof(T) + 16));     // [D] output row (lane 0)
+    T* xt = static_cast<T*>(a.xt0);
+    const T* vals = static_cast<const T*>(a.vals);
+    const int64_t N = a.N;
+    const int32_t n2 = (int32_t)a.n_p2;
+
+    // ---- phase-1 part items
+    int tk = 0;
+    for (;;) {
+        if (lane == 0) tk = atomicAdd(ctr, 1);
+        tk = __shfl_sync(FULL, tk, 0);
+        if (tk >= n_pp) break;
+        phase1_part_k1<T>(a, xt, p1_order[tk], lane);
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(ctr + 1, 1);
+    }
+    tk -= n_pp;                                   // first phase-2 ticket of this warp
+
+    // ---- phase 2, pipelined.  Issuer state: current row, its segment batch
+    const uint64_t pol = l2_evict_first();
+    int64_t s1 = 0, sb = 0;
+    int ns = 0, total = 0, base = 0, excl = 0, orow = -1;
+    bool have_row = false;
+    Seg my{0, 0, 0, 0};
+    int32_t my_base = 0;
+    int tk_next = 0;
+    auto load_batch = [&]() {
+        ns = (int)(s1 - sb < 32 ? s1 - sb : 32);
+        my = Seg{0, 0, 0, 0};
+        my_base = 0;
+        if (lane < ns) { my = a.segs16[sb + lane]; my_base = a.seg_base16[sb + lane]; }
+        const int nch = (my.len + 3) >> 2;
+        int incl = nch;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, off);
+            if (lane >= off) incl += v;
+        }
+        excl = incl - nch;
+        total = __shfl_sync(FULL, incl, 31);
+        base = 0;
+    };
+    auto start_row = [&]() -> bool {
+        if (tk >= n2) return false;
+        const int64_t r = a.p2_order[tk];
+        if (lane == 0) tk_next = atomicAdd(ctr, 1) - n_pp;
+        sb = a.p2_segptr16[r];
+        s1 = a.p2_segptr16[r + 1];
+        orow = a.p2_rows[r];
+        load_batch();
+        have_row = true;
+        return true;
+    };
+    // issue one round into slot s; false when there is no work left (an empty
+    // commit group keeps the group count uniform)
+    auto issue = [&](int s) -> bool {
+        if (!have_row) {
+            if (!start_row()) {
+                asm volatile("cp.async.commit_group;\n" ::);
+                return false;
+            }
+        }
+        const int cc = base + lane;
+        int g = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+            const int cand = g + step;
+            const int e = __shfl_sync(FULL, excl, cand & 31);
+            if (cand < ns && e <= cc) g = cand;
+        }
+        const int64_t g_off = __shfl_sync(FULL, my.val_off, g);
+        const int64_t g_src = __shfl_sync(FULL, my.src, g);
+        const int g_len = __shfl_sync(FULL, my.len, g);
+        const int g_kind = __shfl_sync(FULL, my.kind, g);
+        const int g_excl = __shfl_sync(FULL, excl, g);
+        const int g_base = __shfl_sync(FULL, my_base, g);
+        const bool ok = cc < total;
+        const int e = (cc - g_excl) * 4;
+        const int nv = ok ? min(4, g_len - e) : 0;
+        const unsigned dv = (unsigned)__cvta_generic_to_shared(sv + ((size_t)s * 32 + lane) * 4);
+        const T* pv = ok ? vals + g_off + e : vals;
+        if (sizeof(T) == 8) {
+            cpa16_ef(dv, pv, ok ? 16 : 0, pol);
+            cpa16_ef(dv + 16, pv + 2, ok ? 16 : 0, pol);
+        } else {
+            cpa16_ef(dv, pv, ok ? 16 : 0, pol);
+        }
+        int xb;
+        int info = nv;
+        if (ok && g_kind) {
+            cpa8_ef((unsigned)__cvta_generic_to_shared(six + (size_t)s * 32 + lane), a.idx16 + g_src + e, 8, pol);
+            xb = g_base;
+            info |= 8;
+        } else {
+            xb = ok ? (int)(g_src + e) : 0;
+            if (ok && g_src >= N) info |= 16;
+            if (ok && nv == 4 && ((g_src + e) & (16 / sizeof(T) - 1)) == 0) info |= 32;
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+        // last round of the row?  then the descriptor carries the output row
+        const bool last_batch = sb + 32 >= s1;
+        const bool last = last_batch && base + 32 >= total;
+        smeta[(size_t)s * 32 + lane] = make_int2(xb, info | (last ? 64 : 0));
+        if (lane == 0) srow[s] = orow;                  // read back by lane 0 only
+        base += 32;
+        if (base >= total) {
+            if (!last_batch) {
+                sb += 32;
+                load_batch();
+            } else {
+                have_row = false;
+                tk = __shfl_sync(FULL, tk_next, 0);
+            }
+        }
+        return true;
+    };
+
+    bool t_ready = false;
+    T acc0 = T(0), acc1 = T(0);
+    int issued = 0;
+    for (int s = 0; s < D - 1; ++s) issued += issue(s) ? 1 : 0;
+    for (int c = 0; c < issued; ++c) {
+        if (issue((c + D - 1) % D)) ++issued;
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(D - 1) : "memory");
+        const int s = c % D;
+        const int2 m = smeta[(size_t)s * 32 + lane];
+        const int nv = m.y & 7;
+        if (!t_ready && __any_sync(FULL, (m.y & 16) != 0)) {
+            if (lane == 0) {
+                unsigned long long spins = 0;
+                while (ld_acquire_gpu(ctr + 1) < n_pp) {
+                    __nanosleep(64);
+                    if (++spins > (1ull << 26)) __trap();
+                }
+            }
+            __syncwarp();
+            t_ready = true;
+        }
+        T w[4], x[4];
+        const T* pw = sv + ((size_t)s * 32 + lane) * 4;
+        if (sizeof(T) == 8) {
+            const double2 p0 = reinterpret_cast<const double2*>(pw)[0], p1 = reinterpret_cast<const double2*>(pw)[1];
+            w[0] = (T)p0.x; w[1] = (T)p0.y; w[2] = (T)p1.x; w[3] = (T)p1.y;
+        } else {
+            const float4 p0 = *reinterpret_cast<const float4*>(pw);
+            w[0] = (T)p0.x; w[1] = (T)p0.y; w[2] = (T)p0.z; w[3] = (T)p0.w;
+        }
+        if (m.y & 8) {                                   // CSR: x rows base + u16 offsets, through L1
+            const uint2 q = six[(size_t)s * 32 + lane];
+            const int o[4] = {(int)(q.x & 0xffffu), (int)(q.x >> 16), (int)(q.y & 0xffffu), (int)(q.y >> 16)};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = XLD(xt + m.x + (u < nv ? o[u] : 0));
+        } else if (m.y & 16) {                           // U_b run over T rows (written this launch): L2
+            if (m.y & 32) XV4<T, false>::ld(xt + m.x, x);
+            else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) x[u] = __ldcg(xt + m.x + (u < nv ? u : 0));
+            }
+        } else {                                         // dense-leaf run over X rows (read-only): L1
+            if (m.y & 32) XV4<T, true>::ld(xt + m.x, x);
+            else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) x[u] = XLD(xt + m.x + (u < nv ? u : 0));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const T wu = u < nv ? w[u] : T(0);
+            if (u & 1) acc1 = fma(wu, x[u], acc1);
+            else acc0 = fma(wu, x[u], acc0);
+        }
+        if (m.y & 64) {                                  // warp-uniform: the row's last round
+            T acc = acc0 + acc1;
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL, acc, off);
+            if (lane == 0) static_cast<T*>(a.Y)[srow[s]] = acc;
+            acc0 = T(0);
+            acc1 = T(0);
+        }
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
 // The persistent hot-path kernel (a2-a5).  MODE = M_MATVEC: phase 1, grid
 // barrier, phase 2 -> Y.  MODE = M_SOLVE: Jacobi iterations until every
 // column has r <= tol or `iters` is reached.  GROUPED selects the row-group
@@ -2330,6 +2579,10 @@ struct DeviceHMat {
     // barrier-free nrhs = 1 matvec (tready[n_svd] = the dynamic queue counter)
     int32_t *tready = nullptr, *seg_blk = nullptr, *g1_blk = nullptr, *p2_order = nullptr;
     int64_t n_svd = 0;
+    // pipelined nrhs = 1 matvec (k1p_kernel): phase-1 part items in LPT order,
+    // [0] the queue ticket counter, [1] finished phase-1 items
+    int32_t *p1_order = nullptr, *k1p_ctr = nullptr;
+    int64_t n_pp = 0;
     // resident batched layout (res_kernel); res_ok = false -> streaming path
     bool res_ok = false;
     int res_grid = 0, res_wcap = 0, res_scap = 0;
@@ -2381,6 +2634,15 @@ bool k1_use_stream() {
     const char* e = getenv("VF_K1_KERNEL");
     if (e) return std::strcmp(e, "stream") == 0;
     return VF_K1_DEFAULT_STREAM != 0;
+}
+// the pipelined row kernel (k1p_kernel) vs the row-segment hot_kernel<T,1,1>
+#ifndef VF_K1_DEFAULT_PIPE
+#define VF_K1_DEFAULT_PIPE 0
+#endif
+bool k1_use_pipe() {
+    const char* e = getenv("VF_K1_KERNEL");
+    if (e) return std::strcmp(e, "pipe") == 0;
+    return VF_K1_DEFAULT_PIPE != 0;
 }
 
 // ---- chunk-stream layout of the nrhs = 1 apply (vf_stream.h / vf_stream.cu).
@@ -2976,8 +3238,14 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         const int64_t span16 = getenv("VF_U16_SPAN") ? std::min(65536, std::max(2, atoi(getenv("VF_U16_SPAN")))) : 65536;
         pay16 = D->p1_bytes;                                   // phase 1 unchanged (values, S, V indices)
         for (int64_t r = 0; r < (int64_t)p2_rows.size(); ++r) {
+            // X-sourced runs (dense-leaf rows, CSR) first, then the U_b runs over T
+            // rows: the pipelined kernel (k1p_kernel) streams a row's X part while
+            // phase-1 items may still be producing T
+            for (int pass = 0; pass < 2; ++pass)
             for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1]; ++q) {
                 const Seg sg = segs[q];
+                const bool tsrc = sg.kind == 0 && sg.src >= D->N;
+                if (tsrc != (pass == 1)) continue;
                 if (sg.kind == 0) {
                     s16.push_back(sg); base16.push_back(0);
                     pay16 += (int64_t)sizeof(T) * sg.len;
@@ -3055,10 +3323,19 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         std::iota(order.begin(), order.end(), 0);
         std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) { return D->cost_p2[x] > D->cost_p2[y]; });
         if (order.empty()) order.push_back(0);
+        // phase-1 part items longest first (the queue order of k1p_kernel)
+        std::vector<int32_t> order1(D->cost_p1parts.size());
+        std::iota(order1.begin(), order1.end(), 0);
+        std::stable_sort(order1.begin(), order1.end(),
+                         [&](int32_t x, int32_t y) { return D->cost_p1parts[x] > D->cost_p1parts[y]; });
+        D->n_pp = (int64_t)order1.size();
+        if (order1.empty()) order1.push_back(0);
         D->n_svd = (int64_t)svd_ids.size();
         if ((rc = up((void**)&D->seg_blk, seg_blk.data(), seg_blk.size() * 4)) ||
             (rc = up((void**)&D->g1_blk, g1_blk.data(), g1_blk.size() * 4)) ||
             (rc = up((void**)&D->p2_order, order.data(), order.size() * 4)) ||
+            (rc = up((void**)&D->p1_order, order1.data(), order1.size() * 4)) ||
+            (rc = up((void**)&D->k1p_ctr, nullptr, 16)) ||
             (rc = up((void**)&D->tready, nullptr, (size_t)std::max<int64_t>(D->n_svd + 1, 2) * 4)))
             return rc;
     }
@@ -3976,6 +4253,35 @@ int check_k(int nrhs) {
 // Y = F-hat XT[0:N] with T rows written into XT[N:] -- the chunk-stream kernel
 // if its layout was built, else the row-segment kernel with the LPT row queue
 // and (if built) 16-bit CSR offsets.
+// nrhs = 1 pipelined kernel (k1p_kernel): plain launch, grid = SMs x resident
+// CTAs (it has no grid barrier, so co-residency is not required)
+template <typename T>
+int launch_k1p(Handle* h, void* XT, void* Y, cudaStream_t st) {
+    DeviceHMat* D = h->dev;
+    HotArgs a = hot_args(D, 1, 1);
+    a.xt0 = XT;
+    a.Y = Y;
+    a.p2_order = D->p2_order;
+    a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16;
+    auto fn = k1p_kernel<T>;
+    const size_t smem = (size_t)kWarps * k1p_warp_bytes<T>();
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0, nsm = 148;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kThreads, smem));
+    if (per_sm < 1) return set_error(VF_ECUDA, "k1p kernel cannot be resident");
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
+    const int grid = nsm * std::min(per_sm, VF_K1P_CTAS);
+    CK(cudaMemsetAsync(D->k1p_ctr, 0, 16, st));
+    {
+        Timer tm(h, st, 2);
+        k1p_kernel<T><<<grid, kThreads, smem, st>>>(a, D->k1p_ctr, D->p1_order, (int32_t)D->n_pp);
+        CK(cudaGetLastError());
+    }
+    h->launches_total++;
+    D->last_grid = grid;
+    return VF_OK;
+}
+
 template <typename T>
 int apply_k1(Handle* h, void* XT, void* Y, cudaStream_t st) {
     DeviceHMat* D = h->dev;
@@ -3990,6 +4296,7 @@ int apply_k1(Handle* h, void* XT, void* Y, cudaStream_t st) {
         D->last_grid = grid;
         return VF_OK;
     }
+    if (D->idx16 && k1_use_pipe()) return launch_k1p<T>(h, XT, Y, st);
     HotArgs a = hot_args(D, 1, 1);
     a.xt0 = XT;
     a.Y = Y;
@@ -4226,7 +4533,7 @@ void device_free(Handle* h) {
     if (!D) return;
     cudaSetDevice(h->device);
     void* ptrs[] = {D->pp_group, D->pp_begin, D->pp_len, D->pp_idx, D->pp_n, D->pp_cnt, D->pp_scratch,
-                    D->tready, D->seg_blk, D->g1_blk, D->p2_order, D->r_groups, D->r_outrow, D->r_wblob, D->r_cta_woff, D->r_sblob, D->r_cta_soff,
+                    D->tready, D->seg_blk, D->g1_blk, D->p2_order, D->p1_order, D->k1p_ctr, D->r_groups, D->r_outrow, D->r_wblob, D->r_cta_woff, D->r_sblob, D->r_cta_soff,
                     D->r_p1_ptr, D->r_p1_list, D->r_p2_ptr, D->r_p2_list, D->bounds, D->send, D->recv, D->vals, D->idx, D->segs, D->p1_segptr, D->p1_rows, D->p1_scale, D->p2_segptr, D->p2_rows,
                     D->perm, D->active, D->g1, D->g2, D->gseg, D->gvo, D->grow1, D->grow2, D->gcsr1, D->gcsr2,
                     D->xt[0], D->xt[1], D->Ep, D->Qp, D->Qdp, D->Qvp, D->Yp, D->Qip,

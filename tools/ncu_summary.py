@@ -53,14 +53,14 @@ def launches(path):
 def full(path):
     out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
-    h = rows[0]
+    h, units = rows[0], dict(zip(rows[0], rows[1]))
     print(f"source: {path}")
     for v in rows[2:]:
         d = dict(zip(h, v))
         print(f"\n== {d.get('Kernel Name', '?')[:120]}")
         for k, label in KEYS:
             if k in d:
-                print(f"  {label:32s} {d[k]}")
+                print(f"  {label:32s} {d[k]} {units.get(k, '')}".rstrip())
         st = [(k, d[k]) for k in h if k.startswith("smsp__average_warps_issue_stalled") and k.endswith("ratio")]
         st = sorted(((float(x.replace(",", "")), k) for k, x in st if x), reverse=True)[:5]
         print("  top stall reasons (warps per issue): " +
