@@ -670,6 +670,9 @@ def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
     if max(chunks) <= 2:
         kern = (f"stream_k1_kernel<{tn}> (bulk-copy chunk stream: phase 1 T = S V^T x, warp-granular grid barrier, "
                 "phase 2 row-owner accumulate)" if stream and max(chunks) == 1 else
+                f"k1p_kernel<{tn}> (pipelined: per-warp cp.async rings of 4-term chunks issued rounds ahead, one "
+                "queue of phase-1 part items then LPT rows, no grid barrier; 16-bit CSR offsets, L2 evict-first)"
+                if info.get("k1_kernel", 0) == 2 else
                 f"hot_kernel<{tn},1,1,M_MATVEC> (phase 1 T = S V^T x, grid barrier, phase 2 row-owner accumulate with "
                 "an LPT row queue; F-hat loads L1::no_allocate + L2 evict-first"
                 + (", 16-bit CSR offsets)" if info.get("k1_payload_bytes", 0) > 0 else ")"))

@@ -270,6 +270,11 @@ typedef struct {
     /* bytes one nrhs = 1 vf_matvec streams in the row layout of hot_kernel
        (values, S, V row indices, 16-bit CSR offsets; 0 if that layout is off) */
     int64_t k1_payload_bytes;
+    /* which kernel runs an nrhs = 1 vf_matvec (fixed at upload; VF_K1_KERNEL env
+       = rows | stream | pipe overrides the build default): 0 = hot_kernel<T,1,1>
+       (row segments), 1 = stream_k1_kernel (chunk stream), 2 = k1p_kernel
+       (pipelined per-warp cp.async rings)                                      */
+    int64_t k1_kernel;
 } vf_info_t;
 
 int vf_info(vf_handle h, vf_info_t* out);

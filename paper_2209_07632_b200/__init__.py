@@ -74,7 +74,7 @@ class vf_info_t(ctypes.Structure):
                 ("groups1", ctypes.c_int64), ("groups2", ctypes.c_int64), ("resident", ctypes.c_int64),
                 ("stream_payload_bytes", ctypes.c_int64), ("stream_meta_bytes", ctypes.c_int64),
                 ("stream_chunks", ctypes.c_int64), ("tiles", ctypes.c_int64), ("tile_sources", ctypes.c_int64),
-                ("k1_payload_bytes", ctypes.c_int64)]
+                ("k1_payload_bytes", ctypes.c_int64), ("k1_kernel", ctypes.c_int64)]
 
 
 _lib = None

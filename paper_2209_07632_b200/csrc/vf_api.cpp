@@ -332,7 +332,7 @@ int vf_info(vf_handle hh, vf_info_t* out) {
     out->visible_pairs = h->visible_pairs;
     out->build_seconds = h->build_seconds;
     out->device = h->dev ? h->device : -1;
-    int64_t ph[16];
+    int64_t ph[17];
     device_phase_info(h, ph);
     out->groups1 = ph[7]; out->groups2 = ph[8];
     out->t_rows = ph[0]; out->p1_bytes = ph[1]; out->p2_bytes = ph[2]; out->p1_src_rows = ph[3];
@@ -340,6 +340,7 @@ int vf_info(vf_handle hh, vf_info_t* out) {
     out->resident = ph[9];
     out->stream_payload_bytes = ph[10]; out->stream_meta_bytes = ph[11]; out->stream_chunks = ph[12];
     out->tiles = ph[13]; out->tile_sources = ph[14]; out->k1_payload_bytes = ph[15];
+    out->k1_kernel = ph[16];
     return VF_OK;
 }
 

@@ -1183,6 +1183,11 @@ __device__ __forceinline__ void res_stage(const int32_t* S, int j0, int n, const
 // FP64 tensor-core MMA (DMMA, mma.sync m8n8k4; FP64 has no tcgen05 kind on
 // sm_100a): D(8x8) += A(8x4, row) B(4x8, col).  Fragments: a = A[lane/4][lane%4],
 // b = B[lane%4][lane/4], d[i] = D[lane/4][2 (lane%4) + i].
+// skip DMMAs whose 8x4 weight fragment is all zero (tile padding, sparse
+// unions of source rows); exact, since such a product leaves D = C
+#ifndef VF_BT_SKIP
+#define VF_BT_SKIP 1
+#endif
 __device__ __forceinline__ void dmma884(double* d, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
                  : "+d"(d[0]), "+d"(d[1])
@@ -1282,10 +1287,21 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
                 const int sw = 4 * kr;                      // (j & 3) == kr: swizzled columns
                 const double a0 = ok ? wb[j * 16 + (mn ^ sw)] : 0.0, a1 = ok ? wb[j * 16 + ((8 + mn) ^ sw)] : 0.0;
                 const double b0 = ok ? X[j * 16 + (mn ^ sw)] : 0.0, b1 = ok ? X[j * 16 + ((8 + mn) ^ sw)] : 0.0;
+#if VF_BT_SKIP
+                if (__any_sync(0xffffffffu, a0 != 0.0)) {       // all-zero fragment: D = C exactly
+                    dmma884(dacc[0], a0, b0);
+                    dmma884(dacc[1], a0, b1);
+                }
+                if (__any_sync(0xffffffffu, a1 != 0.0)) {
+                    dmma884(dacc[2], a1, b0);
+                    dmma884(dacc[3], a1, b1);
+                }
+#else
                 dmma884(dacc[0], a0, b0);
                 dmma884(dacc[1], a0, b1);
                 dmma884(dacc[2], a1, b0);
                 dmma884(dacc[3], a1, b1);
+#endif
             }
         } else if (rr < G.nrows) {
             // 8 independent smem load pairs in flight per thread
@@ -1582,10 +1598,23 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                         const int sw = 4 * kr;
                         const double a0 = W0[j * 16 + (mn ^ sw)], a1 = W0[j * 16 + ((8 + mn) ^ sw)];
                         const double b0 = X0[j * KPB + ((cc + mn) ^ sw)], b1 = X0[j * KPB + ((cc + 8 + mn) ^ sw)];
+#if VF_BT_SKIP
+                        // an all-zero 8x4 weight fragment (rows >= nrows, or no term of these
+                        // 8 rows among these 4 sources) leaves D = C exactly: skip its DMMAs
+                        if (__any_sync(0xffffffffu, a0 != 0.0)) {
+                            dmma884(dacc[0], a0, b0);
+                            dmma884(dacc[1], a0, b1);
+                        }
+                        if (__any_sync(0xffffffffu, a1 != 0.0)) {
+                            dmma884(dacc[2], a1, b0);
+                            dmma884(dacc[3], a1, b1);
+                        }
+#else
                         dmma884(dacc[0], a0, b0);
                         dmma884(dacc[1], a0, b1);
                         dmma884(dacc[2], a1, b0);
                         dmma884(dacc[3], a1, b1);
+#endif
                     }
                     __syncthreads();                               // slot free for the slice kBStages ahead
                 }
@@ -2608,6 +2637,7 @@ struct DeviceHMat {
     uint16_t* idx16 = nullptr;
     int32_t* seg_base16 = nullptr;
     int64_t k1_payload = 0;          // bytes one nrhs = 1 apply streams: values + V indices + u16 CSR offsets
+    int k1_kernel = 0;               // nrhs = 1 kernel chosen at upload: 0 rows (hot_kernel), 1 stream, 2 pipelined (k1p)
     // streamed-tile layout of wide batches on a large F-hat (bt_kernel, FP64)
     bool bt_ok = false;
     BTile* bt_tiles = nullptr;
@@ -3540,6 +3570,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             (rc = up((void**)&D->seg_base16, base16.data(), base16.size() * 4)))
             return rc;
         D->k1_payload = pay16;
+        if (k1_use_pipe()) D->k1_kernel = 2;
         std::vector<Seg>().swap(s16);
         std::vector<uint16_t>().swap(i16);
     }
@@ -4296,7 +4327,7 @@ int apply_k1(Handle* h, void* XT, void* Y, cudaStream_t st) {
         D->last_grid = grid;
         return VF_OK;
     }
-    if (D->idx16 && k1_use_pipe()) return launch_k1p<T>(h, XT, Y, st);
+    if (D->idx16 && D->k1_kernel == 2) return launch_k1p<T>(h, XT, Y, st);
     HotArgs a = hot_args(D, 1, 1);
     a.xt0 = XT;
     a.Y = Y;
@@ -4807,8 +4838,9 @@ int64_t device_alg_flops(const Handle* h) { return h->dev ? h->dev->alg_flops_pe
 int64_t device_active_rows(const Handle* h) { return h->dev ? h->dev->n_p2 : -1; }
 void device_phase_info(const Handle* h, int64_t* out9) {
     const DeviceHMat* D = h->dev;
-    if (!D) { for (int i = 0; i < 16; ++i) out9[i] = 0; return; }
+    if (!D) { for (int i = 0; i < 17; ++i) out9[i] = 0; return; }
     out9[15] = D->k1_payload;
+    out9[16] = D->sl.ok ? 1 : D->idx16 ? D->k1_kernel : 0;
     out9[13] = D->bt_ok ? (int64_t)D->bt_n1 + D->bt_n2 : 0;
     out9[14] = D->bt_ok ? D->bt_cells : 0;
     out9[9] = D->res_ok ? 1 : 0;
