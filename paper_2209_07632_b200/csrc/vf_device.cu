@@ -1900,7 +1900,7 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
 }
 template <typename T>
 __host__ __device__ constexpr size_t k1p_warp_bytes() {
-    return (size_t)kK1pD * 32 * (4 * sizeof(T) + 8 + 8) + (size_t)kK1pD * 4;
+    return ((size_t)kK1pD * 32 * (4 * sizeof(T) + 8 + 8) + (size_t)kK1pD * 4 + 15) & ~(size_t)15;   // 16-B aligned rings
 }
 // descriptor (int2): x = first XT row (runs) or run base (CSR); y = valid terms
 // (0..4) | CSR << 3 | T rows << 4 | aligned vector x << 5 | last round of its row << 6
@@ -3267,15 +3267,18 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     if (use16) {
         const int64_t span16 = getenv("VF_U16_SPAN") ? std::min(65536, std::max(2, atoi(getenv("VF_U16_SPAN")))) : 65536;
         pay16 = D->p1_bytes;                                   // phase 1 unchanged (values, S, V indices)
+        const bool xfirst = k1_use_pipe();
         for (int64_t r = 0; r < (int64_t)p2_rows.size(); ++r) {
-            // X-sourced runs (dense-leaf rows, CSR) first, then the U_b runs over T
-            // rows: the pipelined kernel (k1p_kernel) streams a row's X part while
-            // phase-1 items may still be producing T
-            for (int pass = 0; pass < 2; ++pass)
+            // for the pipelined kernel (k1p_kernel) X-sourced runs (dense-leaf rows,
+            // CSR) first, then the U_b runs over T rows: it streams a row's X part
+            // while phase-1 items may still be producing T.  The other kernels keep
+            // the segment order of the u32 layout (same summation order as the
+            // batched / barrier-free schedules: bitwise equal results)
+            for (int pass = 0; pass < (xfirst ? 2 : 1); ++pass)
             for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1]; ++q) {
                 const Seg sg = segs[q];
                 const bool tsrc = sg.kind == 0 && sg.src >= D->N;
-                if (tsrc != (pass == 1)) continue;
+                if (xfirst && tsrc != (pass == 1)) continue;
                 if (sg.kind == 0) {
                     s16.push_back(sg); base16.push_back(0);
                     pay16 += (int64_t)sizeof(T) * sg.len;
@@ -3570,7 +3573,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             (rc = up((void**)&D->seg_base16, base16.data(), base16.size() * 4)))
             return rc;
         D->k1_payload = pay16;
-        if (k1_use_pipe()) D->k1_kernel = 2;
+        if (xfirst) D->k1_kernel = 2;
         std::vector<Seg>().swap(s16);
         std::vector<uint16_t>().swap(i16);
     }

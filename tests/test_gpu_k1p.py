@@ -89,12 +89,13 @@ sys.path.insert(0, {root!r})
 import oracle, paper_2209_07632_b200 as vf, scenegen as sg
 V, F = sg.cfg3_mesh(n=24, crater_D=1000.0 * 24 / 256)
 S = oracle.Scene(V, F)
-M = vf.ViewFactorMatrix.build(V, F, 1e-5, device=0)
 X = sg.random_rhs(S.N, 1, seed=9)
 Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().T
 res = {{}}
 for kern in ("pipe", "rows"):
-    os.environ["VF_K1_KERNEL"] = kern
+    os.environ["VF_K1_KERNEL"] = kern                 # the nrhs = 1 kernel is chosen at upload
+    M = vf.ViewFactorMatrix.build(V, F, 1e-5, device=0)
+    assert M.refresh()["k1_kernel"] == (2 if kern == "pipe" else 0)
     Y = torch.empty((1, S.N), dtype=torch.float64, device="cuda").T
     M.matvec(Xd, Y)
     res[kern] = Y.cpu().numpy()[:, 0]
