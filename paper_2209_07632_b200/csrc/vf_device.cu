@@ -3573,7 +3573,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             (rc = up((void**)&D->seg_base16, base16.data(), base16.size() * 4)))
             return rc;
         D->k1_payload = pay16;
-        if (xfirst) D->k1_kernel = 2;
+        if (k1_use_pipe()) D->k1_kernel = 2;
         std::vector<Seg>().swap(s16);
         std::vector<uint16_t>().swap(i16);
     }
