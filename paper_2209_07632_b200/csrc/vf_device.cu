@@ -1183,11 +1183,6 @@ __device__ __forceinline__ void res_stage(const int32_t* S, int j0, int n, const
 // FP64 tensor-core MMA (DMMA, mma.sync m8n8k4; FP64 has no tcgen05 kind on
 // sm_100a): D(8x8) += A(8x4, row) B(4x8, col).  Fragments: a = A[lane/4][lane%4],
 // b = B[lane%4][lane/4], d[i] = D[lane/4][2 (lane%4) + i].
-// skip DMMAs whose 8x4 weight fragment is all zero (tile padding, sparse
-// unions of source rows); exact, since such a product leaves D = C
-#ifndef VF_BT_SKIP
-#define VF_BT_SKIP 1
-#endif
 __device__ __forceinline__ void dmma884(double* d, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};\n"
                  : "+d"(d[0]), "+d"(d[1])
@@ -1287,21 +1282,10 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
                 const int sw = 4 * kr;                      // (j & 3) == kr: swizzled columns
                 const double a0 = ok ? wb[j * 16 + (mn ^ sw)] : 0.0, a1 = ok ? wb[j * 16 + ((8 + mn) ^ sw)] : 0.0;
                 const double b0 = ok ? X[j * 16 + (mn ^ sw)] : 0.0, b1 = ok ? X[j * 16 + ((8 + mn) ^ sw)] : 0.0;
-#if VF_BT_SKIP
-                if (__any_sync(0xffffffffu, a0 != 0.0)) {       // all-zero fragment: D = C exactly
-                    dmma884(dacc[0], a0, b0);
-                    dmma884(dacc[1], a0, b1);
-                }
-                if (__any_sync(0xffffffffu, a1 != 0.0)) {
-                    dmma884(dacc[2], a1, b0);
-                    dmma884(dacc[3], a1, b1);
-                }
-#else
                 dmma884(dacc[0], a0, b0);
                 dmma884(dacc[1], a0, b1);
                 dmma884(dacc[2], a1, b0);
                 dmma884(dacc[3], a1, b1);
-#endif
             }
         } else if (rr < G.nrows) {
             // 8 independent smem load pairs in flight per thread
@@ -1598,23 +1582,10 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                         const int sw = 4 * kr;
                         const double a0 = W0[j * 16 + (mn ^ sw)], a1 = W0[j * 16 + ((8 + mn) ^ sw)];
                         const double b0 = X0[j * KPB + ((cc + mn) ^ sw)], b1 = X0[j * KPB + ((cc + 8 + mn) ^ sw)];
-#if VF_BT_SKIP
-                        // an all-zero 8x4 weight fragment (rows >= nrows, or no term of these
-                        // 8 rows among these 4 sources) leaves D = C exactly: skip its DMMAs
-                        if (__any_sync(0xffffffffu, a0 != 0.0)) {
-                            dmma884(dacc[0], a0, b0);
-                            dmma884(dacc[1], a0, b1);
-                        }
-                        if (__any_sync(0xffffffffu, a1 != 0.0)) {
-                            dmma884(dacc[2], a1, b0);
-                            dmma884(dacc[3], a1, b1);
-                        }
-#else
                         dmma884(dacc[0], a0, b0);
                         dmma884(dacc[1], a0, b1);
                         dmma884(dacc[2], a1, b0);
                         dmma884(dacc[3], a1, b1);
-#endif
                     }
                     __syncthreads();                               // slot free for the slice kBStages ahead
                 }
