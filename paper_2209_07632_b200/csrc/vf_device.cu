@@ -525,6 +525,126 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
     return acc;
 }
 
+// nrhs = 1 matvec rows (16-bit CSR layout) with the NEXT round's F-hat chunk
+// prefetched into registers: round = one 4-term chunk per lane.  In
+// row_accumulate_k1 a round costs the HBM latency of its values/offsets PLUS
+// the latency of the x gathers that depend on them; here the loads of round
+// i + 1 are issued before the gathers of round i, so the two overlap.  Same
+// lane -> chunk mapping and FMA order as row_accumulate_k1 (bitwise equal).
+#ifndef VF_K1_PF
+#define VF_K1_PF 1
+#endif
+template <typename T>
+struct K1Round {
+    T w[4];
+    uint2 q;            // 16-bit CSR offsets of the 4 terms (CSR runs)
+    int32_t xb;         // first XT row (runs) or run base (CSR)
+    int32_t f;          // valid terms (0..4) | CSR << 3 | vector x << 4 | X rows (L1) << 5
+};
+template <typename T>
+__device__ __forceinline__ void k1_fetch(K1Round<T>& R, int cc, int ns, int total, int excl, const Seg& my, int32_t my_base,
+                                         const T* __restrict__ vals, const uint16_t* __restrict__ idx16, int64_t nx,
+                                         int lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    int g = 0;
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+        const int cand = g + step;
+        const int e = __shfl_sync(FULL, excl, cand & 31);
+        if (cand < ns && e <= cc) g = cand;
+    }
+    const int64_t g_off = __shfl_sync(FULL, my.val_off, g);
+    const int64_t g_src = __shfl_sync(FULL, my.src, g);
+    const int g_len = __shfl_sync(FULL, my.len, g);
+    const int g_kind = __shfl_sync(FULL, my.kind, g);
+    const int g_excl = __shfl_sync(FULL, excl, g);
+    const int g_base = __shfl_sync(FULL, my_base, g);
+    if (cc < total) {
+        const int e = (cc - g_excl) * 4;
+        const int nv = min(4, g_len - e);
+        V4<T>::ld(vals + g_off + e, R.w);
+        if (g_kind) {
+            R.q = ld_stream_u2(reinterpret_cast<const uint2*>(idx16 + g_src + e));
+            R.xb = g_base;
+            R.f = nv | 8 | 32;
+        } else {
+            R.q = make_uint2(0u, 0u);
+            R.xb = (int32_t)(g_src + e);
+            R.f = nv | (VF_XVEC && nv == 4 && ((g_src + e) & (16 / sizeof(T) - 1)) == 0 ? 16 : 0) | (g_src < nx ? 32 : 0);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) R.w[u] = T(0);
+        R.q = make_uint2(0u, 0u);
+        R.xb = 0;
+        R.f = 32;
+    }
+}
+template <typename T>
+__device__ __forceinline__ void k1_consume(const K1Round<T>& R, const T* xt, T& acc0, T& acc1) {
+    const int nv = R.f & 7;
+    T x[4];
+    if (R.f & 8) {
+        const int o[4] = {(int)(R.q.x & 0xffffu), (int)(R.q.x >> 16), (int)(R.q.y & 0xffffu), (int)(R.q.y >> 16)};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) x[u] = XLD(xt + R.xb + (u < nv ? o[u] : 0));
+    } else if (R.f & 32) {                               // X rows (read-only in a matvec): through L1
+        if (R.f & 16) XV4<T, true>::ld(xt + R.xb, x);
+        else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = XLD(xt + R.xb + (u < nv ? u : 0));
+        }
+    } else {                                             // T rows (written by phase 1 of this launch): L2
+        if (R.f & 16) XV4<T, false>::ld(xt + R.xb, x);
+        else {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) x[u] = __ldcg(xt + R.xb + (u < nv ? u : 0));
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const T wu = u < nv ? R.w[u] : T(0);
+        if (u & 1) acc1 = fma(wu, x[u], acc1);
+        else acc0 = fma(wu, x[u], acc0);
+    }
+}
+template <typename T>
+__device__ __forceinline__ T row_accumulate_k1_pf(const Seg* __restrict__ segs, int64_t s0, int64_t s1,
+                                                  const T* __restrict__ vals, const T* xt, int lane, int64_t nx,
+                                                  const uint16_t* __restrict__ idx16,
+                                                  const int32_t* __restrict__ seg_base) {
+    constexpr unsigned FULL = 0xffffffffu;
+    T acc0 = T(0), acc1 = T(0);
+    for (int64_t sb = s0; sb < s1; sb += 32) {
+        const int ns = (int)(s1 - sb < 32 ? s1 - sb : 32);
+        Seg my{0, 0, 0, 0};
+        int32_t my_base = 0;
+        if (lane < ns) { my = segs[sb + lane]; my_base = seg_base[sb + lane]; }
+        const int nch = (my.len + 3) >> 2;
+        int incl = nch;
+#pragma unroll
+        for (int off = 1; off < 32; off <<= 1) {
+            const int v = __shfl_up_sync(FULL, incl, off);
+            if (lane >= off) incl += v;
+        }
+        const int excl = incl - nch;
+        const int total = __shfl_sync(FULL, incl, 31);
+        K1Round<T> cur;
+        k1_fetch<T>(cur, lane, ns, total, excl, my, my_base, vals, idx16, nx, lane);
+        for (int base = 32; base < total; base += 32) {          // warp-uniform
+            K1Round<T> nxt;
+            k1_fetch<T>(nxt, base + lane, ns, total, excl, my, my_base, vals, idx16, nx, lane);
+            k1_consume<T>(cur, xt, acc0, acc1);
+            cur = nxt;
+        }
+        k1_consume<T>(cur, xt, acc0, acc1);
+    }
+    T acc = acc0 + acc1;
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(FULL, acc, off);
+    return acc;
+}
+
 // nrhs = 1, wave-interleaved (VF_K1_WAVE): lane l takes terms base + l of a
 // row's concatenated segments, so one gather instruction touches 32
 // CONSECUTIVE terms -- consecutive CSR columns / contiguous x runs -- i.e. a
@@ -894,6 +1014,8 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
             if (lane == 0) fut = atomicAdd(a.qctr, 1);
             const T acc = (VF_K1_WAVE_DEFAULT && a.idx16) ? row_accumulate_wave<T>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
                                                                        vals, a.idx16, a.seg_base16, xc, lane)
+                        : (VF_K1_PF && a.idx16) ? row_accumulate_k1_pf<T>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
+                                                                           vals, xc, lane, a.N, a.idx16, a.seg_base16)
                         : a.idx16 ? row_accumulate_k1<T, VF_MV_L1 != 0>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
                                                                          vals, a.idx, xc, lane, a.N, nullptr, nullptr,
                                                                          a.idx16, a.seg_base16)
@@ -1481,6 +1603,9 @@ __global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) 
 // phase 2); each output element is summed by one warp in a fixed order and
 // K-parts are added in part order: bitwise reproducible.
 constexpr int kBCols = 128;         // columns per pass over a tile
+#ifndef VF_BT_ACC2
+#define VF_BT_ACC2 0
+#endif
 #ifndef VF_BT_STAGES
 #define VF_BT_STAGES 4
 #endif
@@ -1561,6 +1686,9 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                     }
                 };
                 double dacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#if VF_BT_ACC2
+                double dacc2[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
+#endif
                 int32_t rg[4];
 #pragma unroll
                 for (int p = 0; p < kBStages - 1; ++p) {
@@ -1577,7 +1705,30 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                     const double* W0 = Wsm + (sl % kBStages) * KS * 16;
                     const double* X0 = Xsm + (sl % kBStages) * KS * KPB;
                     const int cc = cw * 16;
+#if VF_BT_ACC2
+                    // two accumulator sets (even / odd k-steps of the part): 8 independent
+                    // DMMA chains per warp instead of 4; the sets are added at the item end
+                    int ks = pw;
+                    for (; ks + nkp < KS / 4; ks += 2 * nkp) {
+                        const int sw = 4 * kr;
+                        const int j = ks * 4 + kr, j2 = (ks + nkp) * 4 + kr;
+                        const double a0 = W0[j * 16 + (mn ^ sw)], a1 = W0[j * 16 + ((8 + mn) ^ sw)];
+                        const double b0 = X0[j * KPB + ((cc + mn) ^ sw)], b1 = X0[j * KPB + ((cc + 8 + mn) ^ sw)];
+                        const double c0 = W0[j2 * 16 + (mn ^ sw)], c1 = W0[j2 * 16 + ((8 + mn) ^ sw)];
+                        const double e0 = X0[j2 * KPB + ((cc + mn) ^ sw)], e1 = X0[j2 * KPB + ((cc + 8 + mn) ^ sw)];
+                        dmma884(dacc[0], a0, b0);
+                        dmma884(dacc[1], a0, b1);
+                        dmma884(dacc[2], a1, b0);
+                        dmma884(dacc[3], a1, b1);
+                        dmma884(dacc2[0], c0, e0);
+                        dmma884(dacc2[1], c0, e1);
+                        dmma884(dacc2[2], c1, e0);
+                        dmma884(dacc2[3], c1, e1);
+                    }
+                    for (; ks < KS / 4; ks += nkp) {
+#else
                     for (int ks = pw; ks < KS / 4; ks += nkp) {
+#endif
                         const int j = ks * 4 + kr;
                         const int sw = 4 * kr;
                         const double a0 = W0[j * 16 + (mn ^ sw)], a1 = W0[j * 16 + ((8 + mn) ^ sw)];
@@ -1590,6 +1741,10 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                     __syncthreads();                               // slot free for the slice kBStages ahead
                 }
                 cpa_wait<0>();
+#if VF_BT_ACC2
+#pragma unroll
+                for (int tl = 0; tl < 4; ++tl) { dacc[tl][0] += dacc2[tl][0]; dacc[tl][1] += dacc2[tl][1]; }
+#endif
                 // K-parts of a column chunk meet in smem, added in part order
                 double* red = bsm + kBStages * kBSlice;            // [8 warps][4 tiles][32 lanes][2]
                 if (nkp > 1) {
