@@ -2572,6 +2572,81 @@ __global__ void rows_decide_kernel(Ctl* ctl, const unsigned char* recv, int64_t 
     }
 }
 
+// ---- column-split Jacobi iteration (1..8 columns on a large F-hat): each
+// column's F-hat product goes through the nrhs = 1 apply (one F-hat stream per
+// column at the HBM-bound kernel's rate) instead of one batched launch whose
+// kp = 2..8 kernels stream F-hat far below it.  Same iteration as the
+// persistent solve (A13: B_0 = E, B_{k+1} = E + rho clamp(F-hat B_k), r_c =
+// ||B_{k+1} - B_k|| / ||E_c||, stop when all r_c <= tol or at iters).
+template <typename T>
+__global__ void col_gather_kernel(const T* __restrict__ xc, int64_t N, int kp, int c, T* __restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = xc[i * kp + c];
+}
+// a4 epilogue of all columns: thread per active tree row; CTA b owns rows
+// [b R, (b + 1) R); per-column (B' - B)^2 summed in a fixed order (thread
+// order within warps by shuffles, then warps in order) into partial[c][b]
+template <typename T>
+__global__ void __launch_bounds__(256) cols_epilogue_kernel(const T* __restrict__ Y, const T* __restrict__ E,
+                                                            const T* xc, T* xn, T* Q, const T* __restrict__ rho,
+                                                            const uint8_t* __restrict__ active, int64_t N, int k,
+                                                            int kp, int clamp, int64_t R, double* partial) {
+    __shared__ double sw[8][8];
+    double d2[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) d2[c] = 0.0;
+    const int64_t r0 = (int64_t)blockIdx.x * R, r1 = min(N, r0 + R);
+    for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+        if (!active[r]) continue;
+        const T rh = rho ? rho[r] : T(1);
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+            if (c >= k) break;
+            T acc = Y[(int64_t)c * N + r];
+            if (clamp) acc = acc > T(0) ? acc : T(0);
+            const int64_t o = r * kp + c;
+            const T bn = E[o] + rh * acc;
+            const double d = (double)bn - (double)xc[o];
+            d2[c] += d * d;
+            xn[o] = bn;
+            Q[o] = acc;
+        }
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) d2[c] += __shfl_xor_sync(0xffffffffu, d2[c], off);
+        if (lane == 0) sw[c][warp] = d2[c];
+    }
+    __syncthreads();
+    if (threadIdx.x < k) {
+        double sum = 0.0;
+        for (int w = 0; w < 8; ++w) sum += sw[threadIdx.x][w];
+        partial[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = sum;
+    }
+}
+__global__ void cols_decide_kernel(Ctl* ctl, const double* partial, int nblk, int k, const double* enorm2,
+                                   double* resid, double tol, int iters) {
+    __shared__ int bad;
+    if (threadIdx.x == 0) bad = 0;
+    __syncthreads();
+    for (int c = threadIdx.x; c < k; c += blockDim.x) {
+        double sum = 0.0;
+        for (int b = 0; b < nblk; ++b) sum += partial[(int64_t)c * nblk + b];
+        const double en = enorm2[c];
+        const double rr = en > 0.0 ? sqrt(sum) / sqrt(en) : 0.0;
+        resid[c] = rr;
+        if (!(rr <= tol)) atomicOr(&bad, 1);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int it = ctl->iter + 1;
+        ctl->iter = it;
+        if (!bad || it >= iters) ctl->done = 1;
+    }
+}
+
 // ---- Alg. 6 time stepping (NEXT-1).  State in tree
 // order, row-major [r][c] over the nscen scenarios; column profiles
 // layer-major [j][r][c] (coalesced over r, c).
@@ -2712,6 +2787,7 @@ struct DeviceHMat {
     void* Yp = nullptr;       // matvec result / T (tree)
     void* Qip = nullptr;      // Qir (tree)
     void* pv[3] = {nullptr, nullptr, nullptr};   // rho/alpha, emis (tree), spare
+    void* xcol = nullptr;     // column-split solves: one iterate column + its T rows, (N + NT) x 1
     double* partial = nullptr;
     double* enorm2 = nullptr;
     double* resid = nullptr;
@@ -4391,6 +4467,59 @@ int iterate_rows(Handle* h, int k, int kp, const void* rho, int clamp, int iters
 // One Jacobi stage.  Persistent path: statistics are deferred to slot and
 // read by stage_stats after the caller's final synchronisation (*deferred =
 // true); ROWS path: synchronous, statistics returned directly.
+// column-split solve (see cols_epilogue_kernel): used for 1..8 columns on a
+// large F-hat (device layout > 256 MB, the matvec column rule) with the 16-bit
+// nrhs = 1 layout; VF_SOLVE_COLSPLIT=1/0 forces it on/off.  The host reads the
+// stop flag after every iteration (one small copy + sync per F-hat stream of
+// k x ~0.9 ms on configs[2]).
+template <typename T>
+int apply_k1(Handle* h, void* XT, void* Y, cudaStream_t st);
+bool use_cols_solve(const Handle* h, int k) {
+    const DeviceHMat* D = h->dev;
+    if (D->world > 1 || h->comm || k > 8 || !D->idx16) return false;
+    const char* e = getenv("VF_SOLVE_COLSPLIT");
+    if (e) return atoi(e) != 0;
+    return D->bytes > ((int64_t)256 << 20);
+}
+template <typename T>
+int iterate_cols(Handle* h, int k, int kp, const void* rho, int clamp, int iters, double tol, cudaStream_t st,
+                 int* iters_done, double* max_resid) {
+    DeviceHMat* D = h->dev;
+    *iters_done = 0;
+    *max_resid = 0;
+    if (iters <= 0) return VF_OK;
+    if (!D->xcol) CK(cudaMalloc(&D->xcol, (size_t)(D->N + D->NT) * D->w));
+    CK(cudaMemsetAsync(D->ctl, 0, sizeof(Ctl), st));
+    const int64_t N = D->N;
+    const int nblk = (int)std::min<int64_t>(148 * 4, std::max<int64_t>(1, (N + 255) / 256));
+    const int64_t R = (N + nblk - 1) / nblk;
+    const int gg = (int)std::min<int64_t>(148 * 4, (N + 255) / 256);
+    for (int it = 0; it < iters; ++it) {
+        const T* xc = (const T*)D->xt[it & 1];
+        T* xn = (T*)D->xt[(it & 1) ^ 1];
+        for (int c = 0; c < k; ++c) {
+            col_gather_kernel<T><<<gg, 256, 0, st>>>(xc, N, kp, c, (T*)D->xcol);
+            h->launches_total++;
+            int rc = apply_k1<T>(h, D->xcol, (T*)D->Yp + (size_t)c * N, st);
+            if (rc) return rc;
+        }
+        cols_epilogue_kernel<T><<<nblk, 256, 0, st>>>((const T*)D->Yp, (const T*)D->Ep, xc, xn, (T*)D->Qp, (const T*)rho,
+                                                       D->active, N, k, kp, clamp, R, D->partial);
+        cols_decide_kernel<<<1, 256, 0, st>>>(D->ctl, D->partial, nblk, k, D->enorm2, D->resid, tol, iters);
+        h->launches_total += 2;
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(D->ctl_host, D->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (D->ctl_host->done) break;
+    }
+    CK(cudaMemcpyAsync(D->resid_host, D->resid, (size_t)k * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *iters_done = D->ctl_host->iter;
+    double mr = 0;
+    for (int c = 0; c < k; ++c) mr = std::max(mr, D->resid_host[c]);
+    *max_resid = mr;
+    return VF_OK;
+}
 template <typename T>
 int solve_stage(Handle* h, int k, int kp, const void* rho, int clamp, int iters, double tol, cudaStream_t st,
                 int slot, int* iters_done, double* max_resid, bool* deferred) {
@@ -4399,6 +4528,10 @@ int solve_stage(Handle* h, int k, int kp, const void* rho, int clamp, int iters,
     if (h->dev->world > 1 || h->comm) {
         *deferred = false;
         return iterate_rows<T>(h, k, kp, rho, clamp, iters, tol, st, iters_done, max_resid);
+    }
+    if (use_cols_solve(h, k)) {
+        *deferred = false;
+        return iterate_cols<T>(h, k, kp, rho, clamp, iters, tol, st, iters_done, max_resid);
     }
     *deferred = true;
     return iterate<T>(h, k, kp, rho, clamp, iters, tol, st, slot);
@@ -4697,7 +4830,7 @@ void device_free(Handle* h) {
                     D->r_p1_ptr, D->r_p1_list, D->r_p2_ptr, D->r_p2_list, D->bounds, D->send, D->recv, D->vals, D->idx, D->segs, D->p1_segptr, D->p1_rows, D->p1_scale, D->p2_segptr, D->p2_rows,
                     D->perm, D->active, D->g1, D->g2, D->gseg, D->gvo, D->grow1, D->grow2, D->gcsr1, D->gcsr2,
                     D->xt[0], D->xt[1], D->Ep, D->Qp, D->Qdp, D->Qvp, D->Yp, D->Qip,
-                    D->pv[0], D->pv[1], D->pv[2], D->partial, D->enorm2, D->resid, D->ctl,
+                    D->pv[0], D->pv[1], D->pv[2], D->xcol, D->partial, D->enorm2, D->resid, D->ctl,
                     D->stage[0], D->stage[1], D->stage[2], D->stage[3], D->stage[4], D->stage[5]};
     for (void* p : ptrs) if (p) cudaFree(p);
     if (D->ctl_host) cudaFreeHost(D->ctl_host);

@@ -441,3 +441,49 @@ def test_wide_batch_chunks_equal_separate_applies(rough, tmp_path_factory, monke
         c0 += n
     assert np.array_equal(host(Y), np.concatenate(parts, axis=1))
     assert rel(host(Y), hm.hmatvec(H, X)) <= 1e-12
+
+
+@pytest.mark.parametrize("k", [1, 3, 8])
+def test_column_split_solves_same_blocks(cap, rough, tmp_path_factory, monkeypatch, k):
+    """Column-split Jacobi (1..8 columns on a large F-hat: each column's product
+    through the nrhs = 1 apply, one epilogue/decision launch per iteration;
+    forced here with VF_SOLVE_COLSPLIT=1 on small meshes) against the oracle's
+    Jacobi / thermal chain on the same blocks: <= 1e-12 with identical
+    iteration counts (A13), and against the persistent batched solve."""
+    for which in ("cap", "rough"):
+        V, F, S, Fd = cap if which == "cap" else rough
+        H, M = oracle_handle(S, Fd, tmp_path_factory, 1e-6, "f64", 2048, "cs" + which)
+        rng = np.random.default_rng(21)
+        E = np.asfortranarray(1000 * rng.random((S.N, k)))
+        E[: S.N // 7, 0] = 0.0                                  # shadowed facets
+        rho = (0.05 + 0.9 * rng.random(S.N)) / max(1.0, np.abs(Fd).sum(1).max())
+        B0, Q0, it0, r0 = oracle.jacobi(lambda X: hm.hmatvec(H, X), E, rho, 1e-13, 200)
+        res = {}
+        for mode in ("1", "0"):
+            monkeypatch.setenv("VF_SOLVE_COLSPLIT", mode)
+            B = empty(S.N, k)
+            M.solve_radiosity(dev(E), dev(rho), B, iters=200, tol=1e-13)
+            res[mode] = (host(B), M.stats()["iters1"])
+        assert res["1"][1] == it0 == res["0"][1]
+        assert rel(res["1"][0], B0) <= 1e-12
+        assert rel(res["1"][0], res["0"][0]) <= 1e-13
+    V, F, S, Fd = cap
+    H, M = oracle_handle(S, Fd, tmp_path_factory, 1e-5, "f64", 16384, "csth")
+    Q = S.insolation(sg.sun_dirs(10.0, k, 0.1))
+    alb, emi = np.full(S.N, 0.12), np.full(S.N, 0.95)
+    ref = oracle.thermal(lambda X: hm.hmatvec(H, X), Q, alb, emi, 1e-12, 100)
+    monkeypatch.setenv("VF_SOLVE_COLSPLIT", "1")
+    T, Qv, Qi = empty(S.N, k), empty(S.N, k), empty(S.N, k)
+    M.solve_thermal(dev(Q), dev(alb), dev(emi), T, Qv, Qi, iters=100, tol=1e-12)
+    st = M.stats()
+    assert (st["iters1"], st["iters2"]) == (ref["it1"], ref["it2"])
+    for a, b in ((Qv, ref["Qvis"]), (Qi, ref["Qir"]), (T, ref["T"])):
+        assert rel(host(a), b) <= 1e-12
+    # no convergence within iters: ENOCONV, B holds the last iterate
+    E2 = np.asfortranarray(np.random.default_rng(1).random((S.N, k)))
+    B0, *_ = oracle.jacobi(lambda X: hm.hmatvec(H, X), E2, np.full(S.N, 0.9), 1e-300, 2)
+    B = empty(S.N, k)
+    with pytest.raises(vf.VFError) as e:
+        M.solve_radiosity(dev(E2), dev(np.full(S.N, 0.9)), B, iters=2, tol=1e-300)
+    assert e.value.code == vf.VF_ENOCONV
+    assert rel(host(B), B0) <= 1e-12
