@@ -2839,7 +2839,8 @@ struct DeviceHMat {
     uint16_t* idx16 = nullptr;
     int32_t* seg_base16 = nullptr;
     int64_t k1_payload = 0;          // bytes one nrhs = 1 apply streams: values + V indices + u16 CSR offsets
-    int k1_kernel = 0;               // nrhs = 1 kernel chosen at upload: 0 rows (hot_kernel), 1 stream, 2 pipelined (k1p)
+    int k1_kernel = 0;
+    int res_p2copies = 0;            // copies of each phase-2 group in the resident layout (column chunks split)               // nrhs = 1 kernel chosen at upload: 0 rows (hot_kernel), 1 stream, 2 pipelined (k1p)
     // streamed-tile layout of wide batches on a large F-hat (bt_kernel, FP64)
     bool bt_ok = false;
     BTile* bt_tiles = nullptr;
@@ -3587,12 +3588,13 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             int phase; int64_t g; int64_t K; std::vector<int32_t> ucols; int ch0 = 0, chstep = 1;
             int role = -1; int64_t kb = 0;                 // K-half [kb, kb + K) of a split group
         };
-        std::vector<HG> hg;
-        // phase-1 groups are few and short: each is replicated kP1Copies times so
-        // that its column chunks run on different SMs (copy i takes chunks i, i + kP1Copies, ...)
-        const int kP1Copies = 4;
-        for (int64_t g = 0; g < (int64_t)g1v.size(); ++g)
-            for (int cpy = 0; cpy < kP1Copies; ++cpy) hg.push_back({1, g, gsegv[g1v[g].seg_off].len, {}, cpy, kP1Copies});
+        // phase-2 groups are replicated like the phase-1 groups when the copies fit
+        // the SMs' shared memory (4, else 2, else 1 copy; VF_RES_P2COPIES forces a
+        // count): with ~ as many groups as SMs (cfg2: 125 on 148) one CTA per group
+        // ran all its column chunks in sequence while other SMs idled
+        const char* p2e = getenv("VF_RES_P2COPIES");
+        std::vector<int> p2try = p2e ? std::vector<int>{std::max(1, atoi(p2e))} : std::vector<int>{4, 2, 1};
+        std::vector<HG> hg2base;
         for (int64_t g = 0; g < (int64_t)g2v.size(); ++g) {
             HG x{2, g, 0, {}, 0, 1};
             for (int q = 0; q < g2v[g].nseg; ++q) x.K += gsegv[g2v[g].seg_off + q].len;
@@ -3604,8 +3606,23 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             std::sort(x.ucols.begin(), x.ucols.end());
             x.ucols.erase(std::unique(x.ucols.begin(), x.ucols.end()), x.ucols.end());
             x.K += (int64_t)x.ucols.size();
-            hg.push_back(std::move(x));
+            hg2base.push_back(std::move(x));
         }
+      for (size_t attempt = 0; attempt < p2try.size(); ++attempt) {
+        const int p2c = p2try[attempt];
+        std::vector<HG> hg;
+        // phase-1 groups are few and short: each is replicated kP1Copies times so
+        // that its column chunks run on different SMs (copy i takes chunks i, i + kP1Copies, ...)
+        const int kP1Copies = 4;
+        for (int64_t g = 0; g < (int64_t)g1v.size(); ++g)
+            for (int cpy = 0; cpy < kP1Copies; ++cpy) hg.push_back({1, g, gsegv[g1v[g].seg_off].len, {}, cpy, kP1Copies});
+        for (const HG& x0 : hg2base)
+            for (int cpy = 0; cpy < p2c; ++cpy) {
+                HG x = x0;
+                x.ch0 = cpy;
+                x.chstep = p2c;
+                hg.push_back(std::move(x));
+            }
         // phase-2 groups with a long K can be split over the two CTAs of a cluster
         // pair (K halves; rank 1 sends its partial tile to rank 0 through DSMEM).
         // Opt-in (VF_RES_SPLIT=1): with about as many groups as SMs (cfg2: 125 on
@@ -3635,6 +3652,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         bool ok = budget > 0 && !hg.empty();
         std::vector<int> owner(hg.size(), -1);
         std::vector<int64_t> used(nsm, 0), load1(nsm, 0), load2(nsm, 0);
+        std::vector<int> ngrp(nsm, 0);                      // <= 64 group descriptors per CTA (in `fixed`)
         if (ok) {
             std::vector<size_t> ord(hg.size());
             std::iota(ord.begin(), ord.end(), 0);
@@ -3646,11 +3664,12 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                 const int64_t n0 = need(hg[q]), n1 = need(hg[q + 1]);
                 int best = -1;
                 for (int c = 0; c + 1 < nsm; c += 2)
-                    if (used[c] + n0 <= budget && used[c + 1] + n1 <= budget &&
+                    if (used[c] + n0 <= budget && used[c + 1] + n1 <= budget && ngrp[c] < 64 && ngrp[c + 1] < 64 &&
                         (best < 0 || load2[c] + load2[c + 1] < load2[best] + load2[best + 1]))
                         best = c;
                 if (best < 0) { ok = false; break; }
                 owner[q] = best; owner[q + 1] = best + 1;
+                ++ngrp[best]; ++ngrp[best + 1];
                 used[best] += n0; used[best + 1] += n1;
                 load2[best] += hg[q].K * (int64_t)(kGroup + 1) + 256;
                 load2[best + 1] += hg[q + 1].K * (int64_t)(kGroup + 1) + 256;
@@ -3662,9 +3681,10 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                 std::vector<int64_t>& ld = hg[q].phase == 1 ? load1 : load2;
                 int best = -1;
                 for (int c = 0; c < nsm; ++c)
-                    if (used[c] + nb <= budget && (best < 0 || ld[c] < ld[best])) best = c;
+                    if (used[c] + nb <= budget && ngrp[c] < 64 && (best < 0 || ld[c] < ld[best])) best = c;
                 if (best < 0) { ok = false; break; }
                 owner[q] = best;
+                ++ngrp[best];
                 used[best] += nb;
                 ld[best] += hg[q].K * (int64_t)(kGroup + 1) / hg[q].chstep + 256;   // time ~ K x chunks taken
             }
@@ -3766,7 +3786,10 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             D->res_grid = nsm;
             D->res_wcap = (int)std::max<int64_t>(wmax, EPL);
             D->res_scap = (int)std::max<int64_t>(smax, 4);
+            D->res_p2copies = p2c;
         }
+        if (ok) break;
+      }
     }
     if (use16 && !s16.empty()) {
         if ((rc = up((void**)&D->segs16, s16.data(), s16.size() * sizeof(Seg))) ||

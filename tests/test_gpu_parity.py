@@ -487,3 +487,35 @@ def test_column_split_solves_same_blocks(cap, rough, tmp_path_factory, monkeypat
         M.solve_radiosity(dev(E2), dev(np.full(S.N, 0.9)), B, iters=2, tol=1e-300)
     assert e.value.code == vf.VF_ENOCONV
     assert rel(host(B), B0) <= 1e-12
+
+
+@pytest.mark.parametrize("k", [16, 64])
+def test_resident_phase2_copies(cfg2_small, tmp_path_factory, monkeypatch, k):
+    """Resident layout with each phase-2 group replicated over 1, 2 or 4 CTAs
+    (copy i takes the column chunks i, i + copies, ...; VF_RES_P2COPIES): every
+    output element is still summed by one CTA in the same order, so the matvec
+    is bitwise identical across copy counts, and the solves match the oracle
+    with identical iteration counts."""
+    V, F, S, Fd = cfg2_small
+    H = hm.compress(S.x, Fd, 1e-6, min_size=2048)
+    p = str(tmp_path_factory.mktemp("p2c") / f"c{k}.hvfm")
+    hm.write_hvfm(H, p)
+    X = sg.random_rhs(S.N, k, seed=6)
+    rng = np.random.default_rng(4)
+    E = np.asfortranarray(100 * rng.random((S.N, k)))
+    rho = np.full(S.N, 0.5 / max(1.0, np.abs(Fd).sum(1).max()))
+    B0, _, it0, _ = oracle.jacobi(lambda Z: hm.hmatvec(H, Z), E, rho, 1e-13, 200)
+    ys = []
+    for copies in ("1", "2", "4"):
+        monkeypatch.setenv("VF_RES_P2COPIES", copies)
+        M = vf.ViewFactorMatrix.load(p, device=0)
+        assert M.refresh()["resident"] == 1
+        Y = empty(S.N, k)
+        M.matvec(dev(X), Y)
+        ys.append(host(Y))
+        B = empty(S.N, k)
+        M.solve_radiosity(dev(E), dev(rho), B, iters=200, tol=1e-13)
+        assert M.stats()["iters1"] == it0
+        assert rel(host(B), B0) <= 1e-12
+    assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2])
+    assert rel(ys[0], hm.hmatvec(H, X)) <= 1e-12
