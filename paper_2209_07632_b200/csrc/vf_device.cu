@@ -534,6 +534,9 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
 #ifndef VF_K1_PF
 #define VF_K1_PF 1
 #endif
+#ifndef VF_K1_ROWPF
+#define VF_K1_ROWPF 1       // row descriptors pipelined over three rows (phase2_rows)
+#endif
 template <typename T>
 struct K1Round {
     T w[4];
@@ -608,11 +611,30 @@ __device__ __forceinline__ void k1_consume(const K1Round<T>& R, const T* xt, T& 
         else acc0 = fma(wu, x[u], acc0);
     }
 }
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+    int v;
+    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// barrier-free matvec: before the first round that reads T rows, wait until all
+// phase-1 items have finished (every item is owned by a running warp of this
+// co-resident grid that waits on nothing before it, so the wait ends)
+__device__ __forceinline__ void k1_wait_t(const int32_t* p1done, int32_t n, int lane) {
+    if (lane == 0) {
+        unsigned long long spins = 0;
+        while (ld_acquire_gpu(p1done) < n) {
+            __nanosleep(64);
+            if (++spins > (1ull << 26)) __trap();
+        }
+    }
+    __syncwarp();
+}
 template <typename T>
 __device__ __forceinline__ T row_accumulate_k1_pf(const Seg* __restrict__ segs, int64_t s0, int64_t s1,
                                                   const T* __restrict__ vals, const T* xt, int lane, int64_t nx,
                                                   const uint16_t* __restrict__ idx16,
-                                                  const int32_t* __restrict__ seg_base) {
+                                                  const int32_t* __restrict__ seg_base, const int32_t* p1done,
+                                                  int32_t n_p1, bool& t_ready) {
     constexpr unsigned FULL = 0xffffffffu;
     T acc0 = T(0), acc1 = T(0);
     for (int64_t sb = s0; sb < s1; sb += 32) {
@@ -634,9 +656,11 @@ __device__ __forceinline__ T row_accumulate_k1_pf(const Seg* __restrict__ segs, 
         for (int base = 32; base < total; base += 32) {          // warp-uniform
             K1Round<T> nxt;
             k1_fetch<T>(nxt, base + lane, ns, total, excl, my, my_base, vals, idx16, nx, lane);
+            if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
             k1_consume<T>(cur, xt, acc0, acc1);
             cur = nxt;
         }
+        if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
         k1_consume<T>(cur, xt, acc0, acc1);
     }
     T acc = acc0 + acc1;
@@ -837,6 +861,10 @@ struct HotArgs {
     const int32_t* seg_blk;
     const int32_t* g1_blk;
     int32_t* qctr;
+    // nrhs = 1 matvec without the phase barrier (u16 layout, X-sourced runs first
+    // in every row): phase-1 part items finished, and how many there are
+    int32_t* p1done;
+    int32_t n_p1items;
     const int32_t* p2_order;
     // nrhs = 1 matvec rows with 16-bit CSR offsets (optional; upload_impl)
     const Seg* segs16;
@@ -893,7 +921,14 @@ template <typename T>
 __device__ __forceinline__ void phase1_part_k1(const HotArgs& a, T* xc, int64_t pi, int lane);
 template <typename T>
 __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_t gwarp, int lane) {
-    for (int32_t q = a.s1_ptr[gwarp]; q < a.s1_ptr[gwarp + 1]; ++q) phase1_part_k1<T>(a, xc, a.s1_items[q], lane);
+    for (int32_t q = a.s1_ptr[gwarp]; q < a.s1_ptr[gwarp + 1]; ++q) {
+        phase1_part_k1<T>(a, xc, a.s1_items[q], lane);
+        if (a.p1done) {                               // release: this item's T rows (or part sums) are written
+            __threadfence();
+            __syncwarp();
+            if (lane == 0) atomicAdd(a.p1done, 1);
+        }
+    }
 }
 // one phase-1 part item pi: (row group of one SVD block, part of its V rows)
 template <typename T>
@@ -1005,6 +1040,38 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
         // nrhs = 1 matvec: rows from a global queue in LPT order (dynamic
         // balance; each row is still summed by one warp in a fixed order);
         // the next ticket is fetched while the current row streams
+        bool t_ready = a.p1done == nullptr;           // with the phase barrier T rows are ready
+#if VF_K1_PF && VF_K1_ROWPF
+        if (a.idx16 && !VF_K1_WAVE_DEFAULT) {
+            // row descriptors software-pipelined over three rows: at the start of
+            // row A the warp already holds B's segment range and output row, issues
+            // the load of C's tree row (ticket fetched one row earlier) and the
+            // ticket of D -- a row start then waits only for its first segment batch
+            const int64_t n2 = a.n_p2;
+            int tA = 0, tB = 0;
+            if (lane == 0) { tA = atomicAdd(a.qctr, 1); tB = atomicAdd(a.qctr, 1); }
+            tA = __shfl_sync(0xffffffffu, tA, 0);
+            tB = __shfl_sync(0xffffffffu, tB, 0);
+            int32_t sbA = 0, s1A = 0, sbB = 0, s1B = 0;     // segment indices < 2^31 (checked at upload)
+            int32_t oA = 0, oB = 0;
+            if (tA < n2) { const int32_t r = a.p2_order[tA]; sbA = (int32_t)a.p2_segptr16[r]; s1A = (int32_t)a.p2_segptr16[r + 1]; oA = a.p2_rows[r]; }
+            int32_t rB = tB < n2 ? a.p2_order[tB] : 0;
+            int fut = 0;
+            if (lane == 0) fut = atomicAdd(a.qctr, 1);     // ticket C
+            while (tA < n2) {
+                const int tC = __shfl_sync(0xffffffffu, fut, 0);
+                const int32_t rC = tC < n2 ? a.p2_order[tC] : 0;
+                if (lane == 0) fut = atomicAdd(a.qctr, 1);  // ticket D
+                if (tB < n2) { sbB = (int32_t)a.p2_segptr16[rB]; s1B = (int32_t)a.p2_segptr16[rB + 1]; oB = a.p2_rows[rB]; }
+                const T acc = row_accumulate_k1_pf<T>(a.segs16, sbA, s1A, vals, xc, lane, a.N, a.idx16, a.seg_base16,
+                                                      a.p1done, a.n_p1items, t_ready);
+                if (lane == 0) static_cast<T*>(a.Y)[oA] = acc;
+                tA = tB; sbA = sbB; s1A = s1B; oA = oB;
+                tB = tC; rB = rC;
+            }
+            return;
+        }
+#endif
         int nxt = 0;
         if (lane == 0) nxt = atomicAdd(a.qctr, 1);
         nxt = __shfl_sync(0xffffffffu, nxt, 0);
@@ -1015,7 +1082,8 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
             const T acc = (VF_K1_WAVE_DEFAULT && a.idx16) ? row_accumulate_wave<T>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
                                                                        vals, a.idx16, a.seg_base16, xc, lane)
                         : (VF_K1_PF && a.idx16) ? row_accumulate_k1_pf<T>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
-                                                                           vals, xc, lane, a.N, a.idx16, a.seg_base16)
+                                                                           vals, xc, lane, a.N, a.idx16, a.seg_base16,
+                                                                           a.p1done, a.n_p1items, t_ready)
                         : a.idx16 ? row_accumulate_k1<T, VF_MV_L1 != 0>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
                                                                          vals, a.idx, xc, lane, a.N, nullptr, nullptr,
                                                                          a.idx16, a.seg_base16)
@@ -1544,7 +1612,7 @@ __global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) 
         if (have_p1) res_phase<T, 1, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red, xch, xpar, gs1, ng1, gs2, ng2);
         trace_ev(a, it, 1);
         if (MODE == M_MATVEC) {
-            if (have_p1 && !a.tready) grid_sync(a.ctl, nblk);   // nrhs = 1: per-block T flags instead
+            if (have_p1 && !a.tready && !a.p1done) grid_sync(a.ctl, nblk);   // nrhs = 1: T flags / item counter instead
             trace_ev(a, it, 2);
             res_phase<T, 2, MODE>(a, r, W, S, Xs, xc, xn, sred, tile, red, xch, xpar, gs1, ng1, gs2, ng2);
             trace_ev(a, it, 3);
@@ -2019,11 +2087,6 @@ __device__ __forceinline__ void cpa8_ef(unsigned d, const void* g, int src_bytes
     asm volatile("cp.async.ca.shared.global.L2::cache_hint [%0], [%1], 8, %2, %3;\n" ::"r"(d), "l"(g), "r"(src_bytes), "l"(pol)
                  : "memory");
 }
-__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
-    int v;
-    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
-    return v;
-}
 template <typename T>
 __host__ __device__ constexpr size_t k1p_warp_bytes() {
     return ((size_t)kK1pD * 32 * (4 * sizeof(T) + 8 + 8) + (size_t)kK1pD * 4 + 15) & ~(size_t)15;   // 16-B aligned rings
@@ -2278,7 +2341,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm<GROUPED>()) hot_kernel(H
         }
         trace_ev(a, it, 1);
         if (MODE == M_MATVEC) {
-            if (have_p1 && !a.tready) grid_sync(a.ctl, nblk);   // nrhs = 1: per-block T flags instead
+            if (have_p1 && !a.tready && !a.p1done) grid_sync(a.ctl, nblk);   // nrhs = 1: T flags / item counter instead
             trace_ev(a, it, 2);
             if constexpr (GROUPED) groups_phase<T, VEC, 2, MODE>(a, xc, xn, stile, sred, stage);
             else phase2_rows<T, KC, VEC, MODE>(a, xc, xn, gwarp, nwarp, lane, sred);
@@ -2840,6 +2903,7 @@ struct DeviceHMat {
     int32_t* seg_base16 = nullptr;
     int64_t k1_payload = 0;          // bytes one nrhs = 1 apply streams: values + V indices + u16 CSR offsets
     int k1_kernel = 0;
+    bool k1_ovl = false;             // nrhs = 1 row kernel without the phase barrier (X-first rows, item counter)
     int res_p2copies = 0;            // copies of each phase-2 group in the resident layout (column chunks split)               // nrhs = 1 kernel chosen at upload: 0 rows (hot_kernel), 1 stream, 2 pipelined (k1p)
     // streamed-tile layout of wide batches on a large F-hat (bt_kernel, FP64)
     bool bt_ok = false;
@@ -2872,6 +2936,16 @@ bool k1_use_stream() {
 #ifndef VF_K1_DEFAULT_PIPE
 #define VF_K1_DEFAULT_PIPE 0
 #endif
+// the row kernel's phase 1 -> phase 2 hand-over by a finished-item counter
+// instead of the grid barrier (VF_K1_OVL=0/1 overrides; read at upload)
+#ifndef VF_K1_OVL_DEFAULT
+#define VF_K1_OVL_DEFAULT 1
+#endif
+bool k1_overlap() {
+    const char* e = getenv("VF_K1_OVL");
+    if (e) return atoi(e) != 0;
+    return VF_K1_OVL_DEFAULT != 0;
+}
 bool k1_use_pipe() {
     const char* e = getenv("VF_K1_KERNEL");
     if (e) return std::strcmp(e, "pipe") == 0;
@@ -3470,7 +3544,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     if (use16) {
         const int64_t span16 = getenv("VF_U16_SPAN") ? std::min(65536, std::max(2, atoi(getenv("VF_U16_SPAN")))) : 65536;
         pay16 = D->p1_bytes;                                   // phase 1 unchanged (values, S, V indices)
-        const bool xfirst = k1_use_pipe();
+        const bool xfirst = k1_use_pipe() || k1_overlap();
         for (int64_t r = 0; r < (int64_t)p2_rows.size(); ++r) {
             // for the pipelined kernel (k1p_kernel) X-sourced runs (dense-leaf rows,
             // CSR) first, then the U_b runs over T rows: it streams a row's X part
@@ -3572,7 +3646,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             (rc = up((void**)&D->p2_order, order.data(), order.size() * 4)) ||
             (rc = up((void**)&D->p1_order, order1.data(), order1.size() * 4)) ||
             (rc = up((void**)&D->k1p_ctr, nullptr, 16)) ||
-            (rc = up((void**)&D->tready, nullptr, (size_t)std::max<int64_t>(D->n_svd + 1, 2) * 4)))
+            (rc = up((void**)&D->tready, nullptr, (size_t)(D->n_svd + 2) * 4)))
             return rc;
     }
 
@@ -3791,7 +3865,8 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         if (ok) break;
       }
     }
-    if (use16 && !s16.empty()) {
+    // the row kernel keeps segment indices of this layout in 32-bit registers
+    if (use16 && !s16.empty() && (int64_t)s16.size() < (int64_t)INT32_MAX) {
         if ((rc = up((void**)&D->segs16, s16.data(), s16.size() * sizeof(Seg))) ||
             (rc = up((void**)&D->p2_segptr16, ptr16.data(), ptr16.size() * 8)) ||
             (rc = up((void**)&D->idx16, i16.data(), i16.size() * 2)) ||
@@ -3799,6 +3874,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             return rc;
         D->k1_payload = pay16;
         if (k1_use_pipe()) D->k1_kernel = 2;
+        D->k1_ovl = !k1_use_pipe() && k1_overlap() && VF_K1_PF;
         std::vector<Seg>().swap(s16);
         std::vector<uint16_t>().swap(i16);
     }
@@ -4616,10 +4692,11 @@ int apply_k1(Handle* h, void* XT, void* Y, cudaStream_t st) {
     HotArgs a = hot_args(D, 1, 1);
     a.xt0 = XT;
     a.Y = Y;
-    CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
+    CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 2) * 4, st));
     a.qctr = D->tready + D->n_svd;
     a.p2_order = D->p2_order;
     if (D->idx16) { a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16; }
+    if (D->idx16 && D->k1_ovl) { a.p1done = D->tready + D->n_svd + 1; a.n_p1items = (int32_t)D->n_pp; }
     return launch_hot<T, M_MATVEC>(h, a, st);
 }
 
