@@ -2689,8 +2689,9 @@ __global__ void __launch_bounds__(256) cols_epilogue_kernel(const T* __restrict_
         partial[(int64_t)threadIdx.x * gridDim.x + blockIdx.x] = sum;
     }
 }
+// it = this iteration's index (the apply launches in between reset ctl)
 __global__ void cols_decide_kernel(Ctl* ctl, const double* partial, int nblk, int k, const double* enorm2,
-                                   double* resid, double tol, int iters) {
+                                   double* resid, double tol, int iters, int it0) {
     __shared__ int bad;
     if (threadIdx.x == 0) bad = 0;
     __syncthreads();
@@ -2704,9 +2705,9 @@ __global__ void cols_decide_kernel(Ctl* ctl, const double* partial, int nblk, in
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        const int it = ctl->iter + 1;
+        const int it = it0 + 1;
         ctl->iter = it;
-        if (!bad || it >= iters) ctl->done = 1;
+        ctl->done = (!bad || it >= iters) ? 1 : 0;
     }
 }
 
@@ -3662,12 +3663,14 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             int phase; int64_t g; int64_t K; std::vector<int32_t> ucols; int ch0 = 0, chstep = 1;
             int role = -1; int64_t kb = 0;                 // K-half [kb, kb + K) of a split group
         };
-        // phase-2 groups are replicated like the phase-1 groups when the copies fit
-        // the SMs' shared memory (4, else 2, else 1 copy; VF_RES_P2COPIES forces a
-        // count): with ~ as many groups as SMs (cfg2: 125 on 148) one CTA per group
-        // ran all its column chunks in sequence while other SMs idled
+        // phase-2 groups can be replicated like the phase-1 groups (copy i takes the
+        // column chunks i, i + copies, ...; VF_RES_P2COPIES = 2 or 4, falling back to
+        // fewer copies when they do not fit).  Measured on cfg2 (profiles/r02_s19_*):
+        // 2 copies 0.531 ms vs 1 copy 0.510 ms per thermal step -- the per-CTA item
+        // count, not the work per group, sets the phase-2 time -- so 1 is the default
         const char* p2e = getenv("VF_RES_P2COPIES");
-        std::vector<int> p2try = p2e ? std::vector<int>{std::max(1, atoi(p2e))} : std::vector<int>{4, 2, 1};
+        std::vector<int> p2try;
+        for (int c = p2e ? std::max(1, std::min(4, atoi(p2e))) : 1; c >= 1; c /= 2) p2try.push_back(c);
         std::vector<HG> hg2base;
         for (int64_t g = 0; g < (int64_t)g2v.size(); ++g) {
             HG x{2, g, 0, {}, 0, 1};
@@ -4604,7 +4607,7 @@ int iterate_cols(Handle* h, int k, int kp, const void* rho, int clamp, int iters
         }
         cols_epilogue_kernel<T><<<nblk, 256, 0, st>>>((const T*)D->Yp, (const T*)D->Ep, xc, xn, (T*)D->Qp, (const T*)rho,
                                                        D->active, N, k, kp, clamp, R, D->partial);
-        cols_decide_kernel<<<1, 256, 0, st>>>(D->ctl, D->partial, nblk, k, D->enorm2, D->resid, tol, iters);
+        cols_decide_kernel<<<1, 256, 0, st>>>(D->ctl, D->partial, nblk, k, D->enorm2, D->resid, tol, iters, it);
         h->launches_total += 2;
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(D->ctl_host, D->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
