@@ -486,9 +486,10 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
 #pragma unroll
                         for (int u = 0; u < 4; ++u) xr[c][u] = (int32_t)(g_src + e + u);
                     }
+                    if (!(g_kind && idx16))          // (16-bit CSR pieces are interleaved and zero-padded)
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (e + u >= g_len) { w[c][u] = T(0); xr[c][u] = g_kind ? g_base : (int32_t)g_src; }
+                        for (int u = 0; u < 4; ++u)
+                            if (e + u >= g_len) { w[c][u] = T(0); xr[c][u] = g_kind ? g_base : (int32_t)g_src; }
                 } else {
                     vx[c] = false;
                     l1[c] = false;
@@ -535,7 +536,7 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
 #define VF_K1_PF 1
 #endif
 #ifndef VF_K1_ROWPF
-#define VF_K1_ROWPF 1       // row descriptors pipelined over three rows (phase2_rows)
+#define VF_K1_ROWPF 0       // row descriptors pipelined over three rows (measured slower: 0.845 vs 0.809 ms)
 #endif
 template <typename T>
 struct K1Round {
@@ -566,10 +567,10 @@ __device__ __forceinline__ void k1_fetch(K1Round<T>& R, int cc, int ns, int tota
         const int e = (cc - g_excl) * 4;
         const int nv = min(4, g_len - e);
         V4<T>::ld(vals + g_off + e, R.w);
-        if (g_kind) {
+        if (g_kind) {                                    // interleaved CSR piece: 4 slots, zero-padded
             R.q = ld_stream_u2(reinterpret_cast<const uint2*>(idx16 + g_src + e));
             R.xb = g_base;
-            R.f = nv | 8 | 32;
+            R.f = 4 | 8 | 32;
         } else {
             R.q = make_uint2(0u, 0u);
             R.xb = (int32_t)(g_src + e);
@@ -669,14 +670,7 @@ __device__ __forceinline__ T row_accumulate_k1_pf(const Seg* __restrict__ segs, 
     return acc;
 }
 
-// nrhs = 1, wave-interleaved (VF_K1_WAVE): lane l takes terms base + l of a
-// row's concatenated segments, so one gather instruction touches 32
-// CONSECUTIVE terms -- consecutive CSR columns / contiguous x runs -- i.e. a
-// few cache lines instead of the 128-term spread of the quad mapping above
-// (fewer L1/TEX wavefronts, the limiter of that kernel on configs[2]).  The
-// segment of a wave is found once (warp-uniform binary search on the wave's
-// first term) and lanes past a segment boundary advance with a ballot loop.
-// Values and 16-bit CSR offsets are scalar streaming loads; U waves in flight.
+// scalar streaming loads (L1::no_allocate, L2 evict-first)
 __device__ __forceinline__ double ld_stream_d(const double* p) {
 #if VF_K1_NA
     double v;
@@ -707,76 +701,6 @@ __device__ __forceinline__ unsigned ld_stream_u16(const uint16_t* p) {
 template <typename T> __device__ __forceinline__ T ld_stream_s(const T* p);
 template <> __device__ __forceinline__ double ld_stream_s<double>(const double* p) { return ld_stream_d(p); }
 template <> __device__ __forceinline__ float ld_stream_s<float>(const float* p) { return ld_stream_f(p); }
-#ifndef VF_K1_WU
-#define VF_K1_WU 4
-#endif
-#ifndef VF_K1_WAVE_DEFAULT
-#define VF_K1_WAVE_DEFAULT 0
-#endif
-template <typename T>
-__device__ __forceinline__ T row_accumulate_wave(const Seg* __restrict__ segs, int64_t s0, int64_t s1,
-                                                 const T* __restrict__ vals, const uint16_t* __restrict__ idx16,
-                                                 const int32_t* __restrict__ seg_base, const T* xt, int lane) {
-    constexpr unsigned FULL = 0xffffffffu;
-    constexpr int U = VF_K1_WU;
-    T acc[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) acc[u] = T(0);
-    for (int64_t sb = s0; sb < s1; sb += 32) {
-        const int ns = (int)(s1 - sb < 32 ? s1 - sb : 32);
-        Seg my{0, 0, 0, 0};
-        int32_t my_base = 0;
-        if (lane < ns) { my = segs[sb + lane]; my_base = seg_base[sb + lane]; }
-        int incl = my.len;
-#pragma unroll
-        for (int off = 1; off < 32; off <<= 1) {
-            const int v = __shfl_up_sync(FULL, incl, off);
-            if (lane >= off) incl += v;
-        }
-        const int excl = incl - my.len;
-        const int total = __shfl_sync(FULL, incl, 31);
-        int g0 = 0;                                                // segment of the current wave's first term
-        for (int w0 = 0; w0 < total; w0 += 32 * U) {
-            T v[U], x[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int wb = w0 + 32 * u;
-                v[u] = T(0);
-                x[u] = T(0);
-                if (wb < total) {                                  // warp-uniform
-                    while (g0 + 1 < ns && __shfl_sync(FULL, excl, (g0 + 1) & 31) <= wb) ++g0;   // uniform walk
-                    const int t = wb + lane;
-                    int g = g0;
-                    for (;;) {                                     // lanes past a boundary advance
-                        const int nb = __shfl_sync(FULL, excl, (g + 1) & 31);
-                        const bool adv = g + 1 < ns && nb <= t;
-                        if (!__any_sync(FULL, adv)) break;
-                        g += adv ? 1 : 0;
-                    }
-                    const int64_t g_off = __shfl_sync(FULL, my.val_off, g);
-                    const int64_t g_src = __shfl_sync(FULL, my.src, g);
-                    const int g_kind = __shfl_sync(FULL, my.kind, g);
-                    const int g_excl = __shfl_sync(FULL, excl, g);
-                    const int g_base = __shfl_sync(FULL, my_base, g);
-                    if (t < total) {
-                        const int e = t - g_excl;
-                        v[u] = ld_stream_s<T>(vals + g_off + e);
-                        const int64_t xr = g_kind ? (int64_t)g_base + ld_stream_u16(idx16 + g_src + e) : g_src + e;
-                        x[u] = XLD(xt + xr);
-                    }
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) acc[u] = fma(v[u], x[u], acc[u]);
-        }
-    }
-    T a = acc[0];
-#pragma unroll
-    for (int u = 1; u < U; ++u) a += acc[u];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) a += __shfl_xor_sync(FULL, a, off);
-    return a;
-}
 
 // Software grid barrier for a cooperative (co-resident) launch.  Traps
 // instead of hanging if a CTA never arrives.
@@ -1042,7 +966,7 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
         // the next ticket is fetched while the current row streams
         bool t_ready = a.p1done == nullptr;           // with the phase barrier T rows are ready
 #if VF_K1_PF && VF_K1_ROWPF
-        if (a.idx16 && !VF_K1_WAVE_DEFAULT) {
+        if (a.idx16) {
             // row descriptors software-pipelined over three rows: at the start of
             // row A the warp already holds B's segment range and output row, issues
             // the load of C's tree row (ticket fetched one row earlier) and the
@@ -1079,9 +1003,7 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
             const int64_t r = a.p2_order[nxt];
             int fut = 0;
             if (lane == 0) fut = atomicAdd(a.qctr, 1);
-            const T acc = (VF_K1_WAVE_DEFAULT && a.idx16) ? row_accumulate_wave<T>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
-                                                                       vals, a.idx16, a.seg_base16, xc, lane)
-                        : (VF_K1_PF && a.idx16) ? row_accumulate_k1_pf<T>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
+            const T acc = (VF_K1_PF && a.idx16) ? row_accumulate_k1_pf<T>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
                                                                            vals, xc, lane, a.N, a.idx16, a.seg_base16,
                                                                            a.p1done, a.n_p1items, t_ready)
                         : a.idx16 ? row_accumulate_k1<T, VF_MV_L1 != 0>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
@@ -2183,7 +2105,7 @@ __global__ void __launch_bounds__(kThreads, VF_K1P_CTAS) k1p_kernel(HotArgs a, i
         const int g_base = __shfl_sync(FULL, my_base, g);
         const bool ok = cc < total;
         const int e = (cc - g_excl) * 4;
-        const int nv = ok ? min(4, g_len - e) : 0;
+        const int nv = ok ? (g_kind ? 4 : min(4, g_len - e)) : 0;   // CSR pieces: interleaved, zero-padded
         const unsigned dv = (unsigned)__cvta_generic_to_shared(sv + ((size_t)s * 32 + lane) * 4);
         const T* pv = ok ? vals + g_off + e : vals;
         if (sizeof(T) == 8) {
@@ -2940,7 +2862,7 @@ bool k1_use_stream() {
 // the row kernel's phase 1 -> phase 2 hand-over by a finished-item counter
 // instead of the grid barrier (VF_K1_OVL=0/1 overrides; read at upload)
 #ifndef VF_K1_OVL_DEFAULT
-#define VF_K1_OVL_DEFAULT 1
+#define VF_K1_OVL_DEFAULT 0     // measured neutral on configs[2] (0.809 vs 0.810 ms): the barrier stays
 #endif
 bool k1_overlap() {
     const char* e = getenv("VF_K1_OVL");
@@ -3546,39 +3468,72 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         const int64_t span16 = getenv("VF_U16_SPAN") ? std::min(65536, std::max(2, atoi(getenv("VF_U16_SPAN")))) : 65536;
         pay16 = D->p1_bytes;                                   // phase 1 unchanged (values, S, V indices)
         const bool xfirst = k1_use_pipe() || k1_overlap();
+        struct Run { Seg sg; int32_t e, f, base; };       // kind 0: sg as is; kind 1: terms [e, f) of CSR seg sg
+        const bool ilv = !getenv("VF_K1_ILV") || atoi(getenv("VF_K1_ILV")) != 0;   // 0: plain order (A/B)
+        std::vector<Run> rs;
         for (int64_t r = 0; r < (int64_t)p2_rows.size(); ++r) {
             // for the pipelined kernel (k1p_kernel) X-sourced runs (dense-leaf rows,
             // CSR) first, then the U_b runs over T rows: it streams a row's X part
             // while phase-1 items may still be producing T.  The other kernels keep
             // the segment order of the u32 layout (same summation order as the
             // batched / barrier-free schedules: bitwise equal results)
+            rs.clear();
             for (int pass = 0; pass < (xfirst ? 2 : 1); ++pass)
             for (int64_t q = p2_segptr[r]; q < p2_segptr[r + 1]; ++q) {
                 const Seg sg = segs[q];
                 const bool tsrc = sg.kind == 0 && sg.src >= D->N;
                 if (xfirst && tsrc != (pass == 1)) continue;
-                if (sg.kind == 0) {
-                    s16.push_back(sg); base16.push_back(0);
-                    pay16 += (int64_t)sizeof(T) * sg.len;
-                    continue;
-                }
+                if (sg.kind == 0) { rs.push_back(Run{sg, 0, sg.len, 0}); continue; }
                 for (int32_t e = 0; e < sg.len;) {
                     const int32_t base = idx[sg.src + e];
                     int32_t f = e + 1;
                     while (f < sg.len && idx[sg.src + f] - base < span16) ++f;
-                    int64_t voff = sg.val_off + e;
-                    if ((voff * (int64_t)sizeof(T)) % 16) {           // realign: copy this run's values
-                        std::vector<T> cp(vals.begin() + voff, vals.begin() + voff + (f - e));
-                        voff = (int64_t)vals.size();
-                        for (T v : cp) vals.push_back(v);
-                        while ((vals.size() * sizeof(T)) % 16) vals.push_back(T(0));
-                    }
-                    while (i16.size() % 4) i16.push_back(0);       // 8-B aligned run start (uint2 loads)
-                    s16.push_back(Seg{voff, (int64_t)i16.size(), f - e, 1});
-                    for (int32_t u = e; u < f; ++u) i16.push_back((uint16_t)(idx[sg.src + u] - base));
-                    base16.push_back(base);
-                    pay16 += (int64_t)(sizeof(T) + 2) * (f - e);
+                    rs.push_back(Run{sg, e, f, base});
                     e = f;
+                }
+            }
+            // Emit.  The kernels walk a row in batches of 32 runs and rounds of 32
+            // 4-term chunks (one per lane, chunk c of a run = its terms 4c..4c+3 in
+            // the plain order).  A CSR run's values and 16-bit offsets are stored
+            // INTERLEAVED per round piece instead: the n chunks a run has in one
+            // round hold its m <= 4n terms of that round as lane i <- terms
+            // i, i + n, i + 2n, i + 3n (explicit zeros with offset 0 where >= m), so
+            // the j-th x gather of the warp touches n CONSECUTIVE sorted columns
+            // (a few cache lines) instead of every 4th column of a 4n-term span.
+            for (size_t b0 = 0; b0 < rs.size(); b0 += 32) {
+                int64_t cum = 0;                                   // chunks before this run in its batch
+                for (size_t i = b0; i < std::min(rs.size(), b0 + 32); ++i) {
+                    const Run& R = rs[i];
+                    const int32_t len = R.f - R.e;
+                    const int64_t nch = (len + 3) / 4;
+                    if (R.sg.kind == 0) {
+                        s16.push_back(R.sg); base16.push_back(0);
+                        pay16 += (int64_t)sizeof(T) * len;
+                        cum += nch;
+                        continue;
+                    }
+                    while ((vals.size() * sizeof(T)) % 16) vals.push_back(T(0));
+                    while (i16.size() % 4) i16.push_back(0);       // 8-B aligned run start (uint2 loads)
+                    const int64_t voff = (int64_t)vals.size(), ioff = (int64_t)i16.size();
+                    vals.resize(vals.size() + 4 * nch, T(0));
+                    i16.resize(i16.size() + 4 * nch, 0);
+                    int64_t c = 0, t = 0;
+                    while (c < nch) {
+                        const int64_t pos = cum + c, rend = (pos / 32 + 1) * 32;
+                        const int64_t n = std::min(nch - c, rend - pos);
+                        const int64_t m = std::min<int64_t>(4 * n, len - t);
+                        for (int64_t u = 0; u < m; ++u) {
+                            const int64_t slot = ilv ? (c + u % n) * 4 + u / n : c * 4 + u;
+                            vals[voff + slot] = vals[R.sg.val_off + R.e + t + u];
+                            i16[ioff + slot] = (uint16_t)(idx[R.sg.src + R.e + t + u] - R.base);
+                        }
+                        c += n;
+                        t += m;
+                    }
+                    s16.push_back(Seg{voff, ioff, len, 1});
+                    base16.push_back(R.base);
+                    pay16 += (int64_t)(sizeof(T) + 2) * len;
+                    cum += nch;
                 }
             }
             ptr16.push_back((int64_t)s16.size());
