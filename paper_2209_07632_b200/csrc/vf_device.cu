@@ -670,37 +670,6 @@ __device__ __forceinline__ T row_accumulate_k1_pf(const Seg* __restrict__ segs, 
     return acc;
 }
 
-// scalar streaming loads (L1::no_allocate, L2 evict-first)
-__device__ __forceinline__ double ld_stream_d(const double* p) {
-#if VF_K1_NA
-    double v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n" : "=d"(v) : "l"(p), "l"(l2_evict_first()));
-    return v;
-#else
-    return __ldg(p);
-#endif
-}
-__device__ __forceinline__ float ld_stream_f(const float* p) {
-#if VF_K1_NA
-    float v;
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;\n" : "=f"(v) : "l"(p), "l"(l2_evict_first()));
-    return v;
-#else
-    return __ldg(p);
-#endif
-}
-__device__ __forceinline__ unsigned ld_stream_u16(const uint16_t* p) {
-    unsigned short v;
-#if VF_K1_NA
-    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;\n" : "=h"(v) : "l"(p), "l"(l2_evict_first()));
-#else
-    v = __ldg(p);
-#endif
-    return v;
-}
-template <typename T> __device__ __forceinline__ T ld_stream_s(const T* p);
-template <> __device__ __forceinline__ double ld_stream_s<double>(const double* p) { return ld_stream_d(p); }
-template <> __device__ __forceinline__ float ld_stream_s<float>(const float* p) { return ld_stream_f(p); }
 
 // Software grid barrier for a cooperative (co-resident) launch.  Traps
 // instead of hanging if a CTA never arrives.
@@ -1596,6 +1565,9 @@ constexpr int kBCols = 128;         // columns per pass over a tile
 #ifndef VF_BT_ACC2
 #define VF_BT_ACC2 0
 #endif
+#ifndef VF_BT_HALF
+#define VF_BT_HALF 1        // tiles of <= 8 rows issue only the upper 8x8 DMMA tiles
+#endif
 #ifndef VF_BT_STAGES
 #define VF_BT_STAGES 4
 #endif
@@ -1717,6 +1689,17 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                     }
                     for (; ks < KS / 4; ks += nkp) {
 #else
+                    if (VF_BT_HALF && B.nrows <= 8) {
+                        // tile-uniform: rows 8..15 are padding, their DMMAs would add zeros
+                        for (int ks = pw; ks < KS / 4; ks += nkp) {
+                            const int j = ks * 4 + kr;
+                            const int sw = 4 * kr;
+                            const double a0 = W0[j * 16 + (mn ^ sw)];
+                            const double b0 = X0[j * KPB + ((cc + mn) ^ sw)], b1 = X0[j * KPB + ((cc + 8 + mn) ^ sw)];
+                            dmma884(dacc[0], a0, b0);
+                            dmma884(dacc[1], a0, b1);
+                        }
+                    } else
                     for (int ks = pw; ks < KS / 4; ks += nkp) {
 #endif
                         const int j = ks * 4 + kr;
