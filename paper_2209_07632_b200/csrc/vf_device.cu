@@ -3453,6 +3453,9 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         const bool xfirst = k1_use_pipe() || k1_overlap();
         struct Run { Seg sg; int32_t e, f, base; };       // kind 0: sg as is; kind 1: terms [e, f) of CSR seg sg
         const bool ilv = !getenv("VF_K1_ILV") || atoi(getenv("VF_K1_ILV")) != 0;   // 0: plain order (A/B)
+        // dense / U runs copied next to the row's CSR pieces, so a warp streams one
+        // contiguous range per row (VF_K1_PACK=0: they stay in the shared layout)
+        const bool pack = !getenv("VF_K1_PACK") || atoi(getenv("VF_K1_PACK")) != 0;
         std::vector<Run> rs;
         for (int64_t r = 0; r < (int64_t)p2_rows.size(); ++r) {
             // for the pipelined kernel (k1p_kernel) X-sourced runs (dense-leaf rows,
@@ -3490,7 +3493,15 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                     const int32_t len = R.f - R.e;
                     const int64_t nch = (len + 3) / 4;
                     if (R.sg.kind == 0) {
-                        s16.push_back(R.sg); base16.push_back(0);
+                        Seg sg = R.sg;
+                        if (pack) {                                // the row's runs contiguous in one region
+                            while ((vals.size() * sizeof(T)) % 16) vals.push_back(T(0));
+                            const int64_t v0 = (int64_t)vals.size();
+                            vals.resize(vals.size() + len);
+                            std::copy(vals.begin() + R.sg.val_off, vals.begin() + R.sg.val_off + len, vals.begin() + v0);
+                            sg.val_off = v0;
+                        }
+                        s16.push_back(sg); base16.push_back(0);
                         pay16 += (int64_t)sizeof(T) * len;
                         cum += nch;
                         continue;
