@@ -535,6 +535,9 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
 #ifndef VF_K1_PF
 #define VF_K1_PF 1
 #endif
+#ifndef VF_K1_L2PF
+#define VF_K1_L2PF 0        // rounds ahead for the bulk L2 prefetch of a batch's values (0 = off)
+#endif
 #ifndef VF_K1_ROWPF
 #define VF_K1_ROWPF 0       // row descriptors pipelined over three rows (measured slower: 0.845 vs 0.809 ms)
 #endif
@@ -652,10 +655,31 @@ __device__ __forceinline__ T row_accumulate_k1_pf(const Seg* __restrict__ segs, 
         }
         const int excl = incl - nch;
         const int total = __shfl_sync(FULL, incl, 31);
+#if VF_K1_L2PF
+        // the batch's runs are contiguous in vals (packed 16-bit layout): round b's
+        // values sit near vb + 4 b chunks; lane 0 prefetches round b + VF_K1_L2PF's
+        // values into L2 with one bulk prefetch, so the HBM stream runs ahead of the
+        // warp's register-limited loads
+        const int64_t vb = __shfl_sync(FULL, my.val_off, 0);
+        const int64_t ve = __shfl_sync(FULL, my.val_off + my.len, ns - 1);
+        auto l2pf = [&](int b) {
+            if (lane == 0) {
+                const int64_t a0 = vb + (int64_t)(b + 32 * VF_K1_L2PF) * 4;
+                if (a0 < ve) {
+                    const int64_t nb = min((int64_t)(32 * 4 * sizeof(T)), ((ve - a0) * (int64_t)sizeof(T) + 15) & ~(int64_t)15);
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(vals + a0), "r"((unsigned)nb) : "memory");
+                }
+            }
+        };
+        l2pf(0);
+#endif
         K1Round<T> cur;
         k1_fetch<T>(cur, lane, ns, total, excl, my, my_base, vals, idx16, nx, lane);
         for (int base = 32; base < total; base += 32) {          // warp-uniform
             K1Round<T> nxt;
+#if VF_K1_L2PF
+            l2pf(base);
+#endif
             k1_fetch<T>(nxt, base + lane, ns, total, excl, my, my_base, vals, idx16, nx, lane);
             if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
             k1_consume<T>(cur, xt, acc0, acc1);
