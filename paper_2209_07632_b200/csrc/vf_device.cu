@@ -1590,7 +1590,7 @@ constexpr int kBCols = 128;         // columns per pass over a tile
 #define VF_BT_ACC2 0
 #endif
 #ifndef VF_BT_HALF
-#define VF_BT_HALF 1        // tiles of <= 8 rows issue only the upper 8x8 DMMA tiles
+#define VF_BT_HALF 0        // tiles of <= 8 rows: only the upper 8x8 DMMA tiles (measured 8.89 vs 8.77 ms at k=128: off)
 #endif
 #ifndef VF_BT_STAGES
 #define VF_BT_STAGES 4
@@ -3477,9 +3477,10 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         const bool xfirst = k1_use_pipe() || k1_overlap();
         struct Run { Seg sg; int32_t e, f, base; };       // kind 0: sg as is; kind 1: terms [e, f) of CSR seg sg
         const bool ilv = !getenv("VF_K1_ILV") || atoi(getenv("VF_K1_ILV")) != 0;   // 0: plain order (A/B)
-        // dense / U runs copied next to the row's CSR pieces, so a warp streams one
-        // contiguous range per row (VF_K1_PACK=0: they stay in the shared layout)
-        const bool pack = !getenv("VF_K1_PACK") || atoi(getenv("VF_K1_PACK")) != 0;
+        // VF_K1_PACK=1: dense / U runs copied next to the row's CSR pieces (one
+        // contiguous range per row).  Measured 0.812 vs 0.805 ms without on
+        // configs[2] (profiles/r02_s22_*), so off: they stay in the shared layout
+        const bool pack = getenv("VF_K1_PACK") && atoi(getenv("VF_K1_PACK")) != 0;
         std::vector<Run> rs;
         for (int64_t r = 0; r < (int64_t)p2_rows.size(); ++r) {
             // for the pipelined kernel (k1p_kernel) X-sourced runs (dense-leaf rows,
