@@ -535,6 +535,9 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
 #ifndef VF_K1_PF
 #define VF_K1_PF 1
 #endif
+#ifndef VF_K1_PFD
+#define VF_K1_PFD 1         // rounds of the F-hat stream in registers ahead of the gathers (1 or 2)
+#endif
 #ifndef VF_K1_L2PF
 #define VF_K1_L2PF 0        // rounds ahead for the bulk L2 prefetch of a batch's values (0 = off)
 #endif
@@ -675,6 +678,26 @@ __device__ __forceinline__ T row_accumulate_k1_pf(const Seg* __restrict__ segs, 
 #endif
         K1Round<T> cur;
         k1_fetch<T>(cur, lane, ns, total, excl, my, my_base, vals, idx16, nx, lane);
+#if VF_K1_PFD >= 2
+        // two rounds in flight: rounds i + 1 and i + 2 are fetched before round i's gathers
+        if (32 < total) {
+            K1Round<T> nx1;
+            k1_fetch<T>(nx1, 32 + lane, ns, total, excl, my, my_base, vals, idx16, nx, lane);
+            int base = 64;
+            for (; base < total; base += 32) {
+                K1Round<T> nx2;
+                k1_fetch<T>(nx2, base + lane, ns, total, excl, my, my_base, vals, idx16, nx, lane);
+                if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
+                k1_consume<T>(cur, xt, acc0, acc1);
+                cur = nx1;
+                nx1 = nx2;
+            }
+            if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
+            k1_consume<T>(cur, xt, acc0, acc1);
+            cur = nx1;
+        }
+        if (0)
+#endif
         for (int base = 32; base < total; base += 32) {          // warp-uniform
             K1Round<T> nxt;
 #if VF_K1_L2PF
