@@ -1861,9 +1861,15 @@ __device__ __forceinline__ void tc_wait(uint64_t* bar, unsigned parity) {
 constexpr int kTRaw = kTS * 128 * 4;              // raw X slice, row-major [32 sources][128 columns]
 constexpr int kTA = 128 * kTS * 4;                // one K-major A operand (hi or lo)
 constexpr int kTB = 16 * kTS * 4;                 // one K-major B operand (hi or lo)
-constexpr int kTSmem = 3 * (kTRaw + 2 * kTB) + 2 * (2 * kTA);   // 3 staging slots, 2 A buffer pairs
+#ifndef VF_TC_AB
+#define VF_TC_AB 2          // split (hi, lo) A buffer pairs: 2 = split of slice s + 1 overlaps the MMAs of s
+#endif
+#ifndef VF_TC_CTAS
+#define VF_TC_CTAS 1        // CTAs per SM (2 needs VF_TC_AB = 1 to fit shared memory)
+#endif
+constexpr int kTSmem = 3 * (kTRaw + 2 * kTB) + VF_TC_AB * (2 * kTA);   // 3 staging slots, A buffer pairs
 
-__global__ void __launch_bounds__(256, 1) bt_tc_kernel(TArgs a) {
+__global__ void __launch_bounds__(256, VF_TC_CTAS) bt_tc_kernel(TArgs a) {
     extern __shared__ __align__(1024) unsigned char tsm[];
     __shared__ uint32_t tmem_base;
     __shared__ __align__(8) uint64_t bar_mma;
@@ -1926,12 +1932,14 @@ __global__ void __launch_bounds__(256, 1) bt_tc_kernel(TArgs a) {
                     }
                     cpa_commit();
                     cpa_wait<2>();
-                    if (sl >= 1 && sl + 2 >= nsl) tc_wait(&bar_mma, (mma_issued - 1) & 1);   // A[(sl) % 2] free
+                    // A[sl % VF_TC_AB] free: the MMAs of slice sl - VF_TC_AB ... with two buffers the wait
+                    // above (slot reuse) already covered slice sl - 1 whenever sl + 2 < nsl
+                    if (sl >= 1 && (VF_TC_AB == 1 || sl + 2 >= nsl)) tc_wait(&bar_mma, (mma_issued - 1) & 1);
                     __syncthreads();
                     {   // split + transpose: hi = tf32(x), lo = x - hi into K-major A[sl % 2]
                         const float* rw = reinterpret_cast<const float*>(raw(sl % 3));
-                        unsigned char* ah = abuf(sl & 1, 0);
-                        unsigned char* al = abuf(sl & 1, 1);
+                        unsigned char* ah = abuf(sl % VF_TC_AB, 0);
+                        unsigned char* al = abuf(sl % VF_TC_AB, 1);
                         for (int task = t; task < 128 * (kTS / 4); task += 256) {
                             const int c = task & 127, j4 = task >> 7;
                             float4 hv, lv;
@@ -1955,7 +1963,7 @@ __global__ void __launch_bounds__(256, 1) bt_tc_kernel(TArgs a) {
                     __syncthreads();
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                     if (t == 0) {
-                        const unsigned ah = tc_smem(abuf(sl & 1, 0)), al = tc_smem(abuf(sl & 1, 1));
+                        const unsigned ah = tc_smem(abuf(sl % VF_TC_AB, 0)), al = tc_smem(abuf(sl % VF_TC_AB, 1));
                         const unsigned bh = tc_smem(bsl(sl % 3, 0)), bl = tc_smem(bsl(sl % 3, 1));
 #pragma unroll
                         for (int ks = 0; ks < kTS / 8; ++ks) {
@@ -4384,7 +4392,7 @@ int launch_bt_tc(Handle* h, HotArgs& ha, cudaStream_t st) {
     if (per_sm < 1) return set_error(VF_ECUDA, "bt_tc_kernel cannot be resident");
     int nsm = 148;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
-    const int grid = nsm;                                  // one CTA per SM (TMEM: 32 columns each)
+    const int grid = nsm * std::min(per_sm, VF_TC_CTAS);   // TMEM: 32 columns per CTA
     TArgs b{D->bt_tiles, D->bt_n1, D->bt_n2, D->bt_Whi, D->bt_Wlo, D->bt_src, D->bt_out, (float*)ha.xt0, (float*)ha.Y,
             D->N, ha.kp, D->bt_ctr, D->ctl};
     CK(cudaMemsetAsync(D->bt_ctr, 0, 16, st));
