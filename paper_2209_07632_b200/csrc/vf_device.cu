@@ -2010,6 +2010,206 @@ __global__ void __launch_bounds__(256, VF_TC_CTAS) bt_tc_kernel(TArgs a) {
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(tmem));
 }
 
+// ---- bt_tc2_kernel: the FP32 streamed tiles of bt_tc_kernel as a
+// warp-specialised pipeline (one CTA of 12 warps per SM; units = (tile,
+// 128-column block) assigned round-robin, slices of 32 sources):
+//   warp 0      producer: per slice, 32 lanes issue cp.async.bulk copies of
+//               the slice's source rows (512 B each) and of the pre-split
+//               weights (2 x 2 KB) into stage slot g % 4, completion by
+//               transaction count on full[slot];
+//   warps 4-7   split: raw X slice -> hi = tf32(x), lo = x - hi, transposed
+//               into the K-major A pair g % 2, then arrive on afull;
+//   warp 1      MMA (one lane): 3 x 4 tcgen05.mma kind::tf32 per slice into
+//               TMEM accumulator u % 2, commits free the stage slot and the
+//               A pair, and at a unit's end signal accfull;
+//   warps 8-11  epilogue: tcgen05.ld of their 32 TMEM lanes, store, arrive
+//               on accempty.
+// All roles walk the same (unit, slice) sequence, so every barrier's phase
+// parity is a function of the running slice / unit counters.  Phase-1
+// outputs (T rows, written with st.global) are made visible to the phase-2
+// bulk copies (async proxy) by fence.proxy.async + the grid barrier.
+constexpr int kT2S = 4;                            // stage slots
+constexpr int kT2A = 2;                            // A pairs
+constexpr int kT2Slot = kTRaw + 2 * kTB;           // raw X slice + W hi + W lo
+constexpr int kT2Smem = kT2S * kT2Slot + kT2A * 2 * kTA;
+__device__ __forceinline__ void t2_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(tc_smem(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void t2_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];\n" ::"r"(tc_smem(bar)) : "memory");
+}
+__device__ __forceinline__ void t2_expect(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 _, [%0], %1;\n" ::"r"(tc_smem(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void t2_bulk(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                     tc_smem(dst)),
+                 "l"(src), "r"(bytes), "r"(tc_smem(bar))
+                 : "memory");
+}
+__global__ void __launch_bounds__(384, 1) bt_tc2_kernel(TArgs a) {
+    extern __shared__ __align__(1024) unsigned char tsm[];
+    __shared__ uint32_t tmem_base;
+    __shared__ __align__(8) uint64_t full[kT2S], sempty[kT2S], afull[kT2A], aempty[kT2A], accfull[2], accempty[2];
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 32;\n" ::"r"(tc_smem(&tmem_base)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (t == 32) {
+        for (int i = 0; i < kT2S; ++i) { t2_init(&full[i], 1); t2_init(&sempty[i], 1); }
+        for (int i = 0; i < kT2A; ++i) { t2_init(&afull[i], 4); t2_init(&aempty[i], 1); }
+        for (int i = 0; i < 2; ++i) { t2_init(&accfull[i], 1); t2_init(&accempty[i], 4); }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = tmem_base;
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(16 >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+    constexpr unsigned LBOA = (128 / 8) * 128, LBOB = (16 / 8) * 128;
+    auto slot_raw = [&](int st) { return tsm + st * kT2Slot; };
+    auto slot_w = [&](int st, int h) { return tsm + st * kT2Slot + kTRaw + h * kTB; };
+    auto abuf = [&](int q, int h) { return tsm + kT2S * kT2Slot + q * 2 * kTA + h * kTA; };
+    const int ncb = a.kp / 128;
+    uint32_t g = 0, u = 0;                                 // running slice / unit counters (all roles)
+    for (int phase = 1; phase <= 2; ++phase) {
+        const int nt = phase == 1 ? a.n1 : a.n2, base = phase == 1 ? 0 : a.n1;
+        const int nunits = nt * ncb;
+        for (int un = blockIdx.x; un < nunits; un += gridDim.x) {
+            const int it = un / ncb, cb = (un - it * ncb) * 128;
+            const BTile B = a.tiles[base + it];
+            const int nsl = (B.K + kTS - 1) / kTS;
+            if (nsl == 0) {                                // empty tile: zeros, no pipeline use
+                if (warp >= 8) {
+                    const int col = cb + (warp - 8) * 32 + lane;
+                    for (int rr = 0; rr < B.nrows; ++rr) {
+                        const int64_t orow = a.outrow[B.out_off + rr];
+                        float* dst = phase == 1 ? a.XT + (a.N + orow) * a.kp + col : a.Y + orow * a.kp + col;
+                        *dst = 0.0f;
+                    }
+                }
+                continue;
+            }
+            const int32_t* S = a.src + B.s_off;
+            if (warp == 0) {                               // ---- producer
+                for (int sl = 0; sl < nsl; ++sl, ++g) {
+                    const int st = g % kT2S;
+                    if (g >= (uint32_t)kT2S) tc_wait(&sempty[st], ((g / kT2S) - 1) & 1);
+                    const int j0 = sl * kTS, n = min(kTS, B.K - j0);
+                    if (lane == 0) t2_expect(&full[st], (unsigned)(n * 512 + 2 * kTB));
+                    __syncwarp();
+                    if (lane < n) {
+                        const int64_t row = S[j0 + lane];
+                        t2_bulk(slot_raw(st) + lane * 512, a.XT + row * a.kp + cb, 512, &full[st]);
+                    }
+                    const int64_t wo = B.w_off + (int64_t)sl * kTS * 16;
+                    if (lane == 0) t2_bulk(slot_w(st, 0), a.Whi + wo, kTB, &full[st]);
+                    if (lane == 1) t2_bulk(slot_w(st, 1), a.Wlo + wo, kTB, &full[st]);
+                }
+            } else if (warp >= 4 && warp < 8) {            // ---- split + transpose
+                const int ts = t - 128;
+                for (int sl = 0; sl < nsl; ++sl, ++g) {
+                    const int st = g % kT2S, ab = g % kT2A;
+                    const int j0 = sl * kTS, n = min(kTS, B.K - j0);
+                    tc_wait(&full[st], (g / kT2S) & 1);
+                    if (g >= (uint32_t)kT2A) tc_wait(&aempty[ab], ((g / kT2A) - 1) & 1);
+                    const float* rw = reinterpret_cast<const float*>(slot_raw(st));
+                    unsigned char* ah = abuf(ab, 0);
+                    unsigned char* al = abuf(ab, 1);
+                    for (int task = ts; task < 128 * (kTS / 4); task += 128) {
+                        const int c = task & 127, j4 = task >> 7;
+                        float4 hv, lv;
+                        float* hp = &hv.x;
+                        float* lp = &lv.x;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int j = 4 * j4 + q;
+                            const float x = j < n ? rw[j * 128 + c] : 0.0f;
+                            uint32_t hb;
+                            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hb) : "f"(x));
+                            hp[q] = __uint_as_float(hb);
+                            lp[q] = x - hp[q];
+                        }
+                        const int off = (c >> 3) * 128 + j4 * LBOA + (c & 7) * 16;
+                        *reinterpret_cast<float4*>(ah + off) = hv;
+                        *reinterpret_cast<float4*>(al + off) = lv;
+                    }
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    __syncwarp();
+                    if (lane == 0) t2_arrive(&afull[ab]);
+                }
+            } else if (warp == 1) {                        // ---- MMA issuer
+                const int acc = u & 1;
+                if (u >= 2) tc_wait(&accempty[acc], ((u / 2) - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                for (int sl = 0; sl < nsl; ++sl, ++g) {
+                    const int st = g % kT2S, ab = g % kT2A;
+                    tc_wait(&full[st], (g / kT2S) & 1);
+                    tc_wait(&afull[ab], (g / kT2A) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                    if (lane == 0) {
+                        const unsigned ah = tc_smem(abuf(ab, 0)), al = tc_smem(abuf(ab, 1));
+                        const unsigned bh = tc_smem(slot_w(st, 0)), bl = tc_smem(slot_w(st, 1));
+#pragma unroll
+                        for (int ks = 0; ks < kTS / 8; ++ks) {
+                            const uint32_t first = (sl == 0 && ks == 0) ? 0u : 1u;
+                            const uint64_t dah = tc_desc(ah + 2 * ks * LBOA, LBOA, 128), dal = tc_desc(al + 2 * ks * LBOA, LBOA, 128);
+                            const uint64_t dbh = tc_desc(bh + 2 * ks * LBOB, LBOB, 128), dbl = tc_desc(bl + 2 * ks * LBOB, LBOB, 128);
+                            tc_mma(tmem + acc * 16, dah, dbh, idesc, first);
+                            tc_mma(tmem + acc * 16, dah, dbl, idesc, 1u);
+                            tc_mma(tmem + acc * 16, dal, dbh, idesc, 1u);
+                        }
+                        tc_commit(&sempty[st]);
+                        tc_commit(&aempty[ab]);
+                        if (sl + 1 == nsl) tc_commit(&accfull[acc]);
+                    }
+                    __syncwarp();
+                }
+                ++u;
+            } else if (warp >= 8) {                        // ---- epilogue
+                const int acc = u & 1;
+                g += nsl;
+                tc_wait(&accfull[acc], (u / 2) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                uint32_t r[16];
+                const uint32_t ta = tmem + acc * 16 + ((uint32_t)((warp - 8) * 32) << 16);
+                asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+                             : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                               "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                               "=r"(r[14]), "=r"(r[15])
+                             : "r"(ta));
+                asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) t2_arrive(&accempty[acc]);
+                const int col = cb + (warp - 8) * 32 + lane;
+#pragma unroll
+                for (int rr = 0; rr < 16; ++rr) {
+                    if (rr >= B.nrows) break;
+                    const int64_t orow = a.outrow[B.out_off + rr];
+                    float* dst = phase == 1 ? a.XT + (a.N + orow) * a.kp + col : a.Y + orow * a.kp + col;
+                    *dst = __uint_as_float(r[rr]);
+                }
+                ++u;
+            } else {                                       // warps 2, 3: idle, keep the counters
+                g += nsl;
+                ++u;
+            }
+        }
+        if (phase == 1) {
+            // T rows (generic-proxy stores) -> phase-2 bulk copies (async proxy) on any SM
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+            __threadfence();
+            grid_sync(a.ctl, gridDim.x);
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 32;\n" ::"r"(tmem));
+}
+
 // ---- nrhs = 1 pipelined apply (k1p_kernel; SURVEY §8(a) a2 + a3, Alg. 5
 // P:263-276 at one right-hand side -- the HBM-bound per-time-step MVP).
 // Why: the row kernel above keeps one 4-term chunk per lane in flight and
@@ -4383,8 +4583,36 @@ int launch_bt(Handle* h, HotArgs& ha, cudaStream_t st) {
 }
 
 // Cooperative launch of the FP32 tcgen05 tile kernel (one CTA of 8 warps per SM).
+int launch_bt_tc2(Handle* h, HotArgs& ha, cudaStream_t st) {
+    DeviceHMat* D = h->dev;
+    const size_t smem = (size_t)kT2Smem;
+    CK(cudaFuncSetAttribute(bt_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bt_tc2_kernel, 384, smem));
+    if (per_sm < 1) return set_error(VF_ECUDA, "bt_tc2_kernel cannot be resident");
+    int nsm = 148;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
+    TArgs b{D->bt_tiles, D->bt_n1, D->bt_n2, D->bt_Whi, D->bt_Wlo, D->bt_src, D->bt_out, (float*)ha.xt0, (float*)ha.Y,
+            D->N, ha.kp, D->bt_ctr, D->ctl};
+    CK(cudaMemsetAsync(D->ctl, 0, offsetof(Ctl, bar_gen), st));
+    void* args[] = {&b};
+    {
+        Timer tm(h, st, 2);
+        CK(cudaLaunchCooperativeKernel((const void*)bt_tc2_kernel, dim3(nsm), dim3(384), args, smem, st));
+    }
+    h->launches_total++;
+    D->last_grid = nsm;
+    return VF_OK;
+}
+#ifndef VF_TC2_DEFAULT
+#define VF_TC2_DEFAULT 0
+#endif
 int launch_bt_tc(Handle* h, HotArgs& ha, cudaStream_t st) {
     DeviceHMat* D = h->dev;
+    {
+        const char* e = getenv("VF_TC2");
+        if (e ? atoi(e) != 0 : VF_TC2_DEFAULT != 0) return launch_bt_tc2(h, ha, st);
+    }
     const size_t smem = (size_t)kTSmem;
     CK(cudaFuncSetAttribute(bt_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
