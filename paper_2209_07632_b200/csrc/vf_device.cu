@@ -1038,7 +1038,13 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
         const int col = (int)(item - r * nchunk) * CW + c * VEC;
         const bool col_ok = col < a.kp;
         T acc[VEC];
-        if (KC == 1 && VEC == 1)
+        if (KC == 1 && VEC == 1 && MODE == M_STEP && a.idx16) {
+            // ROWS iteration (one launch, X rows read-only): the prefetching row
+            // kernel on the interleaved 16-bit layout, after the grid barrier
+            bool t_ready = true;
+            acc[0] = row_accumulate_k1_pf<T>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1], vals, xc, lane, a.N,
+                                             a.idx16, a.seg_base16, nullptr, 0, t_ready);
+        } else if (KC == 1 && VEC == 1)
             // X rows through L1 where they are read-only for the whole launch:
             // matvec, and the one-iteration M_STEP launch (the persistent solve
             // re-writes both buffers across iterations: L2 only)
@@ -3701,7 +3707,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     std::vector<uint16_t> i16;
     std::vector<int32_t> base16;
     int64_t pay16 = 0;
-    const bool use16 = !h->sharded && !getenv("VF_K1_U32");
+    const bool use16 = !getenv("VF_K1_U32");           // sharded handles too (ROWS M_STEP iterations)
     if (use16) {
         const int64_t span16 = getenv("VF_U16_SPAN") ? std::min(65536, std::max(2, atoi(getenv("VF_U16_SPAN")))) : 65536;
         pay16 = D->p1_bytes;                                   // phase 1 unchanged (values, S, V indices)
@@ -4770,6 +4776,7 @@ int iterate_rows(Handle* h, int k, int kp, const void* rho, int clamp, int iters
     CK(cudaMemsetAsync(D->ctl, 0, sizeof(Ctl), st));
     HotArgs a = hot_args(D, kp, k);
     a.E = D->Ep; a.rho = rho; a.Q = D->Qp; a.iters = iters; a.clamp = clamp; a.tol = tol;
+    if (kp == 1 && D->idx16) { a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16; }
     const int batch = 4;
     for (int launched = 0;;) {
         for (int b = 0; b < batch; ++b) {
