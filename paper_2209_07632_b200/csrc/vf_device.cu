@@ -2083,6 +2083,51 @@ __global__ void __launch_bounds__(384, 1) bt_tc2_kernel(TArgs a) {
     for (int phase = 1; phase <= 2; ++phase) {
         const int nt = phase == 1 ? a.n1 : a.n2, base = phase == 1 ? 0 : a.n1;
         const int nunits = nt * ncb;
+        if (warp == 0) {
+            // ---- producer, flattened over (unit, slice): the source indices of the
+            // next slice (and the next unit's tile descriptor) are loaded while the
+            // current slice's copies are issued, so no dependent global load sits
+            // between a freed stage slot and its refill
+            auto next_unit = [&](int un) {                 // next unit >= un with slices, or nunits
+                while (un < nunits) {
+                    const BTile Bq = a.tiles[base + un / ncb];
+                    if (Bq.K > 0) return un;
+                    un += gridDim.x;
+                }
+                return nunits;
+            };
+            int un = next_unit(blockIdx.x), sl = 0;
+            BTile B = un < nunits ? a.tiles[base + un / ncb] : BTile{};
+            int32_t row = (un < nunits && lane < min(kTS, B.K)) ? a.src[B.s_off + lane] : 0;
+            while (un < nunits) {
+                const int nsl = (B.K + kTS - 1) / kTS;
+                const int cb = (un % ncb) * 128;
+                // next cursor and its indices (in flight during this slice's issue)
+                int un2 = un, sl2 = sl + 1;
+                BTile B2 = B;
+                if (sl2 >= nsl) {
+                    un2 = next_unit(un + gridDim.x);
+                    sl2 = 0;
+                    if (un2 < nunits) B2 = a.tiles[base + un2 / ncb];
+                }
+                int32_t row2 = 0;
+                if (un2 < nunits) {
+                    const int j2 = sl2 * kTS + lane;
+                    if (lane < kTS && j2 < B2.K) row2 = a.src[B2.s_off + j2];
+                }
+                const int st = g % kT2S;
+                if (g >= (uint32_t)kT2S) tc_wait(&sempty[st], ((g / kT2S) - 1) & 1);
+                const int j0 = sl * kTS, n = min(kTS, B.K - j0);
+                if (lane == 0) t2_expect(&full[st], (unsigned)(n * 512 + 2 * kTB));
+                __syncwarp();
+                if (lane < n) t2_bulk(slot_raw(st) + lane * 512, a.XT + (int64_t)row * a.kp + cb, 512, &full[st]);
+                const int64_t wo = B.w_off + (int64_t)sl * kTS * 16;
+                if (lane == 0) t2_bulk(slot_w(st, 0), a.Whi + wo, kTB, &full[st]);
+                if (lane == 1) t2_bulk(slot_w(st, 1), a.Wlo + wo, kTB, &full[st]);
+                ++g;
+                un = un2; sl = sl2; B = B2; row = row2;
+            }
+        } else
         for (int un = blockIdx.x; un < nunits; un += gridDim.x) {
             const int it = un / ncb, cb = (un - it * ncb) * 128;
             const BTile B = a.tiles[base + it];
@@ -2098,23 +2143,7 @@ __global__ void __launch_bounds__(384, 1) bt_tc2_kernel(TArgs a) {
                 }
                 continue;
             }
-            const int32_t* S = a.src + B.s_off;
-            if (warp == 0) {                               // ---- producer
-                for (int sl = 0; sl < nsl; ++sl, ++g) {
-                    const int st = g % kT2S;
-                    if (g >= (uint32_t)kT2S) tc_wait(&sempty[st], ((g / kT2S) - 1) & 1);
-                    const int j0 = sl * kTS, n = min(kTS, B.K - j0);
-                    if (lane == 0) t2_expect(&full[st], (unsigned)(n * 512 + 2 * kTB));
-                    __syncwarp();
-                    if (lane < n) {
-                        const int64_t row = S[j0 + lane];
-                        t2_bulk(slot_raw(st) + lane * 512, a.XT + row * a.kp + cb, 512, &full[st]);
-                    }
-                    const int64_t wo = B.w_off + (int64_t)sl * kTS * 16;
-                    if (lane == 0) t2_bulk(slot_w(st, 0), a.Whi + wo, kTB, &full[st]);
-                    if (lane == 1) t2_bulk(slot_w(st, 1), a.Wlo + wo, kTB, &full[st]);
-                }
-            } else if (warp >= 4 && warp < 8) {            // ---- split + transpose
+            if (warp >= 4 && warp < 8) {                   // ---- split + transpose
                 const int ts = t - 128;
                 for (int sl = 0; sl < nsl; ++sl, ++g) {
                     const int st = g % kT2S, ab = g % kT2A;
