@@ -12,8 +12,9 @@ else:
     V, F = sg.cfg3_mesh(n=n, crater_D=1000.0 * n / 256)
     M = vf.ViewFactorMatrix.build(V, F, 1e-5)
     M.save(fhat)
-X = torch.from_numpy(np.ascontiguousarray(sg.random_rhs(M.N, k).T)).cuda().T
-Y = torch.empty((k, M.N), dtype=torch.float64, device="cuda").T
+tdt = torch.float32 if M.refresh()["dtype"] == vf.VF_F32 else torch.float64
+X = torch.from_numpy(np.ascontiguousarray(sg.random_rhs(M.N, k).T)).to("cuda", tdt).T
+Y = torch.empty((k, M.N), dtype=tdt, device="cuda").T
 for _ in range(4):
     M.matvec(X, Y)
 torch.cuda.synchronize()
