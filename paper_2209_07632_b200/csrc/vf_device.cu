@@ -2034,7 +2034,13 @@ __global__ void __launch_bounds__(256, VF_TC_CTAS) bt_tc_kernel(TArgs a) {
 // parity is a function of the running slice / unit counters.  Phase-1
 // outputs (T rows, written with st.global) are made visible to the phase-2
 // bulk copies (async proxy) by fence.proxy.async + the grid barrier.
-constexpr int kT2S = 4;                            // stage slots
+#ifndef VF_T2S
+#define VF_T2S 4
+#endif
+#ifndef VF_T2_LDGSTS
+#define VF_T2_LDGSTS 0      // producer copies with 16-B cp.async (LDGSTS) + mbarrier arrive instead of bulk copies
+#endif
+constexpr int kT2S = VF_T2S;                       // stage slots
 constexpr int kT2A = 2;                            // A pairs
 constexpr int kT2Slot = kTRaw + 2 * kTB;           // raw X slice + W hi + W lo
 constexpr int kT2Smem = kT2S * kT2Slot + kT2A * 2 * kTA;
@@ -2064,7 +2070,7 @@ __global__ void __launch_bounds__(384, 1) bt_tc2_kernel(TArgs a) {
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (t == 32) {
-        for (int i = 0; i < kT2S; ++i) { t2_init(&full[i], 1); t2_init(&sempty[i], 1); }
+        for (int i = 0; i < kT2S; ++i) { t2_init(&full[i], VF_T2_LDGSTS ? 32 : 1); t2_init(&sempty[i], 1); }
         for (int i = 0; i < kT2A; ++i) { t2_init(&afull[i], 4); t2_init(&aempty[i], 1); }
         for (int i = 0; i < 2; ++i) { t2_init(&accfull[i], 1); t2_init(&accempty[i], 4); }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -2118,12 +2124,26 @@ __global__ void __launch_bounds__(384, 1) bt_tc2_kernel(TArgs a) {
                 const int st = g % kT2S;
                 if (g >= (uint32_t)kT2S) tc_wait(&sempty[st], ((g / kT2S) - 1) & 1);
                 const int j0 = sl * kTS, n = min(kTS, B.K - j0);
+                const int64_t wo = B.w_off + (int64_t)sl * kTS * 16;
+#if VF_T2_LDGSTS
+                // one 512-B source row per warp instruction (lane = 16-B piece), then
+                // the weights; each lane's arrive fires when its copies have landed
+                for (int j = 0; j < n; ++j) {
+                    const int32_t rj = __shfl_sync(0xffffffffu, row, j);
+                    cpa<16>(slot_raw(st) + j * 512 + lane * 16, a.XT + (int64_t)rj * a.kp + cb + lane * 4, 16);
+                }
+                for (int q = lane; q < 2 * (kTB / 16); q += 32) {
+                    const int h = q / (kTB / 16), u2 = q - h * (kTB / 16);
+                    cpa<16>(slot_w(st, h) + u2 * 16, (h ? a.Wlo : a.Whi) + wo + u2 * 4, 16);
+                }
+                asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(tc_smem(&full[st])) : "memory");
+#else
                 if (lane == 0) t2_expect(&full[st], (unsigned)(n * 512 + 2 * kTB));
                 __syncwarp();
                 if (lane < n) t2_bulk(slot_raw(st) + lane * 512, a.XT + (int64_t)row * a.kp + cb, 512, &full[st]);
-                const int64_t wo = B.w_off + (int64_t)sl * kTS * 16;
                 if (lane == 0) t2_bulk(slot_w(st, 0), a.Whi + wo, kTB, &full[st]);
                 if (lane == 1) t2_bulk(slot_w(st, 1), a.Wlo + wo, kTB, &full[st]);
+#endif
                 ++g;
                 un = un2; sl = sl2; B = B2; row = row2;
             }
@@ -2183,6 +2203,8 @@ __global__ void __launch_bounds__(384, 1) bt_tc2_kernel(TArgs a) {
                     const int st = g % kT2S, ab = g % kT2A;
                     tc_wait(&full[st], (g / kT2S) & 1);
                     tc_wait(&afull[ab], (g / kT2A) & 1);
+                    // weights written by cp.async (generic proxy) -> read by the MMA (async proxy)
+                    if (VF_T2_LDGSTS) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
                     if (lane == 0) {
                         const unsigned ah = tc_smem(abuf(ab, 0)), al = tc_smem(abuf(ab, 1));
