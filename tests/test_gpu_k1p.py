@@ -59,10 +59,10 @@ print(json.dumps(out))
 """
 
 
-def _run(env):
+def _run(env, kernel="pipe"):
     r = subprocess.run([sys.executable, "-c", _CASE.format(root=ROOT)],
                        env=dict({k: v for k, v in os.environ.items() if k != "VF_K1_KERNEL"},
-                                VF_K1_KERNEL="pipe", **env),
+                                VF_K1_KERNEL=kernel, **env),
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     return json.loads(r.stdout.strip().splitlines()[-1])
@@ -116,3 +116,20 @@ def test_k1p_equals_row_kernel_on_product_build():
     assert r.returncode == 0, r.stderr[-3000:]
     d = json.loads(r.stdout.strip().splitlines()[-1])
     assert d["d"] <= 1e-13 and d["ex"] <= 1e-4, d
+
+
+@pytest.mark.parametrize("env", [{}, {"VF_P1_PART": "64"}, {"VF_U16_SPAN": "7"},
+                                 {"VF_P1_PART": "32", "VF_U16_SPAN": "2"}, {"VF_K1_ILV": "0"},
+                                 {"VF_K1_PACK": "1"}, {"VF_K1_OVL": "1"}])
+def test_default_row_kernel_forced_layouts(env):
+    """The default nrhs = 1 kernel (hot_kernel<T,1,1> with the register-prefetching
+    row accumulator on the interleaved 16-bit layout) under the same forced
+    layouts: multi-part phase-1 groups, CSR rows cut into runs of span 7 / 2
+    (runs crossing rounds, rows of many segment batches, interleaved pieces of
+    every size), the plain (non-interleaved) order, per-row packing and the
+    barrier-free hand-over: <= 1e-12 / 1e-5 vs the oracle's Alg. 5 on the same
+    blocks, bitwise repeatable."""
+    out = _run(env, kernel="rows")
+    for name, d in out.items():
+        bound = 1e-12 if name.endswith("f64") else 1e-5
+        assert d["err"] <= bound and d["same"] and d["k1"] > 0, (name, d)

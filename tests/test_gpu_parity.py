@@ -540,3 +540,27 @@ def test_resident_phase2_copies(cfg2_small, tmp_path_factory, monkeypatch, k):
         assert rel(host(B), B0) <= 1e-12
     assert np.array_equal(ys[0], ys[1]) and np.array_equal(ys[0], ys[2])
     assert rel(ys[0], hm.hmatvec(H, X)) <= 1e-12
+
+
+
+@pytest.fixture(scope="module")
+def terrain64():
+    V, F = sg.cfg3_mesh(n=64, crater_D=1000.0 * 64 / 256)     # the configs[2] recipe at 64^2 cells
+    S = oracle.Scene(V, F)
+    M = vf.ViewFactorMatrix.build(V, F, 1e-5)
+    return V, F, S, M
+
+
+@pytest.mark.parametrize("k", [1, 4, 64, 128])
+def test_terrain64_sampled_rows_vs_exact_F(terrain64, k):
+    """configs[2]'s recipe at 64^2 cells (8,192 facets), the product's own
+    device build: sampled rows of Y = F-hat X at nrhs 1 (default row kernel),
+    4 (column split), 64 and 128 (streamed tiles / resident layout) against
+    the same rows of the oracle's exact F (eq. FF-def): <= 10 tol."""
+    V, F, S, M = terrain64
+    X = sg.random_rhs(S.N, k, seed=11)
+    Y = empty(S.N, k)
+    M.matvec(dev(X), Y)
+    rows = np.random.default_rng(9).choice(S.N, 800, replace=False)
+    Yex = oracle.apply_csr(S.F_csr_rows(rows), X)
+    assert rel(host(Y)[rows], Yex) <= 10 * 1e-5
