@@ -444,10 +444,11 @@ def run_gpu(args, rank, world, local_rank):
         flops_launch = flops_iter * n_iters / max(l2, 1)
         bytes_launch = bytes_iter * n_iters / max(l2, 1)
         smax = pk.get("sm_max_mhz", 1965.0)
-        peak_tf = fp64_peak_tflops(smax) if dt == "f64" else fp32_peak_tflops(smax)
+        # res_kernel contracts on the FP64 tensor cores (DMMA; FP32 factors widened to FP64)
+        dmma = bool(info.get("resident"))
+        peak_tf = fp64_peak_tflops(smax) if dt == "f64" or dmma else fp32_peak_tflops(smax)
         ach_tf = flops_launch / (avg * 1e-3) / 1e12 if avg > 0 else 0.0
         ach_gbs = bytes_launch / (avg * 1e-3) / 1e9 if avg > 0 else 0.0
-        dmma = bool(info.get("resident")) and dt == "f64"     # res_kernel contracts on FP64 tensor cores (DMMA)
         traffic, traffic_src = ncu_traffic(f"cfg2_{dt}")
         roof = {"bound": "tensor" if dmma else "alu", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
                 "frac": ach_tf / peak_tf if peak_tf else None, "traffic": traffic, "traffic_source": traffic_src,
@@ -459,7 +460,7 @@ def run_gpu(args, rank, world, local_rank):
                            "Jacobi solve: phase 1 V^T X, grid barrier, phase 2 row-owner accumulate + fused "
                            "epilogue, residual decision; one launch per thermal stage)"),
                 "peak_basis": (("derived FP64 DMMA peak (= the DFMA rate on B200): " if dmma else "derived: ")
-                               + f"148 SM x {64 if dt == 'f64' else 128} {dt.upper()} FMA/clk x 2 x "
+                               + f"148 SM x {64 if dt == 'f64' or dmma else 128} {'F64' if dmma else dt.upper()} FMA/clk x 2 x "
                                f"{smax:.0f} MHz (sm_max of {pk_kind} MEASURED_PEAKS.json); DESIGN.md §7"),
                 "avg_launch_ms": avg, "launches": l2, "applies_per_launch": n_iters / max(l2, 1),
                 "flops_per_apply": flops_iter, "flops_per_launch": flops_launch,
@@ -624,8 +625,8 @@ def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
         # values + S + V row indices + 16-bit CSR offsets), else values + 32-bit indices
         if kp == 1 and stream:
             fh = info["stream_payload_bytes"]
-        elif kp == 1 and info.get("k1_payload_bytes", 0) > 0 and not rows_mode:
-            fh = info["k1_payload_bytes"]
+        elif kp == 1 and info.get("k1_payload_bytes", 0) > 0:
+            fh = info["k1_payload_bytes"]             # (ROWS M_STEP launches read the same 16-bit layout)
         else:
             fh = info["p1_bytes"] + info["p2_bytes"]
         return (fh + (info["p1_src_rows"] + info["p2_src_rows"]) * kp * w
@@ -647,7 +648,8 @@ def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
     if max(chunks) > 2:
         smax = pk.get("sm_max_mhz", 1965.0)
         tiles = info.get("tiles", 0) > 0 and max(chunks) > 8
-        if tiles and dt == "f32":
+        tc = os.environ.get("VF_TC", "0") not in ("", "0") or os.environ.get("VF_TC2", "0") not in ("", "0")
+        if tiles and dt == "f32" and tc:
             # tcgen05 kind::tf32 with 3xTF32: the measured bf16 peak x the nominal tf32/bf16 ratio
             # (1.1 / 2.25 PFLOP/s dense), / 3 MMAs per useful product
             peak_tf = pk.get("bf16_tflops", 1619.6) * (1.1 / 2.25) / 3.0
@@ -655,12 +657,12 @@ def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
                      "peak_basis": f"3xTF32 on tcgen05: {pk_kind} MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 "
                                    "(nominal tf32/bf16 dense ratio) / 3"}
         else:
-            peak_tf = fp64_peak_tflops(smax) if dt == "f64" else fp32_peak_tflops(smax)
-            dmma = tiles and dt == "f64"
+            dmma = tiles                      # bt_kernel<double|float>: DMMA (FP32 widened to FP64)
+            peak_tf = fp64_peak_tflops(smax) if dt == "f64" or dmma else fp32_peak_tflops(smax)
             bound = {"bound": "tensor" if dmma else "alu", "achieved": ach_tf, "peak": peak_tf, "unit": "TFLOP/s",
                      "frac": ach_tf / peak_tf,
                      "peak_basis": (("derived FP64 DMMA peak (= the DFMA rate on B200): " if dmma else "derived: ")
-                                    + f"148 SM x {64 if dt == 'f64' else 128} FMA/clk x 2 x {smax:.0f} MHz "
+                                    + f"148 SM x {64 if dt == 'f64' or dmma else 128} FMA/clk x 2 x {smax:.0f} MHz "
                                       f"(sm_max of {pk_kind} MEASURED_PEAKS.json)")}
     else:
         bound = {"bound": "hbm", "achieved": ach_gbs, "peak": hbm, "unit": "GB/s", "frac": ach_gbs / hbm,
@@ -679,6 +681,10 @@ def terrain_roofline(info, k, dt, tm, steps, rows_mode, pk, pk_kind, workload):
     elif info.get("tiles", 0) > 0 and dt == "f64":
         kern = ("bt_kernel (streamed 16-row tiles, [K][16] weights x staged XT rows on FP64 tensor cores, DMMA "
                 "m8n8k4; phase 1 T tiles, grid barrier, phase 2 row tiles)")
+    elif info.get("tiles", 0) > 0 and not (os.environ.get("VF_TC", "0") not in ("", "0")
+                                           or os.environ.get("VF_TC2", "0") not in ("", "0")):
+        kern = ("bt_kernel<float> (streamed 16-row tiles, FP32 [K][16] weights x staged FP32 XT rows widened to FP64 "
+                "in registers, DMMA m8n8k4 with FP64 accumulation, one rounding to FP32 at the store)")
     elif info.get("tiles", 0) > 0:
         kern = ("bt_tc_kernel (streamed 16-row tiles on tcgen05 kind::tf32, TMEM accumulator, 3xTF32 split; "
                 "phase 1 T tiles, grid barrier, phase 2 row tiles)")

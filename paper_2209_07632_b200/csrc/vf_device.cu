@@ -66,6 +66,17 @@ struct Seg {                            // one run of a row's terms
     int32_t kind;                       // 0 contiguous, 1 gather
 };
 
+// compact descriptor of a run in the 16-bit nrhs = 1 row layout (16 B, one
+// vector load per lane): value offset and source (XT row, or offset into the
+// 16-bit CSR offsets) as 32-bit, len | kind << 31, the CSR run's column base.
+// Built at upload when every field fits (else the u32 layout is used)
+struct __align__(16) SegC {
+    uint32_t off;
+    uint32_t src;
+    int32_t lk;
+    int32_t base;
+};
+
 struct Ctl {                            // device-side loop state
     int iter;                           // completed iterations
     int done;
@@ -342,6 +353,25 @@ __device__ __forceinline__ int4 ld_stream_i4(const int4* p) {
     return __ldg(p);
 #endif
 }
+template <typename T> __device__ __forceinline__ T ld_stream_s(const T* p);
+template <> __device__ __forceinline__ double ld_stream_s<double>(const double* p) {
+#if VF_K1_NA
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;\n" : "=d"(v) : "l"(p), "l"(l2_evict_first()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
+template <> __device__ __forceinline__ float ld_stream_s<float>(const float* p) {
+#if VF_K1_NA
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;\n" : "=f"(v) : "l"(p), "l"(l2_evict_first()));
+    return v;
+#else
+    return __ldg(p);
+#endif
+}
 template <typename T> struct V4;
 template <> struct V4<double> {
     static __device__ __forceinline__ void ld(const double* p, double* v) {
@@ -541,6 +571,9 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
 #ifndef VF_K1_L2PF
 #define VF_K1_L2PF 0        // rounds ahead for the bulk L2 prefetch of a batch's values (0 = off)
 #endif
+#ifndef VF_K1_TL1
+#define VF_K1_TL1 0         // nrhs = 1 rows: T-row gathers through L1 (A/B option)
+#endif
 #ifndef VF_K1_ROWPF
 #define VF_K1_ROWPF 0       // row descriptors pipelined over three rows (measured slower: 0.845 vs 0.809 ms)
 #endif
@@ -552,7 +585,7 @@ struct K1Round {
     int32_t f;          // valid terms (0..4) | CSR << 3 | vector x << 4 | X rows (L1) << 5
 };
 template <typename T>
-__device__ __forceinline__ void k1_fetch(K1Round<T>& R, int cc, int ns, int total, int excl, const Seg& my, int32_t my_base,
+__device__ __forceinline__ void k1_fetch(K1Round<T>& R, int cc, int ns, int total, int excl, const SegC& my,
                                          const T* __restrict__ vals, const uint16_t* __restrict__ idx16, int64_t nx,
                                          int lane) {
     constexpr unsigned FULL = 0xffffffffu;
@@ -563,12 +596,13 @@ __device__ __forceinline__ void k1_fetch(K1Round<T>& R, int cc, int ns, int tota
         const int e = __shfl_sync(FULL, excl, cand & 31);
         if (cand < ns && e <= cc) g = cand;
     }
-    const int64_t g_off = __shfl_sync(FULL, my.val_off, g);
-    const int64_t g_src = __shfl_sync(FULL, my.src, g);
-    const int g_len = __shfl_sync(FULL, my.len, g);
-    const int g_kind = __shfl_sync(FULL, my.kind, g);
+    const int64_t g_off = (int64_t)__shfl_sync(FULL, my.off, g);
+    const int64_t g_src = (int64_t)__shfl_sync(FULL, my.src, g);
+    const int g_lk = __shfl_sync(FULL, my.lk, g);
+    const int g_len = g_lk & 0x7fffffff;
+    const int g_kind = (int)((unsigned)g_lk >> 31);
     const int g_excl = __shfl_sync(FULL, excl, g);
-    const int g_base = __shfl_sync(FULL, my_base, g);
+    const int g_base = __shfl_sync(FULL, my.base, g);
     if (cc < total) {
         const int e = (cc - g_excl) * 4;
         const int nv = min(4, g_len - e);
@@ -605,10 +639,12 @@ __device__ __forceinline__ void k1_consume(const K1Round<T>& R, const T* xt, T& 
             for (int u = 0; u < 4; ++u) x[u] = XLD(xt + R.xb + (u < nv ? u : 0));
         }
     } else {                                             // T rows (written by phase 1 of this launch): L2
-        if (R.f & 16) XV4<T, false>::ld(xt + R.xb, x);
+        // (VF_K1_TL1=1: through L1 -- no SM reads a T row before the phase barrier /
+        // the finished-item wait, so no L1 holds a stale line of one)
+        if (R.f & 16) XV4<T, VF_K1_TL1 != 0>::ld(xt + R.xb, x);
         else {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) x[u] = __ldcg(xt + R.xb + (u < nv ? u : 0));
+            for (int u = 0; u < 4; ++u) x[u] = VF_K1_TL1 ? XLD(xt + R.xb + (u < nv ? u : 0)) : __ldcg(xt + R.xb + (u < nv ? u : 0));
         }
     }
 #pragma unroll
@@ -637,19 +673,20 @@ __device__ __forceinline__ void k1_wait_t(const int32_t* p1done, int32_t n, int 
     __syncwarp();
 }
 template <typename T>
-__device__ __forceinline__ T row_accumulate_k1_pf(const Seg* __restrict__ segs, int64_t s0, int64_t s1,
+__device__ __forceinline__ T row_accumulate_k1_pf(const SegC* __restrict__ segc, int64_t s0, int64_t s1,
                                                   const T* __restrict__ vals, const T* xt, int lane, int64_t nx,
-                                                  const uint16_t* __restrict__ idx16,
-                                                  const int32_t* __restrict__ seg_base, const int32_t* p1done,
+                                                  const uint16_t* __restrict__ idx16, const int32_t* p1done,
                                                   int32_t n_p1, bool& t_ready) {
     constexpr unsigned FULL = 0xffffffffu;
     T acc0 = T(0), acc1 = T(0);
     for (int64_t sb = s0; sb < s1; sb += 32) {
         const int ns = (int)(s1 - sb < 32 ? s1 - sb : 32);
-        Seg my{0, 0, 0, 0};
-        int32_t my_base = 0;
-        if (lane < ns) { my = segs[sb + lane]; my_base = seg_base[sb + lane]; }
-        const int nch = (my.len + 3) >> 2;
+        SegC my{0u, 0u, 0, 0};
+        if (lane < ns) {
+            const int4 d = ld_stream_i4(reinterpret_cast<const int4*>(segc + sb + lane));
+            my = SegC{(uint32_t)d.x, (uint32_t)d.y, d.z, d.w};
+        }
+        const int nch = ((my.lk & 0x7fffffff) + 3) >> 2;
         int incl = nch;
 #pragma unroll
         for (int off = 1; off < 32; off <<= 1) {
@@ -663,8 +700,8 @@ __device__ __forceinline__ T row_accumulate_k1_pf(const Seg* __restrict__ segs, 
         // values sit near vb + 4 b chunks; lane 0 prefetches round b + VF_K1_L2PF's
         // values into L2 with one bulk prefetch, so the HBM stream runs ahead of the
         // warp's register-limited loads
-        const int64_t vb = __shfl_sync(FULL, my.val_off, 0);
-        const int64_t ve = __shfl_sync(FULL, my.val_off + my.len, ns - 1);
+        const int64_t vb = (int64_t)__shfl_sync(FULL, my.off, 0);
+        const int64_t ve = (int64_t)__shfl_sync(FULL, my.off, ns - 1) + __shfl_sync(FULL, my.lk & 0x7fffffff, ns - 1);
         auto l2pf = [&](int b) {
             if (lane == 0) {
                 const int64_t a0 = vb + (int64_t)(b + 32 * VF_K1_L2PF) * 4;
@@ -677,16 +714,16 @@ __device__ __forceinline__ T row_accumulate_k1_pf(const Seg* __restrict__ segs, 
         l2pf(0);
 #endif
         K1Round<T> cur;
-        k1_fetch<T>(cur, lane, ns, total, excl, my, my_base, vals, idx16, nx, lane);
+        k1_fetch<T>(cur, lane, ns, total, excl, my, vals, idx16, nx, lane);
 #if VF_K1_PFD >= 2
         // two rounds in flight: rounds i + 1 and i + 2 are fetched before round i's gathers
         if (32 < total) {
             K1Round<T> nx1;
-            k1_fetch<T>(nx1, 32 + lane, ns, total, excl, my, my_base, vals, idx16, nx, lane);
+            k1_fetch<T>(nx1, 32 + lane, ns, total, excl, my, vals, idx16, nx, lane);
             int base = 64;
             for (; base < total; base += 32) {
                 K1Round<T> nx2;
-                k1_fetch<T>(nx2, base + lane, ns, total, excl, my, my_base, vals, idx16, nx, lane);
+                k1_fetch<T>(nx2, base + lane, ns, total, excl, my, vals, idx16, nx, lane);
                 if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
                 k1_consume<T>(cur, xt, acc0, acc1);
                 cur = nx1;
@@ -703,7 +740,7 @@ __device__ __forceinline__ T row_accumulate_k1_pf(const Seg* __restrict__ segs, 
 #if VF_K1_L2PF
             l2pf(base);
 #endif
-            k1_fetch<T>(nxt, base + lane, ns, total, excl, my, my_base, vals, idx16, nx, lane);
+            k1_fetch<T>(nxt, base + lane, ns, total, excl, my, vals, idx16, nx, lane);
             if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
             k1_consume<T>(cur, xt, acc0, acc1);
             cur = nxt;
@@ -811,6 +848,7 @@ struct HotArgs {
     const int64_t* p2_segptr16;
     const uint16_t* idx16;
     const int32_t* seg_base16;
+    const SegC* segc16;           // the same runs as compact descriptors (row_accumulate_k1_pf)
     unsigned long long* trace;    // optional: [iter][event][cta] globaltimer (VF_TRACE_FILE)
     int trace_iters;
 };
@@ -857,12 +895,21 @@ __device__ __forceinline__ void solve_epilogue(const HotArgs& a, const T* xc, T*
 #define VF_P1_UNROLL 1
 #endif
 constexpr int kP1Unroll = VF_P1_UNROLL;
-template <typename T>
+// nrhs = 1 phase 1: V values streamed like the phase-2 runs (L1::no_allocate,
+// L2 evict-first: VF_P1_NA) and, where X is read-only for the launch (matvec,
+// ROWS step), x_j through L1 (VF_P1_L1); same loads, same FMA order
+#ifndef VF_P1_NA
+#define VF_P1_NA 1
+#endif
+#ifndef VF_P1_L1
+#define VF_P1_L1 1
+#endif
+template <typename T, bool L1X = false>
 __device__ __forceinline__ void phase1_part_k1(const HotArgs& a, T* xc, int64_t pi, int lane);
-template <typename T>
+template <typename T, bool L1X = false>
 __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_t gwarp, int lane) {
     for (int32_t q = a.s1_ptr[gwarp]; q < a.s1_ptr[gwarp + 1]; ++q) {
-        phase1_part_k1<T>(a, xc, a.s1_items[q], lane);
+        phase1_part_k1<T, L1X>(a, xc, a.s1_items[q], lane);
         if (a.p1done) {                               // release: this item's T rows (or part sums) are written
             __threadfence();
             __syncwarp();
@@ -871,7 +918,7 @@ __device__ __forceinline__ void phase1_groups_k1(const HotArgs& a, T* xc, int64_
     }
 }
 // one phase-1 part item pi: (row group of one SVD block, part of its V rows)
-template <typename T>
+template <typename T, bool L1X>
 __device__ __forceinline__ void phase1_part_k1(const HotArgs& a, T* xc, int64_t pi, int lane) {
     const T* vals = static_cast<const T*>(a.vals);
     {
@@ -896,10 +943,10 @@ __device__ __forceinline__ void phase1_part_k1(const HotArgs& a, T* xc, int64_t 
 #pragma unroll kP1Unroll
             for (int j = j0 + lane; j < jn; j += 32) {
                 const int64_t row = sg.kind ? (int64_t)__ldg(a.idx + sg.src + j) : sg.src + j;
-                const T x = __ldcg(xc + row);
+                const T x = (VF_P1_L1 && L1X) ? XLD(xc + row) : __ldcg(xc + row);
                 T v[H];
 #pragma unroll
-                for (int r = 0; r < H; ++r) v[r] = vo[r] >= 0 ? __ldg(vb + vo[r] + j) : T(0);
+                for (int r = 0; r < H; ++r) v[r] = vo[r] >= 0 ? (VF_P1_NA ? ld_stream_s<T>(vb + vo[r] + j) : __ldg(vb + vo[r] + j)) : T(0);
 #pragma unroll
                 for (int r = 0; r < H; ++r) acc[r] = fma(v[r], x, acc[r]);
             }
@@ -1003,7 +1050,7 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
                 const int32_t rC = tC < n2 ? a.p2_order[tC] : 0;
                 if (lane == 0) fut = atomicAdd(a.qctr, 1);  // ticket D
                 if (tB < n2) { sbB = (int32_t)a.p2_segptr16[rB]; s1B = (int32_t)a.p2_segptr16[rB + 1]; oB = a.p2_rows[rB]; }
-                const T acc = row_accumulate_k1_pf<T>(a.segs16, sbA, s1A, vals, xc, lane, a.N, a.idx16, a.seg_base16,
+                const T acc = row_accumulate_k1_pf<T>(a.segc16, sbA, s1A, vals, xc, lane, a.N, a.idx16,
                                                       a.p1done, a.n_p1items, t_ready);
                 if (lane == 0) static_cast<T*>(a.Y)[oA] = acc;
                 tA = tB; sbA = sbB; s1A = s1B; oA = oB;
@@ -1019,8 +1066,8 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
             const int64_t r = a.p2_order[nxt];
             int fut = 0;
             if (lane == 0) fut = atomicAdd(a.qctr, 1);
-            const T acc = (VF_K1_PF && a.idx16) ? row_accumulate_k1_pf<T>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
-                                                                           vals, xc, lane, a.N, a.idx16, a.seg_base16,
+            const T acc = (VF_K1_PF && a.idx16) ? row_accumulate_k1_pf<T>(a.segc16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
+                                                                           vals, xc, lane, a.N, a.idx16,
                                                                            a.p1done, a.n_p1items, t_ready)
                         : a.idx16 ? row_accumulate_k1<T, VF_MV_L1 != 0>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
                                                                          vals, a.idx, xc, lane, a.N, nullptr, nullptr,
@@ -1042,8 +1089,8 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
             // ROWS iteration (one launch, X rows read-only): the prefetching row
             // kernel on the interleaved 16-bit layout, after the grid barrier
             bool t_ready = true;
-            acc[0] = row_accumulate_k1_pf<T>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1], vals, xc, lane, a.N,
-                                             a.idx16, a.seg_base16, nullptr, 0, t_ready);
+            acc[0] = row_accumulate_k1_pf<T>(a.segc16, a.p2_segptr16[r], a.p2_segptr16[r + 1], vals, xc, lane, a.N,
+                                             a.idx16, nullptr, 0, t_ready);
         } else if (KC == 1 && VEC == 1)
             // X rows through L1 where they are read-only for the whole launch:
             // matvec, and the one-iteration M_STEP launch (the persistent solve
@@ -1337,6 +1384,11 @@ struct ResCursor {
     RGroup G;
 };
 
+// FP32 resident batches on DMMA as well (VF_RES_F32_DMMA=0: the FFMA loop)
+#ifndef VF_RES_F32_DMMA
+#define VF_RES_F32_DMMA 1
+#endif
+template <typename T> constexpr bool kResDmma = std::is_same<T, double>::value || VF_RES_F32_DMMA != 0;
 template <typename T, int PHASE, int MODE>
 __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, const T* W, const int32_t* S, T* Xs,
                                           T* xc, T* xn, double* sred, double* tile, double* red, double* xch,
@@ -1403,19 +1455,23 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
         const T* X = Xs + (step % kRS) * kKS * 16;
         const RGroup& G = cur.G;
         const int j0 = cur.sl * kKS, n = min(kKS, G.K - j0);
-        if constexpr (std::is_same<T, double>::value) {
+        if constexpr (kResDmma<T>) {
             // the 16 x 16 tile as 4 DMMA 8x8 tiles; warp w takes k-blocks
             // w, w + 8, ... of the slice (A = W^T from the resident block, B = the
-            // staged XT rows); partial tiles are summed over warps at the item end
+            // staged XT rows); partial tiles are summed over warps at the item end.
+            // FP32 factors: widened to FP64 in registers (exact products, FP64
+            // sums, one rounding at the store); the [K][16] swizzle is also
+            // conflict-free for 4-byte elements (lanes kr = 0..3 -> banks
+            // 0-7, 16-23, 8-15, 24-31)
             const int lane = t & 31, warp = t >> 5;
             const int kr = lane & 3, mn = lane >> 2;
-            const double* wb = W + G.w_off + (int64_t)j0 * 16;
+            const T* wb = W + G.w_off + (int64_t)j0 * 16;
             for (int kb = warp * 4; kb < n; kb += 4 * kRW) {
                 const int j = kb + kr;
                 const bool ok = j < n;
                 const int sw = 4 * kr;                      // (j & 3) == kr: swizzled columns
-                const double a0 = ok ? wb[j * 16 + (mn ^ sw)] : 0.0, a1 = ok ? wb[j * 16 + ((8 + mn) ^ sw)] : 0.0;
-                const double b0 = ok ? X[j * 16 + (mn ^ sw)] : 0.0, b1 = ok ? X[j * 16 + ((8 + mn) ^ sw)] : 0.0;
+                const double a0 = ok ? (double)wb[j * 16 + (mn ^ sw)] : 0.0, a1 = ok ? (double)wb[j * 16 + ((8 + mn) ^ sw)] : 0.0;
+                const double b0 = ok ? (double)X[j * 16 + (mn ^ sw)] : 0.0, b1 = ok ? (double)X[j * 16 + ((8 + mn) ^ sw)] : 0.0;
                 dmma884(dacc[0], a0, b0);
                 dmma884(dacc[1], a0, b1);
                 dmma884(dacc[2], a1, b0);
@@ -1451,7 +1507,7 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
         if (j0 + n >= G.K) {                               // last slice: epilogue of item (G, chunk)
             T q = acc0 + acc1;
             acc0 = acc1 = T(0);
-            if constexpr (std::is_same<T, double>::value) {   // sum the warps' DMMA tiles in warp order
+            if constexpr (kResDmma<T>) {                       // sum the warps' DMMA tiles in warp order
                 const int lane = t & 31, warp = t >> 5;
 #pragma unroll
                 for (int tl = 0; tl < 4; ++tl) {
@@ -1465,7 +1521,7 @@ __device__ __forceinline__ void res_phase(const HotArgs& a, const ResArgs& r, co
                     const int ln = (rr & 7) * 4 + ((cc & 7) >> 1), ii = cc & 1;
                     double sum = 0.0;
                     for (int w2 = 0; w2 < kRW; ++w2) sum += red[((w2 * 4 + tl) * 32 + ln) * 2 + ii];
-                    q = sum;
+                    q = (T)sum;
                 }
             }
             if (PHASE == 2 && G.role >= 0) {                 // K split over the cluster pair
@@ -1615,9 +1671,6 @@ __global__ void __launch_bounds__(kRW * 32, 1) res_kernel(HotArgs a, ResArgs r) 
 // phase 2); each output element is summed by one warp in a fixed order and
 // K-parts are added in part order: bitwise reproducible.
 constexpr int kBCols = 128;         // columns per pass over a tile
-#ifndef VF_BT_ACC2
-#define VF_BT_ACC2 0
-#endif
 #ifndef VF_BT_HALF
 #define VF_BT_HALF 0        // tiles of <= 8 rows: only the upper 8x8 DMMA tiles (measured 8.89 vs 8.77 ms at k=128: off)
 #endif
@@ -1632,23 +1685,41 @@ struct BTile {
     int64_t s_off;                  // K source XT rows
     int64_t out_off;                // 16 output rows (tree rows, or T rows for phase 1)
 };
+template <typename TS>
 struct BArgs {
     const BTile* tiles;             // phase-1 tiles [0, n1), then phase-2 tiles [n1, n1 + n2)
     int32_t n1, n2;
-    const double* W;
+    const TS* W;
     const int32_t* src;
     const int32_t* outrow;
-    double* XT;                     // (N + NT) x kp, row-major, tree order
-    double* Y;                      // N x kp
+    TS* XT;                         // (N + NT) x kp, row-major, tree order
+    TS* Y;                          // N x kp
     int64_t N;
     int kp;
     int32_t* ctr;                   // [0] phase-1 queue, [1] phase-2 queue
     Ctl* ctl;
 };
+// shared-memory swizzles of the staged slices (element (row j, column c) at
+// j * width + (c ^ s(j))), chosen so the DMMA fragment loads of a warp (lane =
+// 4 mn + kr reads row j = 4 ks + kr, column mn or 8 + mn of a 16-column chunk)
+// hit 32 distinct banks.  FP64 (2 banks per element): s = 4 (j & 3).  FP32
+// storage (1 bank per element): 8-column groups, s = 8 (j & 3) for rows of >= 32
+// columns, s = 8 ((j >> 1) & 1) for 16-column rows (the weights)
+template <typename TS> __host__ __device__ __forceinline__ int bt_xsw(int j, int width) {
+    return sizeof(TS) == 8 ? 4 * (j & 3) : (width >= 32 ? 8 * (j & 3) : 8 * ((j >> 1) & 1));
+}
+template <typename TS> __host__ __device__ __forceinline__ int bt_wsw(int j) { return bt_xsw<TS>(j, 16); }
 
-__global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
+// TS = double: FP64 F-hat.  TS = float: FP32 factors and right-hand sides,
+// widened to FP64 in registers for the DMMA (exact) and accumulated in FP64,
+// rounded once to FP32 at the store -- the FP32 batched path on the FP64
+// tensor cores, half the staged bytes of the FP64 path
+template <typename TS>
+__global__ void __launch_bounds__(256, 2) bt_kernel(BArgs<TS> a) {
     extern __shared__ __align__(16) double bsm[];
     __shared__ int s_item;
+    constexpr int EPC = 16 / (int)sizeof(TS);           // elements per 16-B copy
+    constexpr int CPR = (int)sizeof(TS);                // 16-B copies per 16-element weight row
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int kr = lane & 3, mn = lane >> 2;
     for (int phase = 1; phase <= 2; ++phase) {
@@ -1660,7 +1731,7 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
             const int it = s_item;
             if (it >= nt) break;
             const BTile B = a.tiles[base + it];
-            const double* Wt = a.W + B.w_off;
+            const TS* Wt = a.W + B.w_off;
             const int32_t* S = a.src + B.s_off;
             for (int cb = 0; cb < a.kp; cb += kBCols) {
                 const int KPB = min(kBCols, a.kp - cb);          // 16, 32, 64 or 128 columns
@@ -1668,9 +1739,9 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                 const int nsl = (B.K + KS - 1) / KS;
                 const int nch = KPB >> 4, nkp = 8 / nch;
                 const int cw = warp % nch, pw = warp / nch;
-                double* Wsm = bsm;                                 // [kBStages][KS][16]
-                double* Xsm = bsm + kBStages * KS * 16;            // [kBStages][KS][KPB] (fits kBStages x kBSlice)
-                const int per = KPB >> 1;                          // 16-B copies per staged row (<= 4 rows per thread)
+                TS* Wsm = reinterpret_cast<TS*>(bsm);              // [kBStages][KS][16]
+                TS* Xsm = Wsm + kBStages * KS * 16;                // [kBStages][KS][KPB] (fits kBStages x kBSlice doubles)
+                const int per = KPB / EPC;                         // 16-B copies per staged row (<= 4 rows per thread)
                 // source rows of a slice, fetched into registers one slice before they are staged
                 // (the XT copies' addresses depend on them: no global-load latency in the staging)
                 auto load_idx = [&](int sl, int32_t* rg) {
@@ -1683,27 +1754,24 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                 };
                 auto stage = [&](int sl, int slot, const int32_t* rg) {
                     const int j0 = sl * KS, n = min(KS, B.K - j0);
-                    double* wd = Wsm + slot * KS * 16;
-                    double* xd = Xsm + slot * KS * KPB;
-                    for (int op = t; op < KS * 8; op += 256) {     // 16-B copies of the weight slice
-                        const int j = op >> 3;
-                        cpa<16>(wd + op * 2, Wt + (int64_t)j0 * 16 + op * 2, j < n ? 16 : 0);
+                    TS* wd = Wsm + slot * KS * 16;
+                    TS* xd = Xsm + slot * KS * KPB;
+                    for (int op = t; op < KS * CPR; op += 256) {   // 16-B copies of the weight slice
+                        const int j = op / CPR;
+                        cpa<16>(wd + op * EPC, Wt + (int64_t)j0 * 16 + op * EPC, j < n ? 16 : 0);
                     }
 #pragma unroll
                     for (int m = 0; m < 4; ++m) {
                         const int op = t + 256 * m;
                         if (op < KS * per) {
-                            const int j = op / per, c = (op - j * per) * 2;
+                            const int j = op / per, c = (op - j * per) * EPC;
                             const bool ok = rg[m] >= 0;
-                            cpa<16>(xd + j * KPB + (c ^ (4 * (j & 3))), a.XT + (int64_t)(ok ? rg[m] : 0) * a.kp + cb + c,
-                                    ok ? 16 : 0);
+                            cpa<16>(xd + j * KPB + (c ^ bt_xsw<TS>(j, KPB)),
+                                    a.XT + (int64_t)(ok ? rg[m] : 0) * a.kp + cb + c, ok ? 16 : 0);
                         }
                     }
                 };
                 double dacc[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-#if VF_BT_ACC2
-                double dacc2[4][2] = {{0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}, {0.0, 0.0}};
-#endif
                 int32_t rg[4];
 #pragma unroll
                 for (int p = 0; p < kBStages - 1; ++p) {
@@ -1711,54 +1779,32 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                     cpa_commit();
                 }
                 load_idx(kBStages - 1, rg);
+                const int wsw = bt_wsw<TS>(kr), xsw = bt_xsw<TS>(kr, KPB);   // (j & 3 = kr below)
                 for (int sl = 0; sl < nsl; ++sl) {
                     if (sl + kBStages - 1 < nsl) stage(sl + kBStages - 1, (sl + kBStages - 1) % kBStages, rg);
                     load_idx(sl + kBStages, rg);                   // in flight during this slice's DMMA
                     cpa_commit();
                     cpa_wait<kBStages - 1>();
                     __syncthreads();
-                    const double* W0 = Wsm + (sl % kBStages) * KS * 16;
-                    const double* X0 = Xsm + (sl % kBStages) * KS * KPB;
+                    const TS* W0 = Wsm + (sl % kBStages) * KS * 16;
+                    const TS* X0 = Xsm + (sl % kBStages) * KS * KPB;
                     const int cc = cw * 16;
-#if VF_BT_ACC2
-                    // two accumulator sets (even / odd k-steps of the part): 8 independent
-                    // DMMA chains per warp instead of 4; the sets are added at the item end
-                    int ks = pw;
-                    for (; ks + nkp < KS / 4; ks += 2 * nkp) {
-                        const int sw = 4 * kr;
-                        const int j = ks * 4 + kr, j2 = (ks + nkp) * 4 + kr;
-                        const double a0 = W0[j * 16 + (mn ^ sw)], a1 = W0[j * 16 + ((8 + mn) ^ sw)];
-                        const double b0 = X0[j * KPB + ((cc + mn) ^ sw)], b1 = X0[j * KPB + ((cc + 8 + mn) ^ sw)];
-                        const double c0 = W0[j2 * 16 + (mn ^ sw)], c1 = W0[j2 * 16 + ((8 + mn) ^ sw)];
-                        const double e0 = X0[j2 * KPB + ((cc + mn) ^ sw)], e1 = X0[j2 * KPB + ((cc + 8 + mn) ^ sw)];
-                        dmma884(dacc[0], a0, b0);
-                        dmma884(dacc[1], a0, b1);
-                        dmma884(dacc[2], a1, b0);
-                        dmma884(dacc[3], a1, b1);
-                        dmma884(dacc2[0], c0, e0);
-                        dmma884(dacc2[1], c0, e1);
-                        dmma884(dacc2[2], c1, e0);
-                        dmma884(dacc2[3], c1, e1);
-                    }
-                    for (; ks < KS / 4; ks += nkp) {
-#else
                     if (VF_BT_HALF && B.nrows <= 8) {
                         // tile-uniform: rows 8..15 are padding, their DMMAs would add zeros
                         for (int ks = pw; ks < KS / 4; ks += nkp) {
                             const int j = ks * 4 + kr;
-                            const int sw = 4 * kr;
-                            const double a0 = W0[j * 16 + (mn ^ sw)];
-                            const double b0 = X0[j * KPB + ((cc + mn) ^ sw)], b1 = X0[j * KPB + ((cc + 8 + mn) ^ sw)];
+                            const double a0 = (double)W0[j * 16 + (mn ^ wsw)];
+                            const double b0 = (double)X0[j * KPB + ((cc + mn) ^ xsw)];
+                            const double b1 = (double)X0[j * KPB + ((cc + 8 + mn) ^ xsw)];
                             dmma884(dacc[0], a0, b0);
                             dmma884(dacc[1], a0, b1);
                         }
                     } else
                     for (int ks = pw; ks < KS / 4; ks += nkp) {
-#endif
                         const int j = ks * 4 + kr;
-                        const int sw = 4 * kr;
-                        const double a0 = W0[j * 16 + (mn ^ sw)], a1 = W0[j * 16 + ((8 + mn) ^ sw)];
-                        const double b0 = X0[j * KPB + ((cc + mn) ^ sw)], b1 = X0[j * KPB + ((cc + 8 + mn) ^ sw)];
+                        const double a0 = (double)W0[j * 16 + (mn ^ wsw)], a1 = (double)W0[j * 16 + ((8 + mn) ^ wsw)];
+                        const double b0 = (double)X0[j * KPB + ((cc + mn) ^ xsw)];
+                        const double b1 = (double)X0[j * KPB + ((cc + 8 + mn) ^ xsw)];
                         dmma884(dacc[0], a0, b0);
                         dmma884(dacc[1], a0, b1);
                         dmma884(dacc[2], a1, b0);
@@ -1767,10 +1813,6 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                     __syncthreads();                               // slot free for the slice kBStages ahead
                 }
                 cpa_wait<0>();
-#if VF_BT_ACC2
-#pragma unroll
-                for (int tl = 0; tl < 4; ++tl) { dacc[tl][0] += dacc2[tl][0]; dacc[tl][1] += dacc2[tl][1]; }
-#endif
                 // K-parts of a column chunk meet in smem, added in part order
                 double* red = bsm + kBStages * kBSlice;            // [8 warps][4 tiles][32 lanes][2]
                 if (nkp > 1) {
@@ -1801,8 +1843,11 @@ __global__ void __launch_bounds__(256, 2) bt_kernel(BArgs a) {
                         if (r >= B.nrows) continue;
                         const int64_t orow = a.outrow[B.out_off + r];
                         const int col = cb + cw * 16 + (tl & 1) * 8 + 2 * kr;
-                        double* dst = phase == 1 ? a.XT + (a.N + orow) * a.kp + col : a.Y + orow * a.kp + col;
-                        *reinterpret_cast<double2*>(dst) = make_double2(dacc[tl][0], dacc[tl][1]);
+                        TS* dst = phase == 1 ? a.XT + (a.N + orow) * a.kp + col : a.Y + orow * a.kp + col;
+                        if (sizeof(TS) == 8)
+                            *reinterpret_cast<double2*>(dst) = make_double2(dacc[tl][0], dacc[tl][1]);
+                        else
+                            *reinterpret_cast<float2*>(dst) = make_float2((float)dacc[tl][0], (float)dacc[tl][1]);
                     }
                 }
                 __syncthreads();                                   // red / ring reuse by the next pass
@@ -2528,7 +2573,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm<GROUPED>()) hot_kernel(H
         T* xn = static_cast<T*>((it & 1) ? a.xt0 : a.xt1);
         if (have_p1) {
             if constexpr (GROUPED) groups_phase<T, VEC, 1, MODE>(a, xc, xn, stile, nullptr, stage);
-            else if constexpr (KC == 1 && VEC == 1) phase1_groups_k1<T>(a, xc, gwarp, lane);
+            else if constexpr (KC == 1 && VEC == 1) phase1_groups_k1<T, VF_MV_L1 != 0>(a, xc, gwarp, lane);
             else phase1_rows<T, KC, VEC>(a, xc, gwarp, nwarp, lane);
             grid_sync(a.ctl, nblk);
         }
@@ -2553,7 +2598,7 @@ __global__ void __launch_bounds__(kThreads, ctas_per_sm<GROUPED>()) hot_kernel(H
         trace_ev(a, it, 0);
         if (have_p1) {                                           // ---- phase 1: T rows
             if constexpr (GROUPED) groups_phase<T, VEC, 1, MODE>(a, xc, xn, stile, nullptr, stage);
-            else if constexpr (KC == 1 && VEC == 1) phase1_groups_k1<T>(a, xc, gwarp, lane);
+            else if constexpr (KC == 1 && VEC == 1) phase1_groups_k1<T, VF_MV_L1 && MODE == M_MATVEC>(a, xc, gwarp, lane);
             else phase1_rows<T, KC, VEC>(a, xc, gwarp, nwarp, lane);
         }
         trace_ev(a, it, 1);
@@ -3119,6 +3164,7 @@ struct DeviceHMat {
     int64_t* p2_segptr16 = nullptr;
     uint16_t* idx16 = nullptr;
     int32_t* seg_base16 = nullptr;
+    SegC* segc16 = nullptr;
     int64_t k1_payload = 0;          // bytes one nrhs = 1 apply streams: values + V indices + u16 CSR offsets
     int k1_kernel = 0;
     bool k1_ovl = false;             // nrhs = 1 row kernel without the phase barrier (X-first rows, item counter)
@@ -3128,6 +3174,7 @@ struct DeviceHMat {
     BTile* bt_tiles = nullptr;
     double* bt_W = nullptr;
     float *bt_Whi = nullptr, *bt_Wlo = nullptr;   // FP32 handles: 3xTF32 split weights (bt_tc_kernel)
+    float* bt_Wf = nullptr;                       // FP32 handles: [K][16] weights (bt_kernel<float>, DMMA)
     int32_t *bt_src = nullptr, *bt_out = nullptr, *bt_ctr = nullptr;
     int32_t bt_n1 = 0, bt_n2 = 0;
     int64_t bt_cells = 0;
@@ -3758,7 +3805,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
     std::vector<uint16_t> i16;
     std::vector<int32_t> base16;
     int64_t pay16 = 0;
-    const bool use16 = !getenv("VF_K1_U32");           // sharded handles too (ROWS M_STEP iterations)
+    bool use16 = !getenv("VF_K1_U32");                 // sharded handles too (ROWS M_STEP iterations)
     if (use16) {
         const int64_t span16 = getenv("VF_U16_SPAN") ? std::min(65536, std::max(2, atoi(getenv("VF_U16_SPAN")))) : 65536;
         pay16 = D->p1_bytes;                                   // phase 1 unchanged (values, S, V indices)
@@ -4130,9 +4177,23 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         if (ok) break;
       }
     }
-    // the row kernel keeps segment indices of this layout in 32-bit registers
+    // the row kernel keeps segment indices of this layout in 32-bit registers,
+    // and its compact descriptors value offsets / sources in 32 bits
+    std::vector<SegC> sc16;
+    if (use16 && !s16.empty() && (int64_t)s16.size() < (int64_t)INT32_MAX) {
+        sc16.reserve(s16.size());
+        for (size_t i = 0; i < s16.size(); ++i) {
+            const Seg& sg = s16[i];
+            if (sg.val_off < 0 || sg.val_off > (int64_t)UINT32_MAX || sg.src < 0 || sg.src > (int64_t)UINT32_MAX ||
+                sg.len < 0 || (sg.kind != 0 && sg.kind != 1)) { sc16.clear(); break; }
+            sc16.push_back(SegC{(uint32_t)sg.val_off, (uint32_t)sg.src, (int32_t)((uint32_t)sg.len | ((uint32_t)sg.kind << 31)),
+                                base16[i]});
+        }
+        if (sc16.empty()) use16 = false;                      // does not fit: the u32 layout
+    }
     if (use16 && !s16.empty() && (int64_t)s16.size() < (int64_t)INT32_MAX) {
         if ((rc = up((void**)&D->segs16, s16.data(), s16.size() * sizeof(Seg))) ||
+            (rc = up((void**)&D->segc16, sc16.data(), sc16.size() * sizeof(SegC))) ||
             (rc = up((void**)&D->p2_segptr16, ptr16.data(), ptr16.size() * 8)) ||
             (rc = up((void**)&D->idx16, i16.data(), i16.size() * 2)) ||
             (rc = up((void**)&D->seg_base16, base16.data(), base16.size() * 4)))
@@ -4141,6 +4202,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         if (k1_use_pipe()) D->k1_kernel = 2;
         D->k1_ovl = !k1_use_pipe() && k1_overlap() && VF_K1_PF;
         std::vector<Seg>().swap(s16);
+        std::vector<SegC>().swap(sc16);
         std::vector<uint16_t>().swap(i16);
     }
     if (!D->res_ok && !h->sharded && !getenv("VF_NO_TILES") && (D->n_g1 + D->n_p2) > 0) {
@@ -4208,6 +4270,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         for (auto* v : {&t1, &t2}) for (auto& x : *v) { wn += (int64_t)x.w.size(); sn += (int64_t)x.srcs.size(); }
         W.reserve(wn); src.reserve(sn);
         std::vector<float> Whi, Wlo;                  // FP32: 3xTF32 split, K-major per 32-source slice
+        std::vector<float> Wf;                        // FP32: [K][16] for bt_kernel<float> (DMMA), FP32 swizzle
         auto tf32_hi = [](float w) {                  // cvt.rna.tf32.f32: round to nearest, ties away
             uint32_t u;
             std::memcpy(&u, &w, 4);
@@ -4224,6 +4287,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                 B.w_off = (int64_t)Whi.size();
                 Whi.resize(Whi.size() + nsl * 512, 0.0f);
                 Wlo.resize(Wlo.size() + nsl * 512, 0.0f);
+                Wf.resize(Wf.size() + nsl * 512, 0.0f);
                 for (int64_t j = 0; j < K; ++j)
                     for (int r = 0; r < 16; ++r) {
                         const float w = (float)x.w[(size_t)j * 16 + (r ^ (4 * (j & 3)))];
@@ -4232,6 +4296,8 @@ int upload_impl(Handle* h, DeviceHMat* D) {
                         const float h = tf32_hi(w);
                         Whi[o] = h;
                         Wlo[o] = w - h;
+                        // bt_kernel<float> (DMMA): [K][16] at the same tile offset (K padded to 32)
+                        Wf[B.w_off + j * 16 + (r ^ bt_wsw<float>((int)(j & 3)))] = w;
                     }
             } else {
                 W.insert(W.end(), x.w.begin(), x.w.end());
@@ -4250,8 +4316,9 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         if (sizeof(T) == 8) {
             if ((rc = up((void**)&D->bt_W, W.data(), W.size() * 8))) return rc;
         } else {
-            if (Whi.empty()) { Whi.resize(512, 0.0f); Wlo.resize(512, 0.0f); }
-            if ((rc = up((void**)&D->bt_Whi, Whi.data(), Whi.size() * 4)) || (rc = up((void**)&D->bt_Wlo, Wlo.data(), Wlo.size() * 4)))
+            if (Whi.empty()) { Whi.resize(512, 0.0f); Wlo.resize(512, 0.0f); Wf.resize(512, 0.0f); }
+            if ((rc = up((void**)&D->bt_Whi, Whi.data(), Whi.size() * 4)) || (rc = up((void**)&D->bt_Wlo, Wlo.data(), Wlo.size() * 4)) ||
+                (rc = up((void**)&D->bt_Wf, Wf.data(), Wf.size() * 4)))
                 return rc;
         }
         if ((rc = up((void**)&D->bt_tiles, tiles.data(), tiles.size() * sizeof(BTile))) ||
@@ -4613,26 +4680,30 @@ int launch_res(Handle* h, HotArgs& a, cudaStream_t st) {
     return VF_OK;
 }
 
-// Cooperative launch of the streamed-tile kernel (2 CTAs per SM).
+// Cooperative launch of the streamed-tile kernel (2 CTAs per SM); TS = the
+// handle's storage type (float: FP32 factors on the FP64 tensor cores)
+template <typename TS>
 int launch_bt(Handle* h, HotArgs& ha, cudaStream_t st) {
     DeviceHMat* D = h->dev;
+    auto fn = bt_kernel<TS>;
     // ring: max over the column widths of KS (16 + KPB) doubles per slice (KPB 64: 32 x 80); red: 8 x 4 x 32 x 2
     const size_t smem = (size_t)(kBStages * kBSlice + 8 * 4 * 32 * 2) * 8;
-    CK(cudaFuncSetAttribute(bt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bt_kernel, 256, smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, 256, smem));
     if (per_sm < 1) return set_error(VF_ECUDA, "bt_kernel cannot be resident");
     int nsm = 148;
     CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device));
     const int grid = nsm * std::min(per_sm, 2);
-    BArgs b{D->bt_tiles, D->bt_n1, D->bt_n2, D->bt_W, D->bt_src, D->bt_out, (double*)ha.xt0, (double*)ha.Y, D->N,
-            ha.kp, D->bt_ctr, D->ctl};
+    const TS* W = std::is_same<TS, double>::value ? (const TS*)D->bt_W : (const TS*)D->bt_Wf;
+    BArgs<TS> b{D->bt_tiles, D->bt_n1, D->bt_n2, W, D->bt_src, D->bt_out, (TS*)ha.xt0, (TS*)ha.Y, D->N,
+                ha.kp, D->bt_ctr, D->ctl};
     CK(cudaMemsetAsync(D->bt_ctr, 0, 16, st));
     CK(cudaMemsetAsync(D->ctl, 0, offsetof(Ctl, bar_gen), st));
     void* args[] = {&b};
     {
         Timer tm(h, st, 2);
-        CK(cudaLaunchCooperativeKernel((const void*)bt_kernel, dim3(grid), dim3(256), args, smem, st));
+        CK(cudaLaunchCooperativeKernel((const void*)fn, dim3(grid), dim3(256), args, smem, st));
     }
     h->launches_total++;
     D->last_grid = grid;
@@ -4664,6 +4735,11 @@ int launch_bt_tc2(Handle* h, HotArgs& ha, cudaStream_t st) {
 #ifndef VF_TC2_DEFAULT
 #define VF_TC2_DEFAULT 0
 #endif
+static bool bt_use_tc() {
+    const char* a = getenv("VF_TC");
+    const char* b = getenv("VF_TC2");
+    return (a && atoi(a) != 0) || (b && atoi(b) != 0) || VF_TC2_DEFAULT != 0;
+}
 int launch_bt_tc(Handle* h, HotArgs& ha, cudaStream_t st) {
     DeviceHMat* D = h->dev;
     {
@@ -4695,13 +4771,15 @@ int launch_bt_tc(Handle* h, HotArgs& ha, cudaStream_t st) {
 template <typename T, int MODE>
 int launch_hot(Handle* h, HotArgs& a, cudaStream_t st) {
     const int kp = a.kp;
+    // FP32 tiles on tcgen05 (3xTF32; VF_TC=1 or VF_TC2=1): measured slower than
+    // bt_kernel<float> on the FP64 tensor cores, so opt-in
     if (MODE == M_MATVEC && std::is_same<T, float>::value && kp >= 128 && kp % 128 == 0 && h->dev->bt_ok &&
-        h->dev->bt_Whi)
+        h->dev->bt_Whi && bt_use_tc())
         return launch_bt_tc(h, a, st);
-    // wide batches on an F-hat that does not fit the resident layout: streamed tiles (FP64 matvec)
-    if (MODE == M_MATVEC && std::is_same<T, double>::value && kp >= 16 && h->dev->bt_ok &&
+    // wide batches on an F-hat that does not fit the resident layout: streamed tiles
+    if (MODE == M_MATVEC && kp >= 16 && h->dev->bt_ok && (std::is_same<T, double>::value || h->dev->bt_Wf) &&
         (kp <= kBCols ? (kp == 16 || kp == 32 || kp == 64 || kp == 128) : kp % kBCols == 0))
-        return launch_bt(h, a, st);
+        return launch_bt<T>(h, a, st);
     if (kp >= 16 && kp % 16 == 0 && h->dev->res_ok &&
         (size_t)h->dev->res_wcap * sizeof(T) + (size_t)h->dev->res_scap * 4 + (size_t)kRS * kKS * 16 * sizeof(T) +
                 (size_t)kp * 8 + 2048 + (size_t)kRW * 4 * 32 * 2 * 8 + 4096 +
@@ -4827,7 +4905,7 @@ int iterate_rows(Handle* h, int k, int kp, const void* rho, int clamp, int iters
     CK(cudaMemsetAsync(D->ctl, 0, sizeof(Ctl), st));
     HotArgs a = hot_args(D, kp, k);
     a.E = D->Ep; a.rho = rho; a.Q = D->Qp; a.iters = iters; a.clamp = clamp; a.tol = tol;
-    if (kp == 1 && D->idx16) { a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16; }
+    if (kp == 1 && D->idx16) { a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16; a.segc16 = D->segc16; }
     const int batch = 4;
     for (int launched = 0;;) {
         for (int b = 0; b < batch; ++b) {
@@ -4948,7 +5026,7 @@ int launch_k1p(Handle* h, void* XT, void* Y, cudaStream_t st) {
     a.xt0 = XT;
     a.Y = Y;
     a.p2_order = D->p2_order;
-    a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16;
+    a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16; a.segc16 = D->segc16;
     auto fn = k1p_kernel<T>;
     const size_t smem = (size_t)kWarps * k1p_warp_bytes<T>();
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -4989,7 +5067,7 @@ int apply_k1(Handle* h, void* XT, void* Y, cudaStream_t st) {
     CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 2) * 4, st));
     a.qctr = D->tready + D->n_svd;
     a.p2_order = D->p2_order;
-    if (D->idx16) { a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16; }
+    if (D->idx16) { a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16; a.segc16 = D->segc16; }
     if (D->idx16 && D->k1_ovl) { a.p1done = D->tready + D->n_svd + 1; a.n_p1items = (int32_t)D->n_pp; }
     return launch_hot<T, M_MATVEC>(h, a, st);
 }
@@ -5003,10 +5081,10 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
     // more than 8 columns on a streamed-tile layout: one bt_kernel launch with the
     // columns padded to 16, 32, 64 or a multiple of 128
     const bool bt = D->bt_ok && !(D->world > 1 || h->comm) && nrhs > 8 && !getenv("VF_NO_TILES_MV");
-    // FP64 tiles (bt_kernel): 16, 32, 64 or a multiple of 128 columns; FP32 tiles on tcgen05
-    // (bt_tc_kernel): the MMA's M = 128 columns per pass
+    // tiles on DMMA (bt_kernel<T>): 16, 32, 64 or a multiple of 128 columns; FP32 tiles on
+    // tcgen05 (bt_tc_kernel, opt-in): the MMA's M = 128 columns per pass
     const int kp = !bt ? pad_k(nrhs)
-                   : sizeof(T) == 4 ? (nrhs + 127) / 128 * 128
+                   : sizeof(T) == 4 && bt_use_tc() ? (nrhs + 127) / 128 * 128
                                     : (nrhs <= 16 ? 16 : nrhs <= 32 ? 32 : nrhs <= 64 ? 64 : (nrhs + 127) / 128 * 128);
     if ((rc = ensure_scratch(D, kp, st))) return rc;
     reset_counters(h);
@@ -5029,7 +5107,7 @@ int matvec_impl(Handle* h, const void* X, void* Y, int nrhs) {
         if (kpn == 1 && !getenv("VF_MV_STATIC") && !getenv("VF_MV_FLAGS")) {
             CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
             a.qctr = D->tready + D->n_svd; a.p2_order = D->p2_order;
-            if (D->idx16) { a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16; }
+            if (D->idx16) { a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16; a.segc16 = D->segc16; }
         }
         if (kpn == 1 && getenv("VF_MV_FLAGS") && !getenv("VF_MV_BARRIER")) {
             CK(cudaMemsetAsync(D->tready, 0, (size_t)(D->n_svd + 1) * 4, st));
@@ -5232,8 +5310,8 @@ void device_free(Handle* h) {
     for (auto& e : D->evpool) if (e) cudaEventDestroy(e);
     for (auto& kv : D->sched) { cudaFree(kv.second.ptr); cudaFree(kv.second.items); }
     stream::free_dev(&D->sl);
-    void* bps[] = {D->bt_tiles, D->bt_W, D->bt_Whi, D->bt_Wlo, D->bt_src, D->bt_out, D->bt_ctr, D->segs16, D->p2_segptr16, D->idx16,
-                   D->seg_base16};
+    void* bps[] = {D->bt_tiles, D->bt_W, D->bt_Whi, D->bt_Wlo, D->bt_Wf, D->bt_src, D->bt_out, D->bt_ctr, D->segs16, D->p2_segptr16, D->idx16,
+                   D->seg_base16, D->segc16};
     for (void* p : bps) if (p) cudaFree(p);
     delete D;
     h->dev = nullptr;

@@ -74,14 +74,35 @@ def handles_f32(tmp_path_factory):
 def test_tiles_f32_tcgen05_3xtf32(handles_f32, k):
     """FP32 streamed tiles on the 5th-generation tensor cores (bt_tc_kernel:
     tcgen05.mma kind::tf32, TMEM accumulator, 3xTF32 split): <= 1e-5 vs the
-    oracle's Alg. 5 of the same (FP32-rounded) blocks, bitwise repeatable."""
+    oracle's Alg. 5 of the same (FP32-rounded) blocks, bitwise repeatable.
+    Opt-in (VF_TC=1): the default FP32 tile kernel is bt_kernel<float>."""
+    os.environ["VF_TC"] = "1"
+    try:
+        _check_f32_tiles(handles_f32, k, seed=21 + k)
+    finally:
+        del os.environ["VF_TC"]
+
+
+@pytest.mark.parametrize("k", [9, 16, 17, 32, 48, 64, 100, 128, 130, 256])
+def test_tiles_f32_dmma(handles_f32, k):
+    """FP32 streamed tiles on the FP64 tensor cores (bt_kernel<float>, the
+    default FP32 wide-batch path: FP32 weights and XT rows staged in shared
+    memory with the FP32 swizzles, widened to FP64 for DMMA m8n8k4, FP64
+    accumulation, one rounding at the store): <= 1e-5 vs the oracle's Alg. 5
+    of the same blocks (north_star FP32 tolerance), bitwise repeatable.  With
+    exact products and FP64 sums the only errors are the FP32 roundings of T
+    and Y, so it must also meet 1e-6."""
+    _check_f32_tiles(handles_f32, k, seed=31 + k, tol=1e-6)
+
+
+def _check_f32_tiles(handles_f32, k, seed, tol=1e-5):
     for name, S, H, M in handles_f32:
-        X = sg.random_rhs(S.N, k, seed=21 + k).astype(np.float32).astype(np.float64)
+        X = sg.random_rhs(S.N, k, seed=seed).astype(np.float32).astype(np.float64)
         Xd = torch.from_numpy(np.ascontiguousarray(X.T.astype(np.float32))).cuda().T
         Y = torch.empty((k, S.N), dtype=torch.float32, device="cuda").T
         M.matvec(Xd, Y)
         R = hm.hmatvec(H, X)
-        assert np.linalg.norm(Y.cpu().numpy().astype(np.float64) - R) / np.linalg.norm(R) <= 1e-5, (name, k)
+        assert np.linalg.norm(Y.cpu().numpy().astype(np.float64) - R) / np.linalg.norm(R) <= tol, (name, k)
         Y2 = torch.empty_like(Y)
         M.matvec(Xd, Y2)
         assert torch.equal(Y, Y2)
