@@ -843,6 +843,12 @@ struct HotArgs {
     int32_t* p1done;
     int32_t n_p1items;
     const int32_t* p2_order;
+    // nrhs = 1 matvec: per-SM row queues (DeviceHMat::smq_*); nullptr = the global LPT queue
+    const int32_t* smq_ptr;
+    const int32_t* smq_rows;
+    const int32_t* smq_pool;
+    int32_t* smq_ctr;
+    int32_t n_smq, n_smq_pool;
     // nrhs = 1 matvec rows with 16-bit CSR offsets (optional; upload_impl)
     const Seg* segs16;
     const int64_t* p2_segptr16;
@@ -1055,6 +1061,70 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
                 if (lane == 0) static_cast<T*>(a.Y)[oA] = acc;
                 tA = tB; sbA = sbB; s1A = s1B; oA = oB;
                 tB = tC; rB = rC;
+            }
+            return;
+        }
+#endif
+#if VF_K1_PF
+        if (a.smq_ptr) {
+            // per-SM queues: the long rows first, from the global LPT pool; then the
+            // queue of this SM (%smid) -- a contiguous tree-order range, so the warps
+            // of an SM stream adjacent rows and share their x / T lines in L1; then
+            // whatever other queues still hold (an SM that finishes early helps the
+            // others, and queues no running SM owns are served too).  Every row is
+            // taken exactly once (atomic tickets) and summed by one warp in the same
+            // fixed order as before: bitwise equal results.
+            constexpr unsigned FULL = 0xffffffffu;
+            unsigned smid;
+            asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+            int32_t* ctr = a.smq_ctr;                 // current queue: ticket counter, row list, length
+            const int32_t* list = a.smq_pool;
+            int32_t len = a.n_smq_pool;
+            int stage = 0, sweep_b = 0, qv = 0;
+            unsigned m = 0;
+            auto set_queue = [&](int q) {
+                ctr = a.smq_ctr + 8 * (q + 1);
+                list = a.smq_rows + a.smq_ptr[q];
+                len = a.smq_ptr[q + 1] - a.smq_ptr[q];
+            };
+            auto next_queue = [&]() -> bool {         // warp-uniform
+                if (stage == 0) {
+                    stage = 1;
+                    if ((int)smid < a.n_smq) { set_queue((int)smid); return true; }
+                }
+                stage = 2;
+                while (m == 0) {                      // sweep: lanes look at 32 queues at a time
+                    if (sweep_b >= a.n_smq) return false;
+                    int rem = 0;
+                    qv = (int)(smid % (unsigned)a.n_smq) + 1 + sweep_b + lane;      // starts after the own queue
+                    if (sweep_b + lane < a.n_smq) {
+                        if (qv >= a.n_smq) qv -= a.n_smq;
+                        rem = (a.smq_ptr[qv + 1] - a.smq_ptr[qv]) - *(volatile int32_t*)(a.smq_ctr + 8 * (qv + 1));
+                    }
+                    m = __ballot_sync(FULL, rem > 0);
+                    sweep_b += 32;
+                }
+                const int l = __ffs(m) - 1;
+                m &= m - 1;
+                set_queue(__shfl_sync(FULL, qv, l));
+                return true;
+            };
+            int t = 0;
+            if (lane == 0) t = atomicAdd(ctr, 1);
+            t = __shfl_sync(FULL, t, 0);
+            for (;;) {
+                while (t >= len) {
+                    if (!next_queue()) return;
+                    if (lane == 0) t = atomicAdd(ctr, 1);
+                    t = __shfl_sync(FULL, t, 0);
+                }
+                const int32_t r = list[t];
+                int fut = 0;
+                if (lane == 0) fut = atomicAdd(ctr, 1);           // next ticket while this row streams
+                const T acc = row_accumulate_k1_pf<T>(a.segc16, a.p2_segptr16[r], a.p2_segptr16[r + 1], vals, xc, lane, a.N,
+                                                      a.idx16, a.p1done, a.n_p1items, t_ready);
+                if (lane == 0) static_cast<T*>(a.Y)[a.p2_rows[r]] = acc;
+                t = __shfl_sync(FULL, fut, 0);
             }
             return;
         }
@@ -3136,6 +3206,13 @@ struct DeviceHMat {
     // barrier-free nrhs = 1 matvec (tready[n_svd] = the dynamic queue counter)
     int32_t *tready = nullptr, *seg_blk = nullptr, *g1_blk = nullptr, *p2_order = nullptr;
     int64_t n_svd = 0;
+    // nrhs = 1 matvec, per-SM row queues (VF_K1_SMQ): the long rows stay in a global
+    // LPT pool (smq_pool, taken first), the others are cut into n_smq contiguous
+    // tree-order ranges of equal cost, one per SM (%smid), so the warps of an SM
+    // work on adjacent rows and share their x / T lines in L1; smq_ctr holds the
+    // pool ticket counter ([0]) and the queue counters ([8 (q + 1)]), zeroed per launch
+    int32_t *smq_ptr = nullptr, *smq_rows = nullptr, *smq_pool = nullptr, *smq_ctr = nullptr;
+    int32_t n_smq = 0, n_smq_pool = 0;
     // pipelined nrhs = 1 matvec (k1p_kernel): phase-1 part items in LPT order,
     // [0] the queue ticket counter, [1] finished phase-1 items
     int32_t *p1_order = nullptr, *k1p_ctr = nullptr;
@@ -3210,6 +3287,18 @@ bool k1_overlap() {
     const char* e = getenv("VF_K1_OVL");
     if (e) return atoi(e) != 0;
     return VF_K1_OVL_DEFAULT != 0;
+}
+// nrhs = 1 matvec rows from per-SM queues (VF_K1_SMQ=0/1 overrides; read at upload)
+#ifndef VF_K1_SMQ_DEFAULT
+#define VF_K1_SMQ_DEFAULT 0
+#endif
+#ifndef VF_K1_SMQ_THR_DEFAULT
+#define VF_K1_SMQ_THR_DEFAULT 2.0
+#endif
+bool k1_smq() {
+    const char* e = getenv("VF_K1_SMQ");
+    if (e) return atoi(e) != 0;
+    return VF_K1_SMQ_DEFAULT != 0;
 }
 bool k1_use_pipe() {
     const char* e = getenv("VF_K1_KERNEL");
@@ -3958,6 +4047,48 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             (rc = up((void**)&D->k1p_ctr, nullptr, 16)) ||
             (rc = up((void**)&D->tready, nullptr, (size_t)(D->n_svd + 2) * 4)))
             return rc;
+        // per-SM row queues of the nrhs = 1 matvec (see DeviceHMat::smq_*)
+        if (k1_smq() && !D->cost_p2.empty()) {
+            int nq = 148;
+            cudaDeviceGetAttribute(&nq, cudaDevAttrMultiProcessorCount, D->device);
+            if (const char* e = getenv("VF_K1_SMQ_NQ")) nq = std::max(1, atoi(e));
+            double thr = VF_K1_SMQ_THR_DEFAULT;
+            if (const char* e = getenv("VF_K1_SMQ_THR")) thr = atof(e);
+            const int64_t nr = (int64_t)D->cost_p2.size();
+            int64_t tot = 0;
+            for (int64_t c : D->cost_p2) tot += c;
+            const double lim = thr * (double)tot / (double)nr;            // long rows: cost > thr x mean
+            std::vector<int32_t> tree(nr), pool, rows, ptr(nq + 1, 0);
+            std::iota(tree.begin(), tree.end(), 0);
+            if (!std::is_sorted(p2_rows.begin(), p2_rows.end()))
+                std::stable_sort(tree.begin(), tree.end(), [&](int32_t x, int32_t y) { return p2_rows[x] < p2_rows[y]; });
+            int64_t stat = 0;
+            for (int32_t r : tree) {
+                if ((double)D->cost_p2[r] > lim) pool.push_back(r);
+                else { rows.push_back(r); stat += D->cost_p2[r]; }
+            }
+            std::stable_sort(pool.begin(), pool.end(), [&](int32_t x, int32_t y) { return D->cost_p2[x] > D->cost_p2[y]; });
+            // contiguous tree-order ranges of equal cost: row i goes to queue floor(prefix / (stat / nq))
+            int64_t pre = 0;
+            size_t i = 0;
+            for (int q = 0; q < nq; ++q) {
+                const double hi = (double)stat * (double)(q + 1) / (double)nq;
+                while (i < rows.size() && (q + 1 == nq || (double)pre + 0.5 * (double)D->cost_p2[rows[i]] < hi)) pre += D->cost_p2[rows[i++]];
+                ptr[q + 1] = (int32_t)i;
+            }
+            D->n_smq = nq;
+            D->n_smq_pool = (int32_t)pool.size();
+            if (pool.empty()) pool.push_back(0);
+            if (rows.empty()) rows.push_back(0);
+            if ((rc = up((void**)&D->smq_ptr, ptr.data(), ptr.size() * 4)) ||
+                (rc = up((void**)&D->smq_rows, rows.data(), rows.size() * 4)) ||
+                (rc = up((void**)&D->smq_pool, pool.data(), pool.size() * 4)) ||
+                (rc = up((void**)&D->smq_ctr, nullptr, (size_t)(nq + 1) * 32)))
+                return rc;
+            if (getenv("VF_LAYOUT_DEBUG"))
+                fprintf(stderr, "[vf layout] smq: %d queues, %d pool rows (cost %.1f %%), %lld queue rows\n", nq, D->n_smq_pool,
+                        100.0 * (double)(tot - stat) / (double)tot, (long long)rows.size());
+        }
     }
 
     // ---- resident batched layout: groups -> CTAs (one per SM), each CTA's
@@ -5069,6 +5200,11 @@ int apply_k1(Handle* h, void* XT, void* Y, cudaStream_t st) {
     a.p2_order = D->p2_order;
     if (D->idx16) { a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16; a.segc16 = D->segc16; }
     if (D->idx16 && D->k1_ovl) { a.p1done = D->tready + D->n_svd + 1; a.n_p1items = (int32_t)D->n_pp; }
+    if (D->idx16 && VF_K1_PF && D->smq_ptr) {
+        CK(cudaMemsetAsync(D->smq_ctr, 0, (size_t)(D->n_smq + 1) * 32, st));
+        a.smq_ptr = D->smq_ptr; a.smq_rows = D->smq_rows; a.smq_pool = D->smq_pool; a.smq_ctr = D->smq_ctr;
+        a.n_smq = D->n_smq; a.n_smq_pool = D->n_smq_pool;
+    }
     return launch_hot<T, M_MATVEC>(h, a, st);
 }
 
@@ -5298,7 +5434,7 @@ void device_free(Handle* h) {
     if (!D) return;
     cudaSetDevice(h->device);
     void* ptrs[] = {D->pp_group, D->pp_begin, D->pp_len, D->pp_idx, D->pp_n, D->pp_cnt, D->pp_scratch,
-                    D->tready, D->seg_blk, D->g1_blk, D->p2_order, D->p1_order, D->k1p_ctr, D->r_groups, D->r_outrow, D->r_wblob, D->r_cta_woff, D->r_sblob, D->r_cta_soff,
+                    D->tready, D->seg_blk, D->g1_blk, D->p2_order, D->smq_ptr, D->smq_rows, D->smq_pool, D->smq_ctr, D->p1_order, D->k1p_ctr, D->r_groups, D->r_outrow, D->r_wblob, D->r_cta_woff, D->r_sblob, D->r_cta_soff,
                     D->r_p1_ptr, D->r_p1_list, D->r_p2_ptr, D->r_p2_list, D->bounds, D->send, D->recv, D->vals, D->idx, D->segs, D->p1_segptr, D->p1_rows, D->p1_scale, D->p2_segptr, D->p2_rows,
                     D->perm, D->active, D->g1, D->g2, D->gseg, D->gvo, D->grow1, D->grow2, D->gcsr1, D->gcsr2,
                     D->xt[0], D->xt[1], D->Ep, D->Qp, D->Qdp, D->Qvp, D->Yp, D->Qip,

@@ -120,16 +120,63 @@ def test_k1p_equals_row_kernel_on_product_build():
 
 @pytest.mark.parametrize("env", [{}, {"VF_P1_PART": "64"}, {"VF_U16_SPAN": "7"},
                                  {"VF_P1_PART": "32", "VF_U16_SPAN": "2"}, {"VF_K1_ILV": "0"},
-                                 {"VF_K1_PACK": "1"}, {"VF_K1_OVL": "1"}])
+                                 {"VF_K1_PACK": "1"}, {"VF_K1_OVL": "1"},
+                                 {"VF_K1_SMQ": "1"}, {"VF_K1_SMQ": "0"},
+                                 {"VF_K1_SMQ": "1", "VF_K1_SMQ_NQ": "500", "VF_K1_SMQ_THR": "1e9"},
+                                 {"VF_K1_SMQ": "1", "VF_K1_SMQ_NQ": "3", "VF_K1_SMQ_THR": "0.5"},
+                                 {"VF_K1_SMQ": "1", "VF_K1_SMQ_THR": "1e9", "VF_K1_OVL": "1", "VF_P1_PART": "64"}])
 def test_default_row_kernel_forced_layouts(env):
     """The default nrhs = 1 kernel (hot_kernel<T,1,1> with the register-prefetching
     row accumulator on the interleaved 16-bit layout) under the same forced
     layouts: multi-part phase-1 groups, CSR rows cut into runs of span 7 / 2
     (runs crossing rounds, rows of many segment batches, interleaved pieces of
     every size), the plain (non-interleaved) order, per-row packing and the
-    barrier-free hand-over: <= 1e-12 / 1e-5 vs the oracle's Alg. 5 on the same
+    barrier-free hand-over, and the per-SM row queues (VF_K1_SMQ: default
+    queue count and pool; 500 queues with no pool, so most queues are only
+    served by the end-of-kernel sweep; 3 queues with most rows in the pool, so
+    most SMs own no queue; no pool with the barrier-free hand-over and
+    multi-part phase 1): <= 1e-12 / 1e-5 vs the oracle's Alg. 5 on the same
     blocks, bitwise repeatable."""
     out = _run(env, kernel="rows")
     for name, d in out.items():
         bound = 1e-12 if name.endswith("f64") else 1e-5
         assert d["err"] <= bound and d["same"] and d["k1"] > 0, (name, d)
+
+
+_SMQ = r"""
+import json, os, sys, numpy as np, torch
+sys.path.insert(0, {root!r})
+import oracle, paper_2209_07632_b200 as vf, scenegen as sg
+V, F = sg.cfg3_mesh(n=32, crater_D=1000.0 * 32 / 256)
+S = oracle.Scene(V, F)
+X = sg.random_rhs(S.N, 1, seed=11)
+Xd = torch.from_numpy(np.ascontiguousarray(X.T)).cuda().T
+res = []
+for env in ({{"VF_K1_SMQ": "0"}}, {{"VF_K1_SMQ": "1"}}, {{"VF_K1_SMQ": "1", "VF_K1_SMQ_NQ": "37", "VF_K1_SMQ_THR": "1.0"}},
+            {{"VF_K1_SMQ": "1", "VF_K1_SMQ_NQ": "1000", "VF_K1_SMQ_THR": "1e9"}}):
+    for k in ("VF_K1_SMQ", "VF_K1_SMQ_NQ", "VF_K1_SMQ_THR"):
+        os.environ.pop(k, None)
+    os.environ.update(env)                            # read at upload
+    M = vf.ViewFactorMatrix.build(V, F, 1e-5, device=0)
+    Y = torch.empty((1, S.N), dtype=torch.float64, device="cuda").T
+    for _ in range(3):
+        Y.zero_()
+        M.matvec(Xd, Y)
+    res.append(Y.cpu().numpy()[:, 0].copy())
+ex = S.F_dense() @ X[:, 0]
+print(json.dumps(dict(same=[bool(np.array_equal(res[0], r)) for r in res[1:]],
+                      ex=float(np.linalg.norm(res[1] - ex) / np.linalg.norm(ex)))))
+"""
+
+
+def test_smq_bitwise_equals_global_queue():
+    """Per-SM row queues change which warp sums a row and when, not how: the
+    product-built configs[2]-recipe F-hat applied with the global LPT queue and
+    with per-SM queues (default; 37 queues with a large pool; 1000 queues, no
+    pool) gives bitwise equal Y, within 10 tol of the oracle's exact F."""
+    r = subprocess.run([sys.executable, "-c", _SMQ.format(root=ROOT)],
+                       env={k: v for k, v in os.environ.items() if not k.startswith("VF_K1_")},
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert all(d["same"]) and d["ex"] <= 1e-4, d
