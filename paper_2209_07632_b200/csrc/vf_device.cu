@@ -574,6 +574,9 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
 #ifndef VF_K1_TL1
 #define VF_K1_TL1 0         // nrhs = 1 rows: T-row gathers through L1 (A/B option)
 #endif
+#ifndef VF_K1_SMQ_CODE
+#define VF_K1_SMQ_CODE 1    // per-SM row queues compiled in (0: A/B builds of the kernel without them)
+#endif
 #ifndef VF_K1_ROWPF
 #define VF_K1_ROWPF 0       // row descriptors pipelined over three rows (measured slower: 0.845 vs 0.809 ms)
 #endif
@@ -1065,7 +1068,7 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
             return;
         }
 #endif
-#if VF_K1_PF
+#if VF_K1_PF && VF_K1_SMQ_CODE
         if (a.smq_ptr) {
             // per-SM queues: the long rows first, from the global LPT pool; then the
             // queue of this SM (%smid) -- a contiguous tree-order range, so the warps
