@@ -572,8 +572,8 @@ __device__ __forceinline__ T row_accumulate_k1(const Seg* __restrict__ segs, int
 #define VF_K1_L2PF 0        // rounds ahead for the bulk L2 prefetch of a batch's values (0 = off)
 #endif
 #ifndef VF_K1_TL1
-#define VF_K1_TL1 0         // nrhs = 1 rows: T-row gathers through L1 (A/B option)
-#endif
+#define VF_K1_TL1 1         // nrhs = 1 rows: T-row gathers through L1 (0.739-0.765 vs 0.795-0.798 ms on configs[2], s32);
+#endif                      // used when the T rows start on a 128-B line of XT (HotArgs::t_l1; VF_K1_TL1=0/1 env at upload)
 #ifndef VF_K1_SMQ_CODE
 #define VF_K1_SMQ_CODE 1    // per-SM row queues compiled in (0: A/B builds of the kernel without them)
 #endif
@@ -628,7 +628,7 @@ __device__ __forceinline__ void k1_fetch(K1Round<T>& R, int cc, int ns, int tota
     }
 }
 template <typename T>
-__device__ __forceinline__ void k1_consume(const K1Round<T>& R, const T* xt, T& acc0, T& acc1) {
+__device__ __forceinline__ void k1_consume(const K1Round<T>& R, const T* xt, T& acc0, T& acc1, bool tl1) {
     const int nv = R.f & 7;
     T x[4];
     if (R.f & 8) {
@@ -642,12 +642,19 @@ __device__ __forceinline__ void k1_consume(const K1Round<T>& R, const T* xt, T& 
             for (int u = 0; u < 4; ++u) x[u] = XLD(xt + R.xb + (u < nv ? u : 0));
         }
     } else {                                             // T rows (written by phase 1 of this launch): L2
-        // (VF_K1_TL1=1: through L1 -- no SM reads a T row before the phase barrier /
-        // the finished-item wait, so no L1 holds a stale line of one)
-        if (R.f & 16) XV4<T, VF_K1_TL1 != 0>::ld(xt + R.xb, x);
+        // (tl1: through L1 -- no SM reads a T row before the phase barrier / the
+        // finished-item wait, and the T rows start on a line of their own, so no L1
+        // holds a stale sector of one; the rows of a U block share all its T rows)
+        if (tl1) {
+            if (R.f & 16) XV4<T, true>::ld(xt + R.xb, x);
+            else {
+#pragma unroll
+                for (int u = 0; u < 4; ++u) x[u] = XLD(xt + R.xb + (u < nv ? u : 0));
+            }
+        } else if (R.f & 16) XV4<T, false>::ld(xt + R.xb, x);
         else {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) x[u] = VF_K1_TL1 ? XLD(xt + R.xb + (u < nv ? u : 0)) : __ldcg(xt + R.xb + (u < nv ? u : 0));
+            for (int u = 0; u < 4; ++u) x[u] = __ldcg(xt + R.xb + (u < nv ? u : 0));
         }
     }
 #pragma unroll
@@ -679,7 +686,7 @@ template <typename T>
 __device__ __forceinline__ T row_accumulate_k1_pf(const SegC* __restrict__ segc, int64_t s0, int64_t s1,
                                                   const T* __restrict__ vals, const T* xt, int lane, int64_t nx,
                                                   const uint16_t* __restrict__ idx16, const int32_t* p1done,
-                                                  int32_t n_p1, bool& t_ready) {
+                                                  int32_t n_p1, bool& t_ready, bool tl1 = false) {
     constexpr unsigned FULL = 0xffffffffu;
     T acc0 = T(0), acc1 = T(0);
     for (int64_t sb = s0; sb < s1; sb += 32) {
@@ -728,12 +735,12 @@ __device__ __forceinline__ T row_accumulate_k1_pf(const SegC* __restrict__ segc,
                 K1Round<T> nx2;
                 k1_fetch<T>(nx2, base + lane, ns, total, excl, my, vals, idx16, nx, lane);
                 if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
-                k1_consume<T>(cur, xt, acc0, acc1);
+                k1_consume<T>(cur, xt, acc0, acc1, tl1);
                 cur = nx1;
                 nx1 = nx2;
             }
             if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
-            k1_consume<T>(cur, xt, acc0, acc1);
+            k1_consume<T>(cur, xt, acc0, acc1, tl1);
             cur = nx1;
         }
         if (0)
@@ -745,11 +752,11 @@ __device__ __forceinline__ T row_accumulate_k1_pf(const SegC* __restrict__ segc,
 #endif
             k1_fetch<T>(nxt, base + lane, ns, total, excl, my, vals, idx16, nx, lane);
             if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
-            k1_consume<T>(cur, xt, acc0, acc1);
+            k1_consume<T>(cur, xt, acc0, acc1, tl1);
             cur = nxt;
         }
         if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
-        k1_consume<T>(cur, xt, acc0, acc1);
+        k1_consume<T>(cur, xt, acc0, acc1, tl1);
     }
     T acc = acc0 + acc1;
 #pragma unroll
@@ -852,6 +859,7 @@ struct HotArgs {
     const int32_t* smq_pool;
     int32_t* smq_ctr;
     int32_t n_smq, n_smq_pool;
+    int32_t t_l1;                 // nrhs = 1 matvec rows: T-row gathers through L1 (VF_K1_TL1)
     // nrhs = 1 matvec rows with 16-bit CSR offsets (optional; upload_impl)
     const Seg* segs16;
     const int64_t* p2_segptr16;
@@ -1060,7 +1068,7 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
                 if (lane == 0) fut = atomicAdd(a.qctr, 1);  // ticket D
                 if (tB < n2) { sbB = (int32_t)a.p2_segptr16[rB]; s1B = (int32_t)a.p2_segptr16[rB + 1]; oB = a.p2_rows[rB]; }
                 const T acc = row_accumulate_k1_pf<T>(a.segc16, sbA, s1A, vals, xc, lane, a.N, a.idx16,
-                                                      a.p1done, a.n_p1items, t_ready);
+                                                      a.p1done, a.n_p1items, t_ready, a.t_l1 != 0);
                 if (lane == 0) static_cast<T*>(a.Y)[oA] = acc;
                 tA = tB; sbA = sbB; s1A = s1B; oA = oB;
                 tB = tC; rB = rC;
@@ -1125,7 +1133,7 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
                 int fut = 0;
                 if (lane == 0) fut = atomicAdd(ctr, 1);           // next ticket while this row streams
                 const T acc = row_accumulate_k1_pf<T>(a.segc16, a.p2_segptr16[r], a.p2_segptr16[r + 1], vals, xc, lane, a.N,
-                                                      a.idx16, a.p1done, a.n_p1items, t_ready);
+                                                      a.idx16, a.p1done, a.n_p1items, t_ready, a.t_l1 != 0);
                 if (lane == 0) static_cast<T*>(a.Y)[a.p2_rows[r]] = acc;
                 t = __shfl_sync(FULL, fut, 0);
             }
@@ -1141,7 +1149,7 @@ __device__ __forceinline__ void phase2_rows(const HotArgs& a, const T* xc, T* xn
             if (lane == 0) fut = atomicAdd(a.qctr, 1);
             const T acc = (VF_K1_PF && a.idx16) ? row_accumulate_k1_pf<T>(a.segc16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
                                                                            vals, xc, lane, a.N, a.idx16,
-                                                                           a.p1done, a.n_p1items, t_ready)
+                                                                           a.p1done, a.n_p1items, t_ready, a.t_l1 != 0)
                         : a.idx16 ? row_accumulate_k1<T, VF_MV_L1 != 0>(a.segs16, a.p2_segptr16[r], a.p2_segptr16[r + 1],
                                                                          vals, a.idx, xc, lane, a.N, nullptr, nullptr,
                                                                          a.idx16, a.seg_base16)
@@ -3216,6 +3224,7 @@ struct DeviceHMat {
     // pool ticket counter ([0]) and the queue counters ([8 (q + 1)]), zeroed per launch
     int32_t *smq_ptr = nullptr, *smq_rows = nullptr, *smq_pool = nullptr, *smq_ctr = nullptr;
     int32_t n_smq = 0, n_smq_pool = 0;
+    bool k1_tl1 = false;             // nrhs = 1 matvec rows: T rows through L1 (they start on a 128-B line of XT)
     // pipelined nrhs = 1 matvec (k1p_kernel): phase-1 part items in LPT order,
     // [0] the queue ticket counter, [1] finished phase-1 items
     int32_t *p1_order = nullptr, *k1p_ctr = nullptr;
@@ -4050,6 +4059,10 @@ int upload_impl(Handle* h, DeviceHMat* D) {
             (rc = up((void**)&D->k1p_ctr, nullptr, 16)) ||
             (rc = up((void**)&D->tready, nullptr, (size_t)(D->n_svd + 2) * 4)))
             return rc;
+        {
+            const char* e = getenv("VF_K1_TL1");
+            D->k1_tl1 = (e ? atoi(e) != 0 : VF_K1_TL1 != 0) && ((size_t)D->N * sizeof(T)) % 128 == 0;
+        }
         // per-SM row queues of the nrhs = 1 matvec (see DeviceHMat::smq_*)
         if (k1_smq() && !D->cost_p2.empty()) {
             int nq = 148;
@@ -5203,6 +5216,7 @@ int apply_k1(Handle* h, void* XT, void* Y, cudaStream_t st) {
     a.p2_order = D->p2_order;
     if (D->idx16) { a.segs16 = D->segs16; a.p2_segptr16 = D->p2_segptr16; a.idx16 = D->idx16; a.seg_base16 = D->seg_base16; a.segc16 = D->segc16; }
     if (D->idx16 && D->k1_ovl) { a.p1done = D->tready + D->n_svd + 1; a.n_p1items = (int32_t)D->n_pp; }
+    a.t_l1 = D->k1_tl1;
     if (D->idx16 && VF_K1_PF && D->smq_ptr) {
         CK(cudaMemsetAsync(D->smq_ctr, 0, (size_t)(D->n_smq + 1) * 32, st));
         a.smq_ptr = D->smq_ptr; a.smq_rows = D->smq_rows; a.smq_pool = D->smq_pool; a.smq_ctr = D->smq_ctr;

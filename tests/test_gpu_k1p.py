@@ -121,7 +121,7 @@ def test_k1p_equals_row_kernel_on_product_build():
 @pytest.mark.parametrize("env", [{}, {"VF_P1_PART": "64"}, {"VF_U16_SPAN": "7"},
                                  {"VF_P1_PART": "32", "VF_U16_SPAN": "2"}, {"VF_K1_ILV": "0"},
                                  {"VF_K1_PACK": "1"}, {"VF_K1_OVL": "1"},
-                                 {"VF_K1_SMQ": "1"}, {"VF_K1_SMQ": "0"},
+                                 {"VF_K1_SMQ": "1"}, {"VF_K1_SMQ": "0"}, {"VF_K1_TL1": "0"}, {"VF_K1_TL1": "1"},
                                  {"VF_K1_SMQ": "1", "VF_K1_SMQ_NQ": "500", "VF_K1_SMQ_THR": "1e9"},
                                  {"VF_K1_SMQ": "1", "VF_K1_SMQ_NQ": "3", "VF_K1_SMQ_THR": "0.5"},
                                  {"VF_K1_SMQ": "1", "VF_K1_SMQ_THR": "1e9", "VF_K1_OVL": "1", "VF_P1_PART": "64"}])
@@ -135,7 +135,8 @@ def test_default_row_kernel_forced_layouts(env):
     queue count and pool; 500 queues with no pool, so most queues are only
     served by the end-of-kernel sweep; 3 queues with most rows in the pool, so
     most SMs own no queue; no pool with the barrier-free hand-over and
-    multi-part phase 1): <= 1e-12 / 1e-5 vs the oracle's Alg. 5 on the same
+    multi-part phase 1), T-row gathers through L2 only / through L1
+    (VF_K1_TL1): <= 1e-12 / 1e-5 vs the oracle's Alg. 5 on the same
     blocks, bitwise repeatable."""
     out = _run(env, kernel="rows")
     for name, d in out.items():
