@@ -627,6 +627,69 @@ __device__ __forceinline__ void k1_fetch(K1Round<T>& R, int cc, int ns, int tota
         R.f = 32;
     }
 }
+// The same fetch without warp shuffles (VF_K1_NOSHFL): shuffles run on the LSU
+// data pipe, where the 11 per round of k1_fetch (5 binary-search steps + 6
+// descriptor fields) were 21 of the pipe's 74 % on configs[2] (ncu, s32:
+// l1tex__data_pipe_lsu_wavefronts_mem_shared with no shared loads or stores).
+// Here the lane -> run mapping of a round comes from one warp OR-reduction
+// (redux.sync): every run that starts inside the round sets the bit of its
+// first lane, a lane's run is (runs started before the round) - 1 + (bits at or
+// below the lane), its first chunk the highest such bit (or the start carried
+// from earlier rounds), and the lane reads its run's 16-B descriptor from
+// global memory (mostly one address per warp, L1 hit: the batch's descriptors
+// were just loaded).  Needs non-empty runs (checked at upload).  Same lane ->
+// chunk mapping and loads as k1_fetch: bitwise equal sums.
+#ifndef VF_K1_NOSHFL
+#define VF_K1_NOSHFL 1
+#endif
+__device__ __forceinline__ int4 ld_desc(const SegC* p) {
+    int4 v;
+    asm volatile("ld.global.nc.L1::evict_first.v4.s32 {%0, %1, %2, %3}, [%4];\n"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+    return v;
+}
+struct K1Map {          // warp-uniform state of the round -> run mapping within one batch of <= 32 runs
+    int c;              // runs that start before the current round
+    int carry;          // first chunk of run c - 1
+};
+template <typename T>
+__device__ __forceinline__ void k1_fetch_d(K1Round<T>& R, int base, int ns, int total, int excl, K1Map& mp,
+                                           const SegC* __restrict__ batch, const T* __restrict__ vals,
+                                           const uint16_t* __restrict__ idx16, int64_t nx, int lane) {
+    constexpr unsigned FULL = 0xffffffffu;
+    const int p = excl - base;
+    const unsigned M = __reduce_or_sync(FULL, (lane < ns && p >= 0 && p < 32) ? (1u << p) : 0u);
+    const unsigned le = M & (FULL >> (31 - lane));
+    const int g = mp.c - 1 + __popc(le);
+    const int start = le ? base + 31 - __clz(le) : mp.carry;
+    mp.c += __popc(M);
+    if (M) mp.carry = base + 31 - __clz(M);
+    const int cc = base + lane;
+    if (cc < total) {
+        const int4 d = ld_desc(batch + g);
+        const int64_t g_off = (int64_t)(uint32_t)d.x;
+        const int64_t g_src = (int64_t)(uint32_t)d.y;
+        const int g_len = d.z & 0x7fffffff;
+        const int e = (cc - start) * 4;
+        const int nv = min(4, g_len - e);
+        V4<T>::ld(vals + g_off + e, R.w);
+        if (d.z < 0) {                                   // interleaved CSR piece: 4 slots, zero-padded
+            R.q = ld_stream_u2(reinterpret_cast<const uint2*>(idx16 + g_src + e));
+            R.xb = d.w;
+            R.f = 4 | 8 | 32;
+        } else {
+            R.q = make_uint2(0u, 0u);
+            R.xb = (int32_t)(g_src + e);
+            R.f = nv | (VF_XVEC && nv == 4 && ((g_src + e) & (16 / sizeof(T) - 1)) == 0 ? 16 : 0) | (g_src < nx ? 32 : 0);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) R.w[u] = T(0);
+        R.q = make_uint2(0u, 0u);
+        R.xb = 0;
+        R.f = 32;
+    }
+}
 template <typename T>
 __device__ __forceinline__ void k1_consume(const K1Round<T>& R, const T* xt, T& acc0, T& acc1, bool tl1) {
     const int nv = R.f & 7;
@@ -693,7 +756,11 @@ __device__ __forceinline__ T row_accumulate_k1_pf(const SegC* __restrict__ segc,
         const int ns = (int)(s1 - sb < 32 ? s1 - sb : 32);
         SegC my{0u, 0u, 0, 0};
         if (lane < ns) {
+#if VF_K1_NOSHFL
+            const int4 d = ld_desc(segc + sb + lane);
+#else
             const int4 d = ld_stream_i4(reinterpret_cast<const int4*>(segc + sb + lane));
+#endif
             my = SegC{(uint32_t)d.x, (uint32_t)d.y, d.z, d.w};
         }
         const int nch = ((my.lk & 0x7fffffff) + 3) >> 2;
@@ -724,16 +791,22 @@ __device__ __forceinline__ T row_accumulate_k1_pf(const SegC* __restrict__ segc,
         l2pf(0);
 #endif
         K1Round<T> cur;
-        k1_fetch<T>(cur, lane, ns, total, excl, my, vals, idx16, nx, lane);
+#if VF_K1_NOSHFL
+        K1Map mp{0, 0};
+#define K1_FETCH(R, base) k1_fetch_d<T>(R, base, ns, total, excl, mp, segc + sb, vals, idx16, nx, lane)
+#else
+#define K1_FETCH(R, base) k1_fetch<T>(R, (base) + lane, ns, total, excl, my, vals, idx16, nx, lane)
+#endif
+        K1_FETCH(cur, 0);
 #if VF_K1_PFD >= 2
         // two rounds in flight: rounds i + 1 and i + 2 are fetched before round i's gathers
         if (32 < total) {
             K1Round<T> nx1;
-            k1_fetch<T>(nx1, 32 + lane, ns, total, excl, my, vals, idx16, nx, lane);
+            K1_FETCH(nx1, 32);
             int base = 64;
             for (; base < total; base += 32) {
                 K1Round<T> nx2;
-                k1_fetch<T>(nx2, base + lane, ns, total, excl, my, vals, idx16, nx, lane);
+                K1_FETCH(nx2, base);
                 if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
                 k1_consume<T>(cur, xt, acc0, acc1, tl1);
                 cur = nx1;
@@ -750,13 +823,14 @@ __device__ __forceinline__ T row_accumulate_k1_pf(const SegC* __restrict__ segc,
 #if VF_K1_L2PF
             l2pf(base);
 #endif
-            k1_fetch<T>(nxt, base + lane, ns, total, excl, my, vals, idx16, nx, lane);
+            K1_FETCH(nxt, base);
             if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
             k1_consume<T>(cur, xt, acc0, acc1, tl1);
             cur = nxt;
         }
         if (!t_ready && __any_sync(FULL, (cur.f & 40) == 0)) { k1_wait_t(p1done, n_p1, lane); t_ready = true; }
         k1_consume<T>(cur, xt, acc0, acc1, tl1);
+#undef K1_FETCH
     }
     T acc = acc0 + acc1;
 #pragma unroll
@@ -4332,7 +4406,7 @@ int upload_impl(Handle* h, DeviceHMat* D) {
         for (size_t i = 0; i < s16.size(); ++i) {
             const Seg& sg = s16[i];
             if (sg.val_off < 0 || sg.val_off > (int64_t)UINT32_MAX || sg.src < 0 || sg.src > (int64_t)UINT32_MAX ||
-                sg.len < 0 || (sg.kind != 0 && sg.kind != 1)) { sc16.clear(); break; }
+                sg.len <= 0 || (sg.kind != 0 && sg.kind != 1)) { sc16.clear(); break; }   // (runs are non-empty: k1_fetch_d)
             sc16.push_back(SegC{(uint32_t)sg.val_off, (uint32_t)sg.src, (int32_t)((uint32_t)sg.len | ((uint32_t)sg.kind << 31)),
                                 base16[i]});
         }
