@@ -989,6 +989,9 @@ constexpr int kP1Unroll = VF_P1_UNROLL;
 // nrhs = 1 phase 1: V values streamed like the phase-2 runs (L1::no_allocate,
 // L2 evict-first: VF_P1_NA) and, where X is read-only for the launch (matvec,
 // ROWS step), x_j through L1 (VF_P1_L1); same loads, same FMA order
+#ifndef VF_P1_TRED
+#define VF_P1_TRED 1        // nrhs = 1 phase 1: transposed butterfly reduction (20 instead of 80 shuffles per pass)
+#endif
 #ifndef VF_P1_NA
 #define VF_P1_NA 1
 #endif
@@ -1041,12 +1044,37 @@ __device__ __forceinline__ void phase1_part_k1(const HotArgs& a, T* xc, int64_t 
 #pragma unroll
                 for (int r = 0; r < H; ++r) acc[r] = fma(v[r], x, acc[r]);
             }
+#if VF_P1_TRED
+            {
+                // the H = 8 butterfly sums on a quarter of the shuffles: at offsets 16, 8
+                // and 4 a lane keeps half of its rows and sends the other half to its
+                // partner (4 + 2 + 1 exchanges instead of 8 + 8 + 8), then offsets 2 and 1
+                // on the one row left; every kept sum is the same a + b of the same two
+                // operands as in the full butterfly (bitwise equal), row r ends in lanes
+                // 4 r .. 4 r + 3.  (Shuffles run on the LSU data pipe, which bounds this
+                // kernel: 160 of them per group were more than its loads.)
+                static_assert(H == 8, "transposed reduction is written for 8 rows per pass");
+                constexpr unsigned FULL = 0xffffffffu;
+                const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+                T s4[4], s2[2];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) s4[i] = (b4 ? acc[4 + i] : acc[i]) + __shfl_xor_sync(FULL, b4 ? acc[i] : acc[4 + i], 16);
+#pragma unroll
+                for (int i = 0; i < 2; ++i) s2[i] = (b3 ? s4[2 + i] : s4[i]) + __shfl_xor_sync(FULL, b3 ? s4[i] : s4[2 + i], 8);
+                T s1 = (b2 ? s2[1] : s2[0]) + __shfl_xor_sync(FULL, b2 ? s2[0] : s2[1], 4);
+                s1 += __shfl_xor_sync(FULL, s1, 2);
+                s1 += __shfl_xor_sync(FULL, s1, 1);
+                const T v = __shfl_sync(FULL, s1, ((lane - h0) * 4) & 31);
+                if (lane >= h0 && lane < h0 + H) mine = (double)v;
+            }
+#else
 #pragma unroll
             for (int r = 0; r < H; ++r) {
 #pragma unroll
                 for (int off = 16; off > 0; off >>= 1) acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], off);
                 if (lane == h0 + r) mine = (double)acc[r];
             }
+#endif
         }
         bool finish = np == 1;
         if (!finish) {                                // publish this part; the last one combines
