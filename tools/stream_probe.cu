@@ -1,0 +1,141 @@
+// Dev tool: what HBM rate does the nrhs = 1 row kernel's ACCESS PATTERN allow?
+// A model of phase 2 of hot_kernel<T,1,1> without its arithmetic: 4 CTAs of 8
+// warps per SM, rows from an atomic queue, a warp streams a row in rounds of
+// 32 lanes x (32 B of values + 8 B of 16-bit offsets), D rounds in flight per
+// warp (registers), optionally followed by 4 dependent 8-B gathers per lane from
+// a 1 MB vector (the x gathers).  Prints GB/s of the value + offset stream for
+// D = 1..4, with / without gathers, rows in random (LPT-like) or memory order.
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/stream_probe tools/stream_probe.cu
+#include <cstdio>
+#include <cstdlib>
+#include <cstdint>
+#include <vector>
+#include <algorithm>
+#include <random>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e_), __LINE__); exit(1); } } while (0)
+
+__device__ __forceinline__ double2 ld_na(const double2* p) {
+    double2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];\n" : "=d"(v.x), "=d"(v.y) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ uint2 ld_na_u2(const uint2* p) {
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];\n" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+}
+
+struct Slot { double2 a, b; uint2 q; };
+
+template <int D, bool GATHER>
+__global__ void __launch_bounds__(256, 4) probe(const double* __restrict__ vals, const uint2* __restrict__ idx,
+                                                const int* __restrict__ order, int nrows, int rounds, int* ctr,
+                                                const double* __restrict__ x, int xmask, double* out) {
+    const int lane = threadIdx.x & 31;
+    int t = 0;
+    if (lane == 0) t = atomicAdd(ctr, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    double acc0 = 0.0, acc1 = 0.0;
+    while (t < nrows) {
+        const int r = order[t];
+        int fut = 0;
+        if (lane == 0) fut = atomicAdd(ctr, 1);
+        const double2* v = reinterpret_cast<const double2*>(vals + (size_t)r * rounds * 128) + lane * 2;
+        const uint2* q = idx + (size_t)r * rounds * 32 + lane;
+        const int xb = (r * 61) & xmask;
+        Slot s[D];
+#pragma unroll
+        for (int d = 0; d < D; ++d)
+            if (d < rounds) { s[d].a = ld_na(v + d * 64); s[d].b = ld_na(v + d * 64 + 1); s[d].q = ld_na_u2(q + d * 32); }
+        for (int i = 0; i < rounds; i += D) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                if (i + d < rounds) {
+                    double x0 = 1.0, x1 = 1.0, x2 = 1.0, x3 = 1.0;
+                    if (GATHER) {
+                        x0 = x[(xb + (s[d].q.x & 0xffffu)) & xmask]; x1 = x[(xb + (s[d].q.x >> 16)) & xmask];
+                        x2 = x[(xb + (s[d].q.y & 0xffffu)) & xmask]; x3 = x[(xb + (s[d].q.y >> 16)) & xmask];
+                    } else {
+                        x0 = (double)(s[d].q.x & 1u); x2 = (double)(s[d].q.y & 1u);
+                    }
+                    acc0 = fma(s[d].a.x, x0, acc0); acc1 = fma(s[d].a.y, x1, acc1);
+                    acc0 = fma(s[d].b.x, x2, acc0); acc1 = fma(s[d].b.y, x3, acc1);
+                    const int n = i + d + D;
+                    if (n < rounds) { s[d].a = ld_na(v + n * 64); s[d].b = ld_na(v + n * 64 + 1); s[d].q = ld_na_u2(q + n * 32); }
+                }
+            }
+        }
+        t = __shfl_sync(0xffffffffu, fut, 0);
+    }
+    acc0 += acc1;
+    for (int off = 16; off > 0; off >>= 1) acc0 += __shfl_xor_sync(0xffffffffu, acc0, off);
+    if (lane == 0 && acc0 == 12345.678) out[0] = acc0;
+}
+
+__global__ void fill_idx(uint32_t* p, size_t n, uint32_t span) {
+    for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+        uint32_t h = (uint32_t)i * 2654435761u;
+        h ^= h >> 15;
+        // sorted-ish near-field offsets: lane-consecutive columns with small jitter
+        const uint32_t lane = (uint32_t)((i >> 1) & 31), half = (uint32_t)(i & 1);
+        const uint32_t lo = (lane * 3 + half * 96 + (h & 1)) % span, hi = (lane * 3 + half * 96 + 192 + ((h >> 1) & 1)) % span;
+        p[i] = lo | (hi << 16);
+    }
+}
+
+template <int D, bool G>
+float run(const double* vals, const uint2* idx, const int* order, int nrows, int rounds, int* ctr, const double* x, int xmask,
+          double* out, int nsm) {
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0)); CK(cudaEventCreate(&e1));
+    float best = 1e30f;
+    for (int rep = 0; rep < 6; ++rep) {
+        CK(cudaMemsetAsync(ctr, 0, 4));
+        CK(cudaEventRecord(e0));
+        probe<D, G><<<nsm * 4, 256>>>(vals, idx, order, nrows, rounds, ctr, x, xmask, out);
+        CK(cudaEventRecord(e1));
+        CK(cudaEventSynchronize(e1));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        if (rep >= 2) best = std::min(best, ms);
+    }
+    CK(cudaGetLastError());
+    return best;
+}
+
+int main(int argc, char** argv) {
+    const int nrows = argc > 1 ? atoi(argv[1]) : 131072, rounds = argc > 2 ? atoi(argv[2]) : 19;
+    int nsm = 148;
+    CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0));
+    const size_t nv = (size_t)nrows * rounds * 128, nq = (size_t)nrows * rounds * 32;
+    double *vals, *x, *out;
+    uint2* idx;
+    int *order, *ctr;
+    CK(cudaMalloc(&vals, nv * 8 + 4096)); CK(cudaMalloc(&idx, nq * 8 + 4096)); CK(cudaMalloc(&x, 131072 * 8));
+    CK(cudaMalloc(&out, 8)); CK(cudaMalloc(&order, nrows * 4)); CK(cudaMalloc(&ctr, 4));
+    CK(cudaMemset(vals, 0, nv * 8 + 4096)); CK(cudaMemset(x, 0, 131072 * 8));
+    fill_idx<<<nsm * 8, 256>>>(reinterpret_cast<uint32_t*>(idx), nq * 2, 2048u);
+    CK(cudaDeviceSynchronize());
+    const double gb = (double)(nv * 8 + nq * 8) / 1e9;
+    printf("rows %d x %d rounds of 1280 B: %.3f GB streamed per launch, grid %d x 256\n", nrows, rounds, gb, nsm * 4);
+    for (int rnd = 0; rnd < 2; ++rnd) {
+        std::vector<int> o(nrows);
+        for (int i = 0; i < nrows; ++i) o[i] = i;
+        if (rnd) { std::mt19937 g(1); std::shuffle(o.begin(), o.end(), g); }
+        CK(cudaMemcpy(order, o.data(), nrows * 4, cudaMemcpyHostToDevice));
+        float ms[8];
+        ms[0] = run<1, false>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+        ms[1] = run<2, false>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+        ms[2] = run<3, false>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+        ms[3] = run<4, false>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+        ms[4] = run<1, true>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+        ms[5] = run<2, true>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+        ms[6] = run<3, true>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+        ms[7] = run<4, true>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+        for (int k = 0; k < 8; ++k)
+            printf("order %s  D %d  gathers %d : %.3f ms  %.0f GB/s\n", rnd ? "random" : "memory", k % 4 + 1, k / 4, ms[k], gb / ms[k] * 1e3);
+    }
+    return 0;
+}
