@@ -29,7 +29,9 @@ __device__ __forceinline__ uint2 ld_na_u2(const uint2* p) {
 
 struct Slot { double2 a, b; uint2 q; };
 
-template <int D, bool GATHER>
+// PAD: extra integer instructions per lane and round (two dependent chains), a
+// stand-in for the row kernel's per-round bookkeeping (~200 instructions)
+template <int D, bool GATHER, int PAD = 0>
 __global__ void __launch_bounds__(256, 4) probe(const double* __restrict__ vals, const uint2* __restrict__ idx,
                                                 const int* __restrict__ order, int nrows, int rounds, int* ctr,
                                                 const double* __restrict__ x, int xmask, double* out) {
@@ -38,6 +40,7 @@ __global__ void __launch_bounds__(256, 4) probe(const double* __restrict__ vals,
     if (lane == 0) t = atomicAdd(ctr, 1);
     t = __shfl_sync(0xffffffffu, t, 0);
     double acc0 = 0.0, acc1 = 0.0;
+    unsigned j0 = lane, j1 = lane * 3u;
     while (t < nrows) {
         const int r = order[t];
         int fut = 0;
@@ -62,6 +65,11 @@ __global__ void __launch_bounds__(256, 4) probe(const double* __restrict__ vals,
                     }
                     acc0 = fma(s[d].a.x, x0, acc0); acc1 = fma(s[d].a.y, x1, acc1);
                     acc0 = fma(s[d].b.x, x2, acc0); acc1 = fma(s[d].b.y, x3, acc1);
+#pragma unroll
+                    for (int p = 0; p < PAD / 2; ++p) {
+                        asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(j0) : "r"(s[d].q.x), "r"(p));
+                        asm volatile("lop3.b32 %0, %0, %1, %2, 0x96;" : "+r"(j1) : "r"(s[d].q.y), "r"(p));
+                    }
                     const int n = i + d + D;
                     if (n < rounds) { s[d].a = ld_na(v + n * 64); s[d].b = ld_na(v + n * 64 + 1); s[d].q = ld_na_u2(q + n * 32); }
                 }
@@ -71,7 +79,7 @@ __global__ void __launch_bounds__(256, 4) probe(const double* __restrict__ vals,
     }
     acc0 += acc1;
     for (int off = 16; off > 0; off >>= 1) acc0 += __shfl_xor_sync(0xffffffffu, acc0, off);
-    if (lane == 0 && acc0 == 12345.678) out[0] = acc0;
+    if (lane == 0 && (acc0 == 12345.678 || (j0 ^ j1) == 0x9e3779b9u)) out[0] = acc0;
 }
 
 __global__ void fill_idx(uint32_t* p, size_t n, uint32_t span) {
@@ -85,7 +93,7 @@ __global__ void fill_idx(uint32_t* p, size_t n, uint32_t span) {
     }
 }
 
-template <int D, bool G>
+template <int D, bool G, int PAD = 0>
 float run(const double* vals, const uint2* idx, const int* order, int nrows, int rounds, int* ctr, const double* x, int xmask,
           double* out, int nsm) {
     cudaEvent_t e0, e1;
@@ -94,7 +102,7 @@ float run(const double* vals, const uint2* idx, const int* order, int nrows, int
     for (int rep = 0; rep < 6; ++rep) {
         CK(cudaMemsetAsync(ctr, 0, 4));
         CK(cudaEventRecord(e0));
-        probe<D, G><<<nsm * 4, 256>>>(vals, idx, order, nrows, rounds, ctr, x, xmask, out);
+        probe<D, G, PAD><<<nsm * 4, 256>>>(vals, idx, order, nrows, rounds, ctr, x, xmask, out);
         CK(cudaEventRecord(e1));
         CK(cudaEventSynchronize(e1));
         float ms;
@@ -136,6 +144,18 @@ int main(int argc, char** argv) {
         ms[7] = run<4, true>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
         for (int k = 0; k < 8; ++k)
             printf("order %s  D %d  gathers %d : %.3f ms  %.0f GB/s\n", rnd ? "random" : "memory", k % 4 + 1, k / 4, ms[k], gb / ms[k] * 1e3);
+        if (rnd) {
+            float mp[6];
+            mp[0] = run<1, true, 40>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+            mp[1] = run<1, true, 80>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+            mp[2] = run<1, true, 120>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+            mp[3] = run<1, true, 160>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+            mp[4] = run<1, true, 200>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+            mp[5] = run<1, true, 280>(vals, idx, order, nrows, rounds, ctr, x, 131071, out, nsm);
+            const int pad[6] = {40, 80, 120, 160, 200, 280};
+            for (int k = 0; k < 6; ++k)
+                printf("order random  D 1  gathers 1  + %d instructions per round : %.3f ms  %.0f GB/s\n", pad[k], mp[k], gb / mp[k] * 1e3);
+        }
     }
     return 0;
 }
